@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""Benchmark of the lv_search hot path (BASELINE.json metric) — one JSON line on rank 0.
+
+A step = one lv_search call over the config's whole query batch (m = 10 000): K1 projection,
+K2/K3 fused reduced scoring + top-R, K4/K5 select + full-D re-rank + top-k.  Inputs are
+resident in HBM; X_low (256 MB) and X (2 GB) exceed the 126 MB L2, so the scan streams from
+HBM every step (no explicit flush).  Default workload: configs[1] (cfg 2, LeanVec-Sphering
+1M x 512, d=128, R=100, k=10).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl lv|reference]
+
+N > 1 (torchrun): query-sharded replicas — each rank holds the full index and searches its own
+m-query batch (weak scaling, no data-path collective).  `--impl reference` times
+the CPU oracle (the only reference this paper has) on a bounded query sample per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "queries/s and % roofline for reduced-dim scoring+top-R+rerank, 10-recall@10"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return {"hbm": j["hbm_gbs"], "bf16": j["bf16_tflops"], "bf16_sus": j.get("bf16_tflops_sustained"),
+                "src": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (clocks line of B200_PROFILING.md)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_index(cfg, dev_rank=0, log=print):
+    """Generate the config's data, fit with the product path (lv_fit_stats + host eig, GPU k-means
+    for GleanVec), encode.  Returns dict with index, device Q, host Q, data."""
+    import torch
+    import lvgen
+    from paper_2410_22347_b200 import fit, lv
+    t0 = time.time()
+    X = lvgen.database(cfg)
+    Q = lvgen.queries(cfg, "test")
+    Ql = lvgen.queries(cfg, "learn")
+    lr = lvgen.learn_rows(cfg)
+    log(f"[bench] generated n={cfg.n} D={cfg.D} in {time.time() - t0:.1f}s")
+    t0 = time.time()
+    Xd = torch.from_numpy(X).cuda()
+    Qld = torch.from_numpy(Ql).cuda()
+    Xl = Xd[torch.from_numpy(lr).cuda()]
+    if cfg.C == 1:
+        f = fit.leanvec_sphering_fit(Qld, Xl, cfg.d)
+        assign = None
+    else:
+        f = fit.gleanvec_fit(Qld, Xl, cfg.C, cfg.d, lvgen.kmeanspp_draws(cfg))
+        assign = lv.lv_assign_tags(Xd, torch.as_tensor(f["centres"], dtype=torch.float32, device="cuda"))
+    torch.cuda.synchronize()
+    t_fit = time.time() - t0
+    ix = lv.lv_index_create(cfg.D, cfg.d, cfg.C, cfg.low_dtype, cfg.full_dtype,
+                            torch.as_tensor(f["A"], dtype=torch.float32), torch.as_tensor(f["B"], dtype=torch.float32))
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    lv.lv_encode_database(ix, Xd, assign)
+    ev1.record()
+    torch.cuda.synchronize()
+    t_enc = ev0.elapsed_time(ev1)
+    log(f"[bench] fit {t_fit:.1f}s encode {t_enc:.1f}ms")
+    Qd = torch.from_numpy(Q).cuda()
+    del Xd, Xl, Qld
+    return {"ix": ix, "Q": Q, "Qd": Qd, "X": X, "A": f["A"], "B": f["B"], "assign": assign,
+            "fit_s": t_fit, "encode_ms": t_enc, "gaps": f.get("gaps")}
+
+
+def roofline_scan(cfg, ms):
+    pk = _peaks()
+    flops = 2.0 * cfg.m_test * cfg.n * cfg.d
+    ach = flops / (ms * 1e-3) / 1e12
+    return {"bound": "tensor", "achieved": round(ach, 1), "peak": pk["bf16"], "unit": "TFLOP/s",
+            "frac": round(ach / pk["bf16"], 4), "frac_of_sustained": round(ach / pk["bf16_sus"], 4) if pk["bf16_sus"] else None,
+            "peak_source": pk["src"], "kernel": "k_score_topr (K2/K3 fused scan)",
+            "algorithmic": f"2*m*n*d = {flops:.3e} flop per launch", "traffic": _ncu_traffic()}
+
+
+def roofline_rerank(cfg, ms):
+    pk = _peaks()
+    b = 4 if cfg.full_dtype == "fp32" else 2
+    byts = cfg.m_test * cfg.R * cfg.D * b + cfg.m_test * cfg.D * 4 + cfg.m_test * cfg.R * 8 + cfg.m_test * cfg.k * 8
+    ach = byts / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s", "frac": round(ach / pk["hbm"], 4),
+            "algorithmic": f"{byts:.3e} B per launch"}
+
+
+def _ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("k_score_topr_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def cpu_baseline(cfg, data, nq, log=print):
+    """The fp64 oracle (as it stands) on a bounded sample of the same workload."""
+    import oracle as O
+    ncores = len(os.sched_getaffinity(0))
+    A, B = data["A"], data["B"]
+    assign = None if data["assign"] is None else data["assign"].cpu().numpy()
+    X = data["X"]
+    t0 = time.time()
+    X_low = O.encode(X, B, assign, store=cfg.low_dtype)
+    t_enc = time.time() - t0
+    Qs = data["Q"][:nq]
+    t0 = time.time()
+    Qp = O.project(Qs, A, store=cfg.low_dtype)
+    cand, _ = O.reduced_search(Qp, X_low, assign, cfg.R)
+    ids, _ = O.rerank_topk(Qs, X, cand, cfg.k)
+    dt = time.time() - t0
+    log(f"[bench] oracle: {nq} queries in {dt:.1f}s (encode {t_enc:.1f}s, untimed)")
+    return {"value": round(nq / dt, 3), "unit": "queries/s", "cores": ncores, "kind": "oracle",
+            "sample": f"{nq} of {cfg.m_test} queries, full n={cfg.n} database (project + exhaustive reduced top-R + "
+                      f"re-rank + top-k, fp64 numpy/OpenBLAS); X_low encode untimed"}, ids, X_low
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="lv", choices=["lv", "reference"])
+    ap.add_argument("--oracle-queries", type=int, default=200)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
+
+    import lvgen
+    cfg = lvgen.get_config(args.config)
+    workload = f"cfg{cfg.cfg_id} {cfg.name}"
+    conf = {"workload": workload, "n": cfg.n, "D": cfg.D, "d": cfg.d, "C": cfg.C, "m": cfg.m_test, "R": cfg.R,
+            "k": cfg.k, "low_dtype": cfg.low_dtype, "full_dtype": cfg.full_dtype,
+            "l2": "no flush: X_low and X exceed the 126 MB L2 and are streamed every step"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        import oracle as O
+        X = lvgen.database(cfg)
+        Q = lvgen.queries(cfg, "test")
+        Ql = lvgen.queries(cfg, "learn")
+        Xl = X[lvgen.learn_rows(cfg)]
+        if cfg.C == 1:
+            f = O.sphering_fit(Ql, Xl, cfg.d)
+            A, B, assign = f["A"], f["B"], None
+        else:
+            g = O.gleanvec_fit(Ql, Xl, cfg.C, cfg.d, lvgen.kmeanspp_draws(cfg))
+            A, B = g["A"], g["B"]
+            assign = O.assign_tags(X, g["centres"])
+        X_low = O.encode(X, B, assign, store=cfg.low_dtype)
+        per = max(1, args.oracle_queries // 4)
+        def step(i):
+            lo = (i * per) % cfg.m_test
+            Qs = Q[lo:lo + per]
+            Qp = O.project(Qs, A, store=cfg.low_dtype)
+            cand, _ = O.reduced_search(Qp, X_low, assign, cfg.R)
+            O.rerank_topk(Qs, X, cand, cfg.k)
+        for i in range(args.warmup):
+            step(i)
+        t0 = time.time()
+        for i in range(args.steps):
+            step(args.warmup + i)
+        dt = time.time() - t0
+        v = per * args.steps / dt
+        ncores = len(os.sched_getaffinity(0))
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "queries/s",
+                          "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": round(1e3 * dt / args.steps, 3), "higher_is_better": True,
+                          "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                          "config": dict(conf, reference_step=f"{per} queries per step (bounded sample)"),
+                          "cpu_baseline": {"value": round(v, 3), "unit": "queries/s", "cores": ncores, "kind": "oracle",
+                                           "sample": f"{per} queries per step x {args.steps} steps, full database"},
+                          "e2e": {"value": round(v, 3), "unit": "queries/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
+
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    from paper_2410_22347_b200 import lv
+
+    data = build_index(cfg, log=log)
+    ix, Qd = data["ix"], data["Qd"]
+    m = Qd.shape[0]
+    ids = torch.empty((m, cfg.k), dtype=torch.int32, device="cuda")
+    sc = torch.empty((m, cfg.k), dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        lv.lv_search(ix, Qd, cfg.k, cfg.R, out=(ids, sc))
+    torch.cuda.synchronize()
+    launches_per_step = lv.lv_search(ix, Qd, cfg.k, cfg.R, out=(ids, sc))[2]["launches"]
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(args.steps):
+            lv.lv_search(ix, Qd, cfg.k, cfg.R, out=(ids, sc))
+        e1.record(st)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * m * args.steps / (ms * 1e-3)
+
+    # per-phase device times (separate, synchronising runs; CUDA events on the launch stream)
+    ph = []
+    for _ in range(max(3, min(args.steps, 10))):
+        ph.append(lv.lv_search(ix, Qd, cfg.k, cfg.R, out=(ids, sc), timing=True)[2]["phase_ms"])
+    ph = np.median(np.array(ph), axis=0)
+
+    # e2e: public API with HOST buffers (pinned), H2D of Q and D2H of results inside the region
+    Qh = torch.from_numpy(data["Q"]).pin_memory()
+    ih = torch.empty((m, cfg.k), dtype=torch.int32).pin_memory()
+    sh = torch.empty((m, cfg.k), dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        lv.lv_search_host(ix, Qh, cfg.k, cfg.R, ih, sh)
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(args.steps):
+        lv.lv_search_host(ix, Qh, cfg.k, cfg.R, ih, sh)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+        barrier()
+    if rank != 0:
+        torch.distributed.destroy_process_group()
+        return
+
+    out = {"metric": METRIC, "value": round(value, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": cfg.low_dtype, "data": "synthetic",
+           "config": dict(conf, parallelism=f"query-sharded replicas x{world}" if world > 1 else "single GPU"),
+           "phases_ms": {"project_K1": round(float(ph[0]), 4), "scan_K2K3": round(float(ph[1]), 4),
+                         "select_rerank_K4K5": round(float(ph[2]), 4), "total": round(float(ph[3]), 4)},
+           "roofline": roofline_scan(cfg, float(ph[1])),
+           "roofline_rerank": roofline_rerank(cfg, float(ph[2])),
+           "e2e": {"value": round(world * m * args.steps / (ms_e2e * 1e-3), 1), "unit": "queries/s",
+                   "h2d_bytes_per_step": int(m * cfg.D * 4), "d2h_bytes_per_step": int(m * cfg.k * 8)},
+           "gpu_launches": int(launches_per_step * args.steps),
+           "clocks": clk.summary(),
+           "index_build": {"fit_s": round(data["fit_s"], 2), "encode_ms": round(data["encode_ms"], 2)}}
+    if world == 1 and not args.no_cpu_baseline:
+        import oracle as O
+        nq = min(args.oracle_queries, m)
+        cb, ora_ids, _ = cpu_baseline(cfg, data, nq, log=log)
+        out["cpu_baseline"] = cb
+        gt, _ = O.exact_topk(data["Q"][:nq], data["X"], 10)
+        gi = ids[:nq].cpu().numpy().astype(np.int64)
+        out["recall_at_10"] = {"gpu": round(O.recall_at_k(gi, gt, 10), 4),
+                               "oracle_emulated": round(O.recall_at_k(ora_ids, gt, 10), 4),
+                               "sample_queries": nq, "ids_equal_frac": float((gi == ora_ids).all(axis=1).mean())}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,180 @@
+/*
+ * lv.h — C ABI of the B200 (sm_100a) reduced-dimension MIPS hot path of
+ * LeanVec-Sphering and GleanVec (arXiv 2410.22347).
+ *
+ * Citations: P:n = PAPER.md line n (read-only paper text), S:n = SPEC.md line n.
+ *
+ * The method (Alg. 1): preprocess q' = f(q), main search for
+ * kappa = R candidates in the reduced space X_low, re-rank those with
+ * full-D inner products and return the top-k.  LeanVec-Sphering uses
+ * f(q) = A q, g(x) = B x (Eq.(5)) with A = P W^-1, B = P W (Alg. 2,
+ * P:215-238).  GleanVec uses one pair (A_c, B_c) per cluster c, tags
+ * c_i = argmax_c <x_i, mu_c> (Eq.(13)), x_low_i = B_{c_i} x_i (Eq.(14)
+ * read with g, P:337-343 vs P:347-348) and the eager query views q_c = A_c q
+ * (Alg. 4).  Here the main search is an exhaustive tensor-core scan
+ * of X_low with a fused per-query top-R; results are exact under
+ * the total order (score desc, original id asc).
+ *
+ * Conventions for every call
+ *  - Pointers are DEVICE pointers unless the argument says HOST.  The caller owns
+ *    every pointer it passes; nothing is freed by the library.
+ *  - Matrices are row-major, contiguous, 16-byte aligned.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Work is enqueued
+ *    in stream order; no call synchronises the device unless documented
+ *    (lv_fit_stats, lv_encode_database, *_host variants, debug timing).
+ *  - Every call returns lv_status; nothing throws or aborts across the ABI.
+ *    lv_last_error() returns a thread-local description of the last non-OK status.
+ *    Asynchronous kernel faults surface at the caller's next synchronisation.
+ *  - There is no CPU fallback: if the device is not an sm_100 GPU every compute
+ *    call returns LV_EUNSUPPORTED.
+ */
+#ifndef LV_H_
+#define LV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LV_OK = 0,
+    LV_EINVAL = 2,        /* usage: bad argument, shape or alignment (S:552 usage class) */
+    LV_EDATA = 3,         /* data: e.g. assign value outside [0, C) (S:552 data class)   */
+    LV_ENUMERIC = 4,      /* numeric; reserved: singular W is detected by the host fit */
+    LV_ECUDA = 5,         /* a CUDA runtime/driver call or kernel launch failed           */
+    LV_ENOMEM = 6,        /* device allocation failed                                      */
+    LV_EUNSUPPORTED = 7   /* no sm_100 device, or a shape the kernels do not support      */
+} lv_status;
+
+typedef enum { LV_F32 = 0, LV_F16 = 1, LV_BF16 = 2 } lv_dtype;
+
+typedef struct lv_index lv_index;   /* opaque, owned by the library */
+
+/* Optional outputs of lv_search (pass NULL to skip). */
+typedef struct {
+    int32_t* cand_ids;     /* device [m, R] or NULL: N_low(j), original ids, sorted by
+                              (reduced score desc, id asc)                                   */
+    float*   cand_scores;  /* device [m, R] or NULL: their reduced scores <q'_{c_i}, x_low_i>  */
+    float*   raw_scores;   /* device [m_pad, n_pad] or NULL: EVERY reduced score, in sorted
+                              (padded) database order; tiny shapes only (kernel self-test)   */
+    int32_t  timing;       /* nonzero: fill phase_ms (synchronises the stream)               */
+    float    phase_ms[4];  /* [0] project (K1), [1] score+top-R (K2/K3), [2] select+re-rank
+                              (K4/K5), [3] whole call                                       */
+    int32_t  launches;     /* number of kernels this call launched                          */
+    int32_t  slots;        /* per-query candidate lists kept by the scan       */
+    int32_t  units;        /* (query pair, database chunk) work units of the scan            */
+    int32_t  grid;         /* CTAs of the scan                                               */
+} lv_search_debug;
+
+/* Human-readable message for the last non-OK status on this thread. */
+const char* lv_last_error(void);
+
+/* Library build string (compile target, version). */
+const char* lv_version(void);
+
+/*
+ * lv_fit_stats — second-moment statistics of §3.2:
+ *   K_Q = sum_{q in Q_learn} q q^T  and, per cluster c, K_X[c] = sum_{x in X_c} x x^T.
+ * They replace the two SVDs of Alg. 2 by eigendecompositions of K_Q
+ * and W K_X W; the host fit (paper_2410_22347_b200/fit.py) does those.
+ *   Q_learn      device fp32 [m_learn, D]
+ *   X_learn      device [n_learn, D], x_dtype LV_F32 or LV_F16
+ *   assign_learn device int32 [n_learn] cluster of each learning row, or NULL (then C must be 1)
+ *   K_Q          HOST fp64 [D, D] out;  K_X  HOST fp64 [C, D, D] out
+ * Products are fp32 FMA over chunks of <= 8192 rows, chunk partials summed in fp64
+ * in a fixed order (deterministic).  Synchronises `stream` before returning.
+ * Errors: LV_EINVAL (sizes <= 0, C < 1, NULL outputs), LV_EDATA (assign out of range).
+ */
+lv_status lv_fit_stats(const float* Q_learn, int64_t m_learn,
+                       const void* X_learn, lv_dtype x_dtype, int64_t n_learn,
+                       int32_t D, const int32_t* assign_learn, int32_t C,
+                       double* K_Q, double* K_X, void* stream);
+
+/*
+ * lv_index_create — an empty index for dimension D, reduced dimension d and C clusters.
+ *   A_stack, B_stack  device fp32 [C, d, D]: A_c (query side, f_c(q) = A_c q) and
+ *                     B_c (database side, g_c(x) = B_c x); copied.
+ *   low_dtype         LV_BF16 or LV_F16: storage of x_low and q' (P:129 reduced footprint)
+ *   full_dtype        LV_F32 or LV_F16: storage of the full vectors used by the re-rank
+ * Constraints: 1 <= d <= D, d % 32 == 0, d <= 256, D % 4 == 0 (LV_F32) / D % 8 == 0 (LV_F16),
+ *              1 <= C <= 1024.  Errors: LV_EINVAL, LV_ENOMEM, LV_EUNSUPPORTED.
+ */
+lv_status lv_index_create(lv_index** out, int32_t D, int32_t d, int32_t C,
+                          lv_dtype low_dtype, lv_dtype full_dtype,
+                          const float* A_stack, const float* B_stack);
+
+/*
+ * lv_encode_database — builds X_low (Eq.(14): x_low_i = B_{c_i} x_i) and the
+ * full-precision copy used by the re-rank.
+ *   X       device [n, D] in x_dtype (LV_F32 or LV_F16), original id order
+ *   assign  device int32 [n] tags c_i (Eq.(13)), or NULL when C == 1
+ * Layout: rows are stably sorted by cluster (counting sort), each
+ * cluster segment is padded to a multiple of 128 rows, so every 128-row tile of X_low
+ * belongs to one cluster; perm maps sorted position -> original id (-1 = padding).
+ * x_low = RNE(fp32 FMA product) to low_dtype.  X is converted to full_dtype.
+ * The caller may free X after the call returns (the call synchronises `stream`).
+ * Replaces any previous contents.  Errors: LV_EINVAL, LV_EDATA, LV_ENOMEM, LV_ECUDA.
+ */
+lv_status lv_encode_database(lv_index* index, const void* X, lv_dtype x_dtype, int64_t n,
+                             const int32_t* assign, void* stream);
+
+/*
+ * lv_project_queries — Alg. 1 line 1 / Alg. 4 preprocess:
+ *   Qp[j, c*d:(c+1)*d] = RNE(A_c q_j) to low_dtype, fp32 FMA accumulation.
+ *   Q   device fp32 [m, D];  Qp device low_dtype [m, C*d]
+ */
+lv_status lv_project_queries(const lv_index* index, const float* Q, int64_t m, void* Qp,
+                             void* stream);
+
+/*
+ * lv_search — the hot path, Alg. 1 with an exhaustive main step:
+ *   1. q'_{j,c} = A_c q_j for all c (K1, projection);
+ *   2. s_ji = <q'_{j,c_i}, x_low_i> for ALL i on tensor cores (Eq.(15)); per query the R
+ *      best under (s desc, original id asc) are kept by a fused top-R (K2/K3); the m x n
+ *      score matrix never reaches HBM;
+ *   3. r_ji = <q_j, x_i> in fp32 on the full vectors for the R candidates (K5);
+ *   4. top-k by (r desc, id asc).
+ *   Q       device fp32 [m, D]
+ *   ids     device int32 [m, k] out (original database ids);  scores device fp32 [m, k] out (r_ji)
+ *   dbg     NULL or lv_search_debug* (HOST struct; its pointers are device pointers)
+ * Constraints: 1 <= k <= R <= n, R <= 512, m >= 1.  The index must be encoded.
+ * Not thread-safe per index (shared workspace).  Errors: LV_EINVAL, LV_ENOMEM, LV_ECUDA.
+ */
+lv_status lv_search(lv_index* index, const float* Q, int64_t m, int32_t k, int32_t R,
+                    int32_t* ids, float* scores, lv_search_debug* dbg, void* stream);
+
+/*
+ * lv_search_host — lv_search with HOST buffers: copies Q_host (fp32 [m, D]) to the device,
+ * runs lv_search, copies ids/scores back into HOST arrays [m, k].  Synchronises `stream`.
+ * Pinned host memory gives full PCIe bandwidth; pageable memory works.
+ */
+lv_status lv_search_host(lv_index* index, const float* Q_host, int64_t m, int32_t k, int32_t R,
+                         int32_t* ids_host, float* scores_host, void* stream);
+
+/*
+ * lv_assign_tags — Eq.(13): assign[i] = argmax_c <x_i, mu_c>, fp32 dot products,
+ * lowest c on ties.  X device [n, D] (x_dtype F32/F16); centres device fp32 [C, D].
+ */
+lv_status lv_assign_tags(const void* X, lv_dtype x_dtype, int64_t n, int32_t D,
+                         const float* centres, int32_t C, int32_t* assign, void* stream);
+
+/* Sizes of the encoded index (HOST out pointers, any may be NULL). */
+lv_status lv_index_info(const lv_index* index, int64_t* n, int64_t* n_pad, int32_t* D,
+                        int32_t* d, int32_t* C);
+
+/*
+ * lv_index_export — test/debug copies of the encoded layout:
+ *   X_low   device low_dtype [n_pad, d] or NULL;  perm device int32 [n_pad] or NULL;
+ *   offsets HOST int64 [C+1] or NULL (padded segment starts).  Synchronises `stream`.
+ */
+lv_status lv_index_export(const lv_index* index, void* X_low, int32_t* perm, int64_t* offsets,
+                          void* stream);
+
+/* Frees every device allocation of the index.  NULL is a no-op. */
+void lv_index_destroy(lv_index* index);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LV_H_ */

@@ -1,0 +1,613 @@
+// C ABI of include/lv.h: argument checking, index memory, work planning and kernel sequencing.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "lv_common.cuh"
+#include "lv_internal.h"
+
+namespace lv {
+size_t score_smem_bytes(int d, int stages);
+}
+
+struct lv_index {
+  int32_t D = 0, d = 0, C = 0;
+  lv_dtype low = LV_BF16, full = LV_F32;
+  float* A = nullptr;          // [C*d, D]
+  float* B = nullptr;          // [C*d, D]
+  int64_t n = 0, n_pad = 0;
+  void* X_low = nullptr;       // [n_pad, d] low dtype, cluster-sorted, 128-row padded segments
+  int32_t* perm = nullptr;     // [n_pad] sorted position -> original id (-1 padding)
+  int32_t* tile_valid = nullptr;  // [n_pad/128]
+  std::vector<int64_t> offsets;   // host [C+1] padded segment starts
+  void* X_full = nullptr;      // [n, D] full dtype, original order
+  CUtensorMap tmap_xlow;
+  // search workspace
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  // host-buffer staging for lv_search_host
+  void* hs = nullptr;
+  size_t hs_bytes = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+lv_status fail(lv_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define LV_CUDA(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess) return fail(LV_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+lv_status check_device(int* nsm = nullptr) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(LV_EUNSUPPORTED, "no CUDA device");
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return fail(LV_EUNSUPPORTED, "no CUDA device");
+  if (p.major != 10 || p.minor != 0)
+    return fail(LV_EUNSUPPORTED, "device sm_%d%d is not sm_100 (this library is built for sm_100a only)", p.major,
+                p.minor);
+  if (nsm) *nsm = p.multiProcessorCount;
+  return LV_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2D row-major [rows, cols] of 16-bit elements; box [128 rows, ch cols]; swizzle = ch*2 bytes.
+lv_status make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int ch, bool bf16) {
+  auto enc = get_encode();
+  if (!enc) return fail(LV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)ch, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                   const_cast<void*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   ch == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LV_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return LV_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <typename T>
+T* carve(uint8_t*& p, size_t count) {
+  T* r = reinterpret_cast<T*>(p);
+  p += (count * sizeof(T) + 255) / 256 * 256;
+  return r;
+}
+
+struct Plan {
+  int m_pad, QP, P, NS, Cap, grid, stages;
+  size_t smem;
+  std::vector<int32_t> chunks;   // P x {tile_begin, tile_end, cluster}
+};
+
+// Work decomposition of the scan.
+lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
+  pl->QP = (int)((m + 255) / 256);
+  pl->m_pad = pl->QP * 256;
+  pl->Cap = (R + 31) / 32 * 32 + 128;
+  const int ntiles = (int)(ix->n_pad / 128);
+  // cluster segments in tiles
+  std::vector<std::pair<int, int>> segs;  // (tile_begin, tile_end)
+  std::vector<int> segc;
+  for (int c = 0; c < ix->C; ++c) {
+    int tb = (int)(ix->offsets[c] / 128), te = (int)(ix->offsets[c + 1] / 128);
+    if (te > tb) {
+      segs.push_back({tb, te});
+      segc.push_back(c);
+    }
+  }
+  // choose the chunk length so that units = P * QP spread evenly over the persistent grid
+  const int G = nsm;
+  const int slots_dep = (G + pl->QP - 1) / pl->QP + 1;
+  double best_eff = -1;
+  int best_len = ntiles;
+  const int maxP = std::min(ntiles, 4096);
+  for (int target = 1; target <= maxP; ++target) {
+    const int len = (ntiles + target - 1) / target;
+    int P = 0;
+    for (auto& s : segs) P += (s.second - s.first + len - 1) / len;
+    const int64_t units = (int64_t)P * pl->QP;
+    const int g = (int)std::min<int64_t>(G, units);
+    const int ns = std::min(P, slots_dep);
+    if (ns > 64 || (size_t)ns * pl->Cap * 8 + (size_t)ix->D * 4 > 200 * 1024) continue;
+    // time ~ max units on one CTA x tiles per unit; efficiency vs perfect spread
+    const double per_cta = (double)((units + g - 1) / g) * len;
+    const double ideal = (double)ntiles * pl->QP / G;
+    double eff = ideal / per_cta;
+    eff -= 1e-4 * (double)P / (double)ntiles;   // prefer fewer, longer chunks on ties
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best_len = len;
+    }
+    if ((int64_t)target * pl->QP > 64ll * G) break;
+  }
+  pl->chunks.clear();
+  for (size_t i = 0; i < segs.size(); ++i) {
+    const int tb = segs[i].first, te = segs[i].second;
+    const int cnt = (te - tb + best_len - 1) / best_len;
+    for (int j = 0; j < cnt; ++j) {
+      // near-equal pieces of the segment
+      const int a = tb + (int)((int64_t)(te - tb) * j / cnt);
+      const int b = tb + (int)((int64_t)(te - tb) * (j + 1) / cnt);
+      pl->chunks.push_back(a);
+      pl->chunks.push_back(b);
+      pl->chunks.push_back(segc[i]);
+    }
+  }
+  pl->P = (int)(pl->chunks.size() / 3);
+  pl->NS = std::min(pl->P, slots_dep);
+  const int64_t units = (int64_t)pl->P * pl->QP;
+  pl->grid = (int)std::min<int64_t>(G, units);
+  const size_t budget = 227 * 1024 - 1024 - 256;
+  const size_t a_bytes = 2 * (size_t)ix->d * 256;
+  const size_t stage_bytes = (size_t)ix->d * 256;
+  int st = (int)std::min<size_t>(8, (budget - a_bytes - 1024) / stage_bytes);
+  while (st >= 2 && lv::score_smem_bytes(ix->d, st) > budget) --st;
+  if (st < 2) return fail(LV_EUNSUPPORTED, "d=%d leaves no room for a 2-stage pipeline", ix->d);
+  pl->stages = st;
+  pl->smem = lv::score_smem_bytes(ix->d, st);
+  return LV_OK;
+}
+
+}  // namespace
+
+namespace lv {
+void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+}  // namespace lv
+
+extern "C" {
+
+const char* lv_last_error(void) { return g_err.c_str(); }
+
+const char* lv_version(void) { return "lv 0.1 sm_100a (tcgen05/TMA fused scan)"; }
+
+lv_status lv_fit_stats(const float* Q_learn, int64_t m_learn, const void* X_learn, lv_dtype x_dtype,
+                       int64_t n_learn, int32_t D, const int32_t* assign_learn, int32_t C, double* K_Q, double* K_X,
+                       void* stream) {
+  lv_status st = check_device();
+  if (st) return st;
+  if (!Q_learn || !X_learn || !K_Q || !K_X || m_learn <= 0 || n_learn <= 0 || D <= 0 || C < 1)
+    return fail(LV_EINVAL, "lv_fit_stats: bad arguments");
+  if (C > 1 && !assign_learn) return fail(LV_EINVAL, "lv_fit_stats: assign_learn required when C > 1");
+  if (x_dtype != LV_F32 && x_dtype != LV_F16) return fail(LV_EINVAL, "lv_fit_stats: x_dtype must be F32 or F16");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t kChunk = 8192;
+  const int nb = (int)((n_learn + lv::kSortBlock - 1) / lv::kSortBlock);
+  // sort learning rows by cluster (pad 1 = no padding)
+  int32_t *hist = nullptr, *bad = nullptr, *perm = nullptr;
+  int64_t *base = nullptr, *seg = nullptr;
+  std::vector<int64_t> hseg(2 * C + 1, 0);
+  if (C > 1) {
+    LV_CUDA(cudaMallocAsync(&hist, sizeof(int32_t) * (size_t)C * nb, s));
+    LV_CUDA(cudaMallocAsync(&base, sizeof(int64_t) * (size_t)C * nb, s));
+    LV_CUDA(cudaMallocAsync(&seg, sizeof(int64_t) * (2 * C + 1), s));
+    LV_CUDA(cudaMallocAsync(&bad, sizeof(int32_t), s));
+    LV_CUDA(cudaMallocAsync(&perm, sizeof(int32_t) * n_learn, s));
+    LV_CUDA(cudaMemsetAsync(bad, 0, sizeof(int32_t), s));
+    LV_CUDA(lv::launch_cluster_hist(assign_learn, n_learn, C, hist, nb, bad, s));
+    LV_CUDA(lv::launch_cluster_scan(hist, nb, C, 1, base, seg, s));
+    LV_CUDA(lv::launch_cluster_scatter(assign_learn, n_learn, C, base, nb, perm, s));
+    int32_t hbad = 0;
+    LV_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    LV_CUDA(cudaMemcpyAsync(hseg.data(), seg, sizeof(int64_t) * (2 * C + 1), cudaMemcpyDeviceToHost, s));
+    LV_CUDA(cudaStreamSynchronize(s));
+    if (hbad) {
+      cudaFreeAsync(hist, s); cudaFreeAsync(base, s); cudaFreeAsync(seg, s); cudaFreeAsync(bad, s); cudaFreeAsync(perm, s);
+      return fail(LV_EDATA, "lv_fit_stats: assign value outside [0, C)");
+    }
+  } else {
+    hseg[0] = 0;
+    hseg[1] = n_learn;
+  }
+  // chunk lists: owner 0 = K_Q rows of Q_learn; owners 1..C = clusters of X_learn
+  std::vector<int64_t> qlo, qhi, xlo, xhi;
+  std::vector<int32_t> xown, qown;
+  for (int64_t r = 0; r < m_learn; r += kChunk) {
+    qlo.push_back(r);
+    qhi.push_back(std::min(m_learn, r + kChunk));
+    qown.push_back(0);
+  }
+  for (int c = 0; c < C; ++c) {
+    const int64_t lo = hseg[c], hi = hseg[c] + (C > 1 ? hseg[C + 1 + c] : n_learn);
+    for (int64_t r = lo; r < hi; r += kChunk) {
+      xlo.push_back(r);
+      xhi.push_back(std::min(hi, r + kChunk));
+      xown.push_back(c);
+    }
+  }
+  const int nq = (int)qlo.size(), nx = (int)xlo.size();
+  const size_t DD = (size_t)D * D;
+  float* part = nullptr;
+  int64_t* dlo = nullptr;
+  int32_t* down = nullptr;
+  double* dK = nullptr;
+  const int ntot = nq + nx;
+  LV_CUDA(cudaMallocAsync(&part, sizeof(float) * DD * std::max(nq, nx), s));
+  LV_CUDA(cudaMallocAsync(&dlo, sizeof(int64_t) * 2 * ntot, s));
+  LV_CUDA(cudaMallocAsync(&down, sizeof(int32_t) * ntot, s));
+  LV_CUDA(cudaMallocAsync(&dK, sizeof(double) * DD * std::max(1, C), s));
+  std::vector<int64_t> hl(2 * ntot);
+  std::copy(qlo.begin(), qlo.end(), hl.begin());
+  std::copy(qhi.begin(), qhi.end(), hl.begin() + nq);
+  std::copy(xlo.begin(), xlo.end(), hl.begin() + 2 * nq);
+  std::copy(xhi.begin(), xhi.end(), hl.begin() + 2 * nq + nx);
+  std::vector<int32_t> ho(ntot);
+  std::copy(qown.begin(), qown.end(), ho.begin());
+  std::copy(xown.begin(), xown.end(), ho.begin() + nq);
+  LV_CUDA(cudaMemcpyAsync(dlo, hl.data(), sizeof(int64_t) * 2 * ntot, cudaMemcpyHostToDevice, s));
+  LV_CUDA(cudaMemcpyAsync(down, ho.data(), sizeof(int32_t) * ntot, cudaMemcpyHostToDevice, s));
+  // K_Q
+  LV_CUDA(lv::launch_stats(Q_learn, 0, D, nullptr, nq, dlo, dlo + nq, D, part, s));
+  LV_CUDA(lv::launch_stats_reduce(part, nq, down, 1, D, dK, s));
+  LV_CUDA(cudaMemcpyAsync(K_Q, dK, sizeof(double) * DD, cudaMemcpyDeviceToHost, s));
+  // K_X per cluster
+  LV_CUDA(lv::launch_stats(X_learn, x_dtype == LV_F16, D, perm, nx, dlo + 2 * nq, dlo + 2 * nq + nx, D, part, s));
+  LV_CUDA(lv::launch_stats_reduce(part, nx, down + nq, C, D, dK, s));
+  LV_CUDA(cudaMemcpyAsync(K_X, dK, sizeof(double) * DD * C, cudaMemcpyDeviceToHost, s));
+  LV_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(part, s);
+  cudaFreeAsync(dlo, s);
+  cudaFreeAsync(down, s);
+  cudaFreeAsync(dK, s);
+  if (C > 1) {
+    cudaFreeAsync(hist, s); cudaFreeAsync(base, s); cudaFreeAsync(seg, s); cudaFreeAsync(bad, s); cudaFreeAsync(perm, s);
+  }
+  LV_CUDA(cudaStreamSynchronize(s));
+  return LV_OK;
+}
+
+lv_status lv_index_create(lv_index** out, int32_t D, int32_t d, int32_t C, lv_dtype low_dtype, lv_dtype full_dtype,
+                          const float* A_stack, const float* B_stack) {
+  lv_status st = check_device();
+  if (st) return st;
+  if (!out || !A_stack || !B_stack) return fail(LV_EINVAL, "lv_index_create: NULL argument");
+  if (d < 1 || d > D || d % 32 != 0 || d > 192) return fail(LV_EINVAL, "lv_index_create: need 32 <= d <= min(D,192), d %% 32 == 0 (d=%d)", d);
+  if (C < 1 || C > 1024) return fail(LV_EINVAL, "lv_index_create: need 1 <= C <= 1024");
+  if (low_dtype != LV_BF16 && low_dtype != LV_F16) return fail(LV_EINVAL, "lv_index_create: low_dtype must be BF16/F16");
+  if (full_dtype != LV_F32 && full_dtype != LV_F16) return fail(LV_EINVAL, "lv_index_create: full_dtype must be F32/F16");
+  if ((full_dtype == LV_F32 && D % 4) || (full_dtype == LV_F16 && D % 8))
+    return fail(LV_EINVAL, "lv_index_create: D=%d breaks 16-byte rows", D);
+  lv_index* ix = new lv_index();
+  ix->D = D;
+  ix->d = d;
+  ix->C = C;
+  ix->low = low_dtype;
+  ix->full = full_dtype;
+  const size_t bytes = sizeof(float) * (size_t)C * d * D;
+  if (cudaMalloc(&ix->A, bytes) != cudaSuccess || cudaMalloc(&ix->B, bytes) != cudaSuccess) {
+    lv_index_destroy(ix);
+    return fail(LV_ENOMEM, "lv_index_create: cudaMalloc failed");
+  }
+  if (cudaMemcpy(ix->A, A_stack, bytes, cudaMemcpyDeviceToDevice) != cudaSuccess ||
+      cudaMemcpy(ix->B, B_stack, bytes, cudaMemcpyDeviceToDevice) != cudaSuccess) {
+    lv_index_destroy(ix);
+    return fail(LV_ECUDA, "lv_index_create: copy failed");
+  }
+  *out = ix;
+  return LV_OK;
+}
+
+static void free_db(lv_index* ix) {
+  cudaFree(ix->X_low);
+  cudaFree(ix->perm);
+  cudaFree(ix->tile_valid);
+  cudaFree(ix->X_full);
+  ix->X_low = ix->X_full = nullptr;
+  ix->perm = ix->tile_valid = nullptr;
+  ix->n = ix->n_pad = 0;
+}
+
+lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int64_t n, const int32_t* assign,
+                             void* stream) {
+  lv_status st = check_device();
+  if (st) return st;
+  if (!ix || !X || n <= 0) return fail(LV_EINVAL, "lv_encode_database: bad arguments");
+  if (x_dtype != LV_F32 && x_dtype != LV_F16) return fail(LV_EINVAL, "lv_encode_database: x_dtype must be F32/F16");
+  if (ix->C > 1 && !assign) return fail(LV_EINVAL, "lv_encode_database: assign required when C > 1");
+  if (n > (int64_t)INT32_MAX - 128 * (int64_t)ix->C) return fail(LV_EINVAL, "lv_encode_database: n too large");
+  cudaStream_t s = (cudaStream_t)stream;
+  free_db(ix);
+  const int C = ix->C;
+  std::vector<int64_t> hseg(2 * C + 1, 0);
+  int32_t* perm_tmp = nullptr;
+  if (C > 1) {
+    const int nb = (int)((n + lv::kSortBlock - 1) / lv::kSortBlock);
+    int32_t *hist = nullptr, *bad = nullptr;
+    int64_t *base = nullptr, *seg = nullptr;
+    LV_CUDA(cudaMallocAsync(&hist, sizeof(int32_t) * (size_t)C * nb, s));
+    LV_CUDA(cudaMallocAsync(&base, sizeof(int64_t) * (size_t)C * nb, s));
+    LV_CUDA(cudaMallocAsync(&seg, sizeof(int64_t) * (2 * C + 1), s));
+    LV_CUDA(cudaMallocAsync(&bad, sizeof(int32_t), s));
+    LV_CUDA(cudaMemsetAsync(bad, 0, sizeof(int32_t), s));
+    LV_CUDA(lv::launch_cluster_hist(assign, n, C, hist, nb, bad, s));
+    LV_CUDA(lv::launch_cluster_scan(hist, nb, C, 128, base, seg, s));
+    int32_t hbad = 0;
+    LV_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    LV_CUDA(cudaMemcpyAsync(hseg.data(), seg, sizeof(int64_t) * (2 * C + 1), cudaMemcpyDeviceToHost, s));
+    LV_CUDA(cudaStreamSynchronize(s));
+    if (hbad) {
+      cudaFree(hist); cudaFree(base); cudaFree(seg); cudaFree(bad);
+      return fail(LV_EDATA, "lv_encode_database: assign value outside [0, C)");
+    }
+    ix->n_pad = hseg[C];
+    if (cudaMalloc(&ix->perm, sizeof(int32_t) * ix->n_pad) != cudaSuccess) return fail(LV_ENOMEM, "perm");
+    LV_CUDA(cudaMemsetAsync(ix->perm, 0xFF, sizeof(int32_t) * ix->n_pad, s));
+    LV_CUDA(lv::launch_cluster_scatter(assign, n, C, base, nb, ix->perm, s));
+    LV_CUDA(cudaStreamSynchronize(s));
+    cudaFree(hist); cudaFree(base); cudaFree(seg); cudaFree(bad);
+    (void)perm_tmp;
+  } else {
+    ix->n_pad = (n + 127) / 128 * 128;
+    hseg[0] = 0;
+    hseg[1] = ix->n_pad;
+    hseg[2] = n;
+    if (cudaMalloc(&ix->perm, sizeof(int32_t) * ix->n_pad) != cudaSuccess) return fail(LV_ENOMEM, "perm");
+    LV_CUDA(lv::launch_iota_perm(ix->perm, n, ix->n_pad, s));
+  }
+  ix->n = n;
+  ix->offsets.assign(hseg.begin(), hseg.begin() + C + 1);
+  // per-tile metadata: valid rows per 128-row tile, W row offset per 64-row tile
+  const int64_t nt = ix->n_pad / 128;
+  std::vector<int32_t> tv(nt), wrow(nt * 2);
+  for (int c = 0; c < C; ++c) {
+    const int64_t st0 = hseg[c], sz = (C > 1) ? hseg[C + 1 + c] : n, en = hseg[c + 1];
+    for (int64_t t = st0 / 128; t < en / 128; ++t) {
+      tv[t] = (int32_t)std::max<int64_t>(0, std::min<int64_t>(128, st0 + sz - t * 128));
+      wrow[2 * t] = wrow[2 * t + 1] = c * ix->d;
+    }
+  }
+  int32_t* dwrow = nullptr;
+  if (cudaMalloc(&ix->tile_valid, sizeof(int32_t) * nt) != cudaSuccess) return fail(LV_ENOMEM, "tile_valid");
+  LV_CUDA(cudaMallocAsync(&dwrow, sizeof(int32_t) * nt * 2, s));
+  LV_CUDA(cudaMemcpyAsync(ix->tile_valid, tv.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, s));
+  LV_CUDA(cudaMemcpyAsync(dwrow, wrow.data(), sizeof(int32_t) * nt * 2, cudaMemcpyHostToDevice, s));
+  // X_low = RNE(B_c x) (K6)
+  const size_t esz = 2;
+  if (cudaMalloc(&ix->X_low, esz * ix->n_pad * ix->d) != cudaSuccess) return fail(LV_ENOMEM, "X_low");
+  LV_CUDA(lv::launch_rows_gemm(X, x_dtype == LV_F16, ix->D, ix->perm, n, ix->n_pad, ix->B, ix->D, dwrow, ix->d,
+                               ix->X_low, ix->low, ix->d, ix->n_pad, s));
+  // full-precision copy for the re-rank
+  const size_t fsz = ix->full == LV_F16 ? 2 : 4;
+  if (cudaMalloc(&ix->X_full, fsz * n * ix->D) != cudaSuccess) return fail(LV_ENOMEM, "X_full");
+  LV_CUDA(lv::launch_convert(X, x_dtype == LV_F16, ix->X_full, ix->full == LV_F16, n * ix->D, s));
+  lv_status ts = make_tmap(&ix->tmap_xlow, ix->X_low, ix->n_pad, ix->d, (ix->d % 64 == 0) ? 64 : 32, ix->low == LV_BF16);
+  LV_CUDA(cudaStreamSynchronize(s));
+  cudaFree(dwrow);
+  return ts;
+}
+
+lv_status lv_project_queries(const lv_index* ix, const float* Q, int64_t m, void* Qp, void* stream) {
+  lv_status st = check_device();
+  if (st) return st;
+  if (!ix || !Q || !Qp || m <= 0) return fail(LV_EINVAL, "lv_project_queries: bad arguments");
+  LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, m, ix->A, ix->D, nullptr, ix->C * ix->d, Qp, ix->low,
+                               (int64_t)ix->C * ix->d, m, (cudaStream_t)stream));
+  return LV_OK;
+}
+
+lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t R, int32_t* ids, float* scores,
+                    lv_search_debug* dbg, void* stream) {
+  int nsm = 0;
+  lv_status st = check_device(&nsm);
+  if (st) return st;
+  if (!ix || !Q || !ids || !scores || m <= 0) return fail(LV_EINVAL, "lv_search: bad arguments");
+  if (ix->n <= 0) return fail(LV_EINVAL, "lv_search: index not encoded");
+  if (k < 1 || k > R || R > 512 || R > ix->n) return fail(LV_EINVAL, "lv_search: need 1 <= k <= R <= min(n, 512)");
+  if (m > (1 << 24)) return fail(LV_EINVAL, "lv_search: m too large");
+  cudaStream_t s = (cudaStream_t)stream;
+  Plan pl;
+  st = plan_search(ix, m, R, nsm, &pl);
+  if (st) return st;
+  const int Cd = ix->C * ix->d;
+  // workspace
+  const size_t need = ((size_t)pl.m_pad * Cd * 2 + 256) + ((size_t)pl.NS * pl.m_pad * pl.Cap * 8 + 256) +
+                      ((size_t)pl.NS * pl.m_pad * 4 + 256) + ((size_t)pl.NS * pl.m_pad * 8 + 256) +
+                      ((size_t)pl.P * pl.QP * 4 + 256) + (pl.chunks.size() * 4 + 256);
+  if (need > ix->ws_bytes) {
+    cudaFree(ix->ws);
+    ix->ws = nullptr;
+    ix->ws_bytes = 0;
+    if (cudaMalloc(&ix->ws, need) != cudaSuccess) return fail(LV_ENOMEM, "lv_search: workspace %zu bytes", need);
+    ix->ws_bytes = need;
+  }
+  uint8_t* p = reinterpret_cast<uint8_t*>(ix->ws);
+  void* Qp = carve<uint16_t>(p, (size_t)pl.m_pad * Cd);
+  uint64_t* cand = carve<uint64_t>(p, (size_t)pl.NS * pl.m_pad * pl.Cap);
+  uint8_t* zero_lo = p;
+  int32_t* cnt = carve<int32_t>(p, (size_t)pl.NS * pl.m_pad);
+  uint64_t* tau = carve<uint64_t>(p, (size_t)pl.NS * pl.m_pad);
+  int32_t* done = carve<int32_t>(p, (size_t)pl.P * pl.QP);
+  uint8_t* zero_hi = p;
+  int32_t* chunk_info = carve<int32_t>(p, pl.chunks.size());
+
+  cudaEvent_t ev[4];
+  const bool timing = dbg && dbg->timing;
+  if (timing) {
+    for (int i = 0; i < 4; ++i) LV_CUDA(cudaEventCreate(&ev[i]));
+    LV_CUDA(cudaEventRecord(ev[0], s));
+  }
+  int launches = 0;
+  LV_CUDA(cudaMemcpyAsync(chunk_info, pl.chunks.data(), pl.chunks.size() * 4, cudaMemcpyHostToDevice, s));
+  LV_CUDA(cudaMemsetAsync(zero_lo, 0, zero_hi - zero_lo, s));
+  // K1 projection (rows >= m are zero)
+  LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, pl.m_pad, ix->A, ix->D, nullptr, Cd, Qp, ix->low, Cd, pl.m_pad, s));
+  ++launches;
+  if (timing) LV_CUDA(cudaEventRecord(ev[1], s));
+  // K2/K3 fused scan
+  CUtensorMap tmap_qp;
+  const int ch = (ix->d % 64 == 0) ? 64 : 32;
+  st = make_tmap(&tmap_qp, Qp, pl.m_pad, Cd, ch, ix->low == LV_BF16);
+  if (st) return st;
+  lv::ScoreArgs sa;
+  sa.m = (int)m;
+  sa.m_pad = pl.m_pad;
+  sa.QP = pl.QP;
+  sa.d = ix->d;
+  sa.R = R;
+  sa.P = pl.P;
+  sa.NS = pl.NS;
+  sa.Cap = pl.Cap;
+  sa.stages = pl.stages;
+  sa.chunk_info = chunk_info;
+  sa.tile_valid = ix->tile_valid;
+  sa.perm = ix->C > 1 ? ix->perm : nullptr;
+  sa.cand = cand;
+  sa.cnt = cnt;
+  sa.tau = tau;
+  sa.done = done;
+  sa.raw = dbg ? dbg->raw_scores : nullptr;
+  sa.n_pad = ix->n_pad;
+  LV_CUDA(lv::launch_score(&tmap_qp, &ix->tmap_xlow, sa, ix->low == LV_BF16, pl.grid, pl.smem, s));
+  ++launches;
+  if (timing) LV_CUDA(cudaEventRecord(ev[2], s));
+  // K4/K5 select + re-rank + top-k
+  lv::RerankArgs ra;
+  ra.m = (int)m;
+  ra.m_pad = pl.m_pad;
+  ra.D = ix->D;
+  ra.R = R;
+  ra.k = k;
+  ra.NS = pl.NS;
+  ra.Cap = pl.Cap;
+  ra.cand = cand;
+  ra.cnt = cnt;
+  ra.Q = Q;
+  ra.X = ix->X_full;
+  ra.full_f16 = ix->full == LV_F16;
+  ra.ids = ids;
+  ra.scores = scores;
+  ra.cand_ids = dbg ? dbg->cand_ids : nullptr;
+  ra.cand_scores = dbg ? dbg->cand_scores : nullptr;
+  LV_CUDA(lv::launch_select_rerank(ra, s));
+  ++launches;
+  if (timing) {
+    LV_CUDA(cudaEventRecord(ev[3], s));
+    LV_CUDA(cudaEventSynchronize(ev[3]));
+    float t01, t12, t23, t03;
+    cudaEventElapsedTime(&t01, ev[0], ev[1]);
+    cudaEventElapsedTime(&t12, ev[1], ev[2]);
+    cudaEventElapsedTime(&t23, ev[2], ev[3]);
+    cudaEventElapsedTime(&t03, ev[0], ev[3]);
+    dbg->phase_ms[0] = t01;
+    dbg->phase_ms[1] = t12;
+    dbg->phase_ms[2] = t23;
+    dbg->phase_ms[3] = t03;
+    for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
+  }
+  if (dbg) {
+    dbg->launches = launches;
+    dbg->slots = pl.NS;
+    dbg->units = pl.P * pl.QP;
+    dbg->grid = pl.grid;
+  }
+  return LV_OK;
+}
+
+lv_status lv_search_host(lv_index* ix, const float* Q_host, int64_t m, int32_t k, int32_t R, int32_t* ids_host,
+                         float* scores_host, void* stream) {
+  lv_status st = check_device();
+  if (st) return st;
+  if (!ix || !Q_host || !ids_host || !scores_host || m <= 0 || k <= 0) return fail(LV_EINVAL, "lv_search_host: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t qb = (size_t)m * ix->D * 4, ob = (size_t)m * k * 4;
+  const size_t need = qb + 2 * ob + 512;
+  if (need > ix->hs_bytes) {
+    cudaFree(ix->hs);
+    ix->hs = nullptr;
+    ix->hs_bytes = 0;
+    if (cudaMalloc(&ix->hs, need) != cudaSuccess) return fail(LV_ENOMEM, "lv_search_host: staging");
+    ix->hs_bytes = need;
+  }
+  uint8_t* p = reinterpret_cast<uint8_t*>(ix->hs);
+  float* dQ = carve<float>(p, (size_t)m * ix->D);
+  int32_t* dI = carve<int32_t>(p, (size_t)m * k);
+  float* dS = carve<float>(p, (size_t)m * k);
+  LV_CUDA(cudaMemcpyAsync(dQ, Q_host, qb, cudaMemcpyHostToDevice, s));
+  st = lv_search(ix, dQ, m, k, R, dI, dS, nullptr, stream);
+  if (st) return st;
+  LV_CUDA(cudaMemcpyAsync(ids_host, dI, ob, cudaMemcpyDeviceToHost, s));
+  LV_CUDA(cudaMemcpyAsync(scores_host, dS, ob, cudaMemcpyDeviceToHost, s));
+  LV_CUDA(cudaStreamSynchronize(s));
+  return LV_OK;
+}
+
+lv_status lv_assign_tags(const void* X, lv_dtype x_dtype, int64_t n, int32_t D, const float* centres, int32_t C,
+                         int32_t* assign, void* stream) {
+  lv_status st = check_device();
+  if (st) return st;
+  if (!X || !centres || !assign || n <= 0 || D <= 0 || C < 1) return fail(LV_EINVAL, "lv_assign_tags: bad arguments");
+  if (x_dtype != LV_F32 && x_dtype != LV_F16) return fail(LV_EINVAL, "lv_assign_tags: x_dtype must be F32/F16");
+  LV_CUDA(lv::launch_assign(X, x_dtype == LV_F16, n, D, centres, C, assign, (cudaStream_t)stream));
+  return LV_OK;
+}
+
+lv_status lv_index_info(const lv_index* ix, int64_t* n, int64_t* n_pad, int32_t* D, int32_t* d, int32_t* C) {
+  if (!ix) return fail(LV_EINVAL, "lv_index_info: NULL index");
+  if (n) *n = ix->n;
+  if (n_pad) *n_pad = ix->n_pad;
+  if (D) *D = ix->D;
+  if (d) *d = ix->d;
+  if (C) *C = ix->C;
+  return LV_OK;
+}
+
+lv_status lv_index_export(const lv_index* ix, void* X_low, int32_t* perm, int64_t* offsets, void* stream) {
+  if (!ix) return fail(LV_EINVAL, "lv_index_export: NULL index");
+  if (ix->n <= 0) return fail(LV_EINVAL, "lv_index_export: index not encoded");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (X_low) LV_CUDA(cudaMemcpyAsync(X_low, ix->X_low, (size_t)ix->n_pad * ix->d * 2, cudaMemcpyDeviceToDevice, s));
+  if (perm) LV_CUDA(cudaMemcpyAsync(perm, ix->perm, (size_t)ix->n_pad * 4, cudaMemcpyDeviceToDevice, s));
+  if (offsets) std::copy(ix->offsets.begin(), ix->offsets.end(), offsets);
+  LV_CUDA(cudaStreamSynchronize(s));
+  return LV_OK;
+}
+
+void lv_index_destroy(lv_index* ix) {
+  if (!ix) return;
+  free_db(ix);
+  cudaFree(ix->A);
+  cudaFree(ix->B);
+  cudaFree(ix->ws);
+  cudaFree(ix->hs);
+  delete ix;
+}
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+// Internal host-side declarations shared by the lv translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/lv.h"
+
+namespace lv {
+
+void set_error(const char* fmt, ...);
+
+// Work decomposition of the fused scan.
+struct ScanPlan {
+  int QP = 0;          // query pairs (256 queries each)
+  int P = 0;           // database chunks (each inside one cluster segment)
+  int NS = 0;          // per-query candidate slots
+  int Cap = 0;         // candidate capacity per (slot, query)
+  int grid = 0;        // CTAs
+  int stages = 0;      // smem pipeline stages for X_low tiles
+  size_t smem = 0;     // dynamic smem bytes
+};
+
+struct ScoreArgs {
+  int m, m_pad, QP, d, R, P, NS, Cap, stages;
+  const int32_t* chunk_info;   // [P][3]: tile_begin, tile_end, cluster
+  const int32_t* tile_valid;   // [n_tiles]
+  const int32_t* perm;         // [n_pad] or nullptr (identity)
+  uint64_t* cand;              // [NS][m_pad][Cap]
+  int32_t* cnt;                // [NS][m_pad]
+  uint64_t* tau;               // [NS][m_pad]
+  int32_t* done;               // [P][QP]
+  float* raw;                  // [m_pad][n_pad] or nullptr
+  int64_t n_pad;
+};
+
+cudaError_t launch_score(const CUtensorMap* tmap_qp, const CUtensorMap* tmap_xlow, const ScoreArgs& a,
+                         bool bf16, int grid, size_t smem, cudaStream_t s);
+
+struct RerankArgs {
+  int m, m_pad, D, R, k, NS, Cap;
+  const uint64_t* cand;
+  const int32_t* cnt;
+  const float* Q;              // [m, D] fp32
+  const void* X;               // [n, D] full dtype
+  int full_f16;
+  int32_t* ids;                // [m, k]
+  float* scores;               // [m, k]
+  int32_t* cand_ids;           // [m, R] or nullptr
+  float* cand_scores;          // [m, R] or nullptr
+};
+cudaError_t launch_select_rerank(const RerankArgs& a, cudaStream_t s);
+
+// out[r, j] = RNE(sum_k in[rowidx[r], k] * W[wrow(r) + j, k]) for 64-row tiles.
+cudaError_t launch_rows_gemm(const void* in, int in_f16, int64_t ld_in, const int32_t* rowidx, int64_t rows_valid,
+                             int64_t nrows, const float* W, int K, const int32_t* tile_wrow64, int ncols,
+                             void* out, int out_dtype, int64_t ld_out, int64_t rows_store, cudaStream_t s);
+cudaError_t launch_iota_perm(int32_t* perm, int64_t n, int64_t n_pad, cudaStream_t s);
+
+cudaError_t launch_stats(const void* in, int in_f16, int64_t ld, const int32_t* rowidx, int nchunks,
+                         const int64_t* chunk_lo, const int64_t* chunk_hi, int D, float* partial, cudaStream_t s);
+cudaError_t launch_stats_reduce(const float* partial, int nchunks, const int32_t* chunk_owner, int nowners, int D,
+                                double* out, cudaStream_t s);
+
+cudaError_t launch_cluster_hist(const int32_t* assign, int64_t n, int C, int32_t* hist, int nblocks, int32_t* bad,
+                                cudaStream_t s);
+cudaError_t launch_cluster_scan(const int32_t* hist, int nblocks, int C, int pad, int64_t* base, int64_t* seg,
+                                cudaStream_t s);
+cudaError_t launch_cluster_scatter(const int32_t* assign, int64_t n, int C, const int64_t* base, int nblocks,
+                                   int32_t* perm, cudaStream_t s);
+
+cudaError_t launch_convert(const void* in, int in_f16, void* out, int out_f16, int64_t count, cudaStream_t s);
+cudaError_t launch_assign(const void* X, int x_f16, int64_t n, int D, const float* centres, int C, int32_t* assign,
+                          cudaStream_t s);
+
+constexpr int kSortBlock = 4096;
+
+}  // namespace lv

