@@ -3,6 +3,7 @@
 #include <cudaTypedefs.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <cmath>
@@ -495,6 +496,10 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   sa.done = done;
   sa.raw = dbg ? dbg->raw_scores : nullptr;
   sa.n_pad = ix->n_pad;
+  {
+    const char* f = getenv("LV_DEBUG_SCAN_FLAGS");
+    sa.flags = f ? atoi(f) : 0;
+  }
   LV_CUDA(lv::launch_score(&tmap_qp, &ix->tmap_xlow, sa, ix->low == LV_BF16, pl.grid, pl.smem, s));
   ++launches;
   if (timing) LV_CUDA(cudaEventRecord(ev[2], s));

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) k_stats(const TIn* __restrict__ in, int64
   const int ch = blockIdx.z;
   const int64_t lo = lo_[ch], hi = hi_[ch];
   const int tx = tid & 15, ty = tid >> 4;
-  float acc[4][4] = {};
+  float acc[4][4] = {}, comp[4][4] = {};
   for (int64_t rb = lo; rb < hi; rb += GK) {
     // 32 rows x 64 cols for each side: 2048 elements, 8 per thread
 #pragma unroll
@@ -123,6 +123,9 @@ __global__ void __launch_bounds__(256) k_stats(const TIn* __restrict__ in, int64
       Bs[rr][cc] = vb;
     }
     __syncthreads();
+    // 32-row partial in fp32, then a compensated (Kahan) add into the running sum: the chunk
+    // sum's error stays at the 32-term level instead of growing with the chunk length.
+    float t[4][4] = {};
 #pragma unroll 8
     for (int k = 0; k < GK; ++k) {
       float av[4], bv[4];
@@ -133,8 +136,17 @@ __global__ void __launch_bounds__(256) k_stats(const TIn* __restrict__ in, int64
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) t[i][j] = fmaf(av[i], bv[j], t[i][j]);
     }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float y = __fsub_rn(t[i][j], comp[i][j]);
+        const float s = __fadd_rn(acc[i][j], y);
+        comp[i][j] = __fsub_rn(__fsub_rn(s, acc[i][j]), y);
+        acc[i][j] = s;
+      }
     __syncthreads();
   }
 #pragma unroll

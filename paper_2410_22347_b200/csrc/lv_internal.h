@@ -35,6 +35,7 @@ struct ScoreArgs {
   int32_t* done;               // [P][QP]
   float* raw;                  // [m_pad][n_pad] or nullptr
   int64_t n_pad;
+  int flags;                   // debug: bit0 = epilogue skips top-R (MMA/TMA throughput probe)
 };
 
 cudaError_t launch_score(const CUtensorMap* tmap_qp, const CUtensorMap* tmap_xlow, const ScoreArgs& a,

@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(acc_empty + acc);
           }
+          if (a.flags & 1) continue;
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
             const int col0 = half * 64 + g * 32;

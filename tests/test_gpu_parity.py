@@ -70,6 +70,20 @@ def _ulp_diff(a, b, dtype):
     return np.abs(a - b) / nxt
 
 
+def _g1_ok(got, ref, absdot, dtype, D):
+    """G1: |got - ref| <= 1 storage ulp(ref) + the fp32-accumulation bound D 2^-24 sum_k |b_k x_k|
+    (the kernel accumulates in fp32, the oracle in fp64; near-zero outputs of cancelling dot
+    products may differ by more than one of their own tiny ulps).  Returns (all ok, flip frac)."""
+    u = _ulp_diff(got, ref, dtype)
+    ulp = np.where(u > 0, np.abs(got - ref) / np.maximum(u, 1e-300), 0)
+    import ml_dtypes
+    t = ml_dtypes.bfloat16 if dtype == "bf16" else np.float16
+    bb = ref.astype(t)
+    one = np.abs(np.nextafter(bb, np.array(np.inf, dtype=t)).astype(np.float64) - bb.astype(np.float64))
+    ok = np.abs(got - ref) <= one + D * 2.0 ** -24 * absdot
+    return ok.all(), float((got != ref).mean())
+
+
 def _tol_ok(got, ref, tol, scale):
     return np.abs(got - ref) <= tol * np.maximum(np.abs(ref), 1e-2 * scale)
 
@@ -89,13 +103,14 @@ def test_g1_encode_project_and_raw_scores(lv, d):
     assert np.array_equal(perm[valid], np.arange(c.n))
     xl_gpu = X_low.float().cpu().numpy().astype(np.float64)[valid]
     xl_ref = O.encode(X, B32[0], None, store=c.low_dtype)
-    u = _ulp_diff(xl_gpu, xl_ref, c.low_dtype)
-    assert u.max() <= 1.0, u.max()
-    assert (u > 0).mean() < 5e-3
+    ok, flips = _g1_ok(xl_gpu, xl_ref, np.abs(X.astype(np.float64)) @ np.abs(B32[0].astype(np.float64)).T,
+                       c.low_dtype, c.D)
+    assert ok and flips < 5e-3, flips
     Qp = lv.lv_project_queries(ix, torch.from_numpy(Q).cuda()).float().cpu().numpy().astype(np.float64)
     qp_ref = O.project(Q, A32, store=c.low_dtype)[:, 0, :]
-    u = _ulp_diff(Qp, qp_ref, c.low_dtype)
-    assert u.max() <= 1.0 and (u > 0).mean() < 5e-3
+    ok, flips = _g1_ok(Qp, qp_ref, np.abs(Q.astype(np.float64)) @ np.abs(A32[0].astype(np.float64)).T,
+                       c.low_dtype, c.D)
+    assert ok and flips < 5e-3, flips
     ids, sc, dbg = lv.lv_search(ix, torch.from_numpy(Q).cuda(), k, R, raw=True)
     raw = dbg["raw"].cpu().numpy()[: c.m_test][:, valid].astype(np.float64)
     ref = qp_ref @ xl_ref.T
@@ -234,8 +249,9 @@ def test_gleanvec_parity_small(lv):
         assert np.array_equal(seg, np.nonzero(assign == cc)[0])     # stable
     valid = perm >= 0
     xl_ref = O.encode(X, B32, assign, store=c.low_dtype)[perm[valid]]
-    u = _ulp_diff(X_low.float().cpu().numpy().astype(np.float64)[valid], xl_ref, c.low_dtype)
-    assert u.max() <= 1.0
+    absdot = O.encode(np.abs(X), np.abs(B32), assign)[perm[valid]]
+    ok, flips = _g1_ok(X_low.float().cpu().numpy().astype(np.float64)[valid], xl_ref, absdot, c.low_dtype, c.D)
+    assert ok and flips < 5e-3, flips
     _check_search(lv, c, X, Q, A32, B32, assign, R, k, C)
 
 
