@@ -81,13 +81,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 2D row-major [rows, cols] of 16-bit elements; box [128 rows, ch cols]; swizzle = ch*2 bytes.
-lv_status make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int ch, bool bf16) {
+// 2D row-major [rows, cols] of 16-bit elements; box [box_rows, ch cols]; swizzle = ch*2 bytes.
+lv_status make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int ch, bool bf16, int box_rows) {
   auto enc = get_encode();
   if (!enc) return fail(LV_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t gstride[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {(cuuint32_t)ch, 128};
+  cuuint32_t box[2] = {(cuuint32_t)ch, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
                    const_cast<void*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -107,30 +107,19 @@ T* carve(uint8_t*& p, size_t count) {
 }
 
 struct Plan {
-  int m_pad, QP, P, NS, Cap, grid, stages;
+  int m_pad, QP, NS, Cap, grid, stages;
   size_t smem;
-  std::vector<int32_t> chunks;   // P x {tile_begin, tile_end, cluster}
+  std::vector<int32_t> chunks[2];   // phase A / phase B: P x {tile_begin, tile_end, cluster}
+  int P[2] = {0, 0};
 };
 
-// Work decomposition of the scan.
-lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
-  pl->QP = (int)((m + 255) / 256);
-  pl->m_pad = pl->QP * 256;
-  pl->Cap = (R + 31) / 32 * 32 + 128;
-  const int ntiles = (int)(ix->n_pad / 128);
-  // cluster segments in tiles
-  std::vector<std::pair<int, int>> segs;  // (tile_begin, tile_end)
-  std::vector<int> segc;
-  for (int c = 0; c < ix->C; ++c) {
-    int tb = (int)(ix->offsets[c] / 128), te = (int)(ix->offsets[c + 1] / 128);
-    if (te > tb) {
-      segs.push_back({tb, te});
-      segc.push_back(c);
-    }
-  }
-  // choose the chunk length so that units = P * QP spread evenly over the persistent grid
-  const int G = nsm;
-  const int slots_dep = (G + pl->QP - 1) / pl->QP + 1;
+// Chunks of the given segments (tile ranges) so that units = P * QP spread evenly over the grid.
+void make_chunks(const std::vector<std::pair<int, int>>& segs, const std::vector<int>& segc, int QP, int G,
+                 int maxChunks, std::vector<int32_t>* out) {
+  int ntiles = 0;
+  for (auto& s : segs) ntiles += s.second - s.first;
+  out->clear();
+  if (ntiles == 0) return;
   double best_eff = -1;
   int best_len = ntiles;
   const int maxP = std::min(ntiles, 4096);
@@ -138,42 +127,75 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
     const int len = (ntiles + target - 1) / target;
     int P = 0;
     for (auto& s : segs) P += (s.second - s.first + len - 1) / len;
-    const int64_t units = (int64_t)P * pl->QP;
+    if (P > maxChunks) continue;
+    const int64_t units = (int64_t)P * QP;
     const int g = (int)std::min<int64_t>(G, units);
-    const int ns = std::min(P, slots_dep);
-    if (ns > 64 || (size_t)ns * pl->Cap * 8 + (size_t)ix->D * 4 > 200 * 1024) continue;
     // time ~ max units on one CTA x tiles per unit; efficiency vs perfect spread
     const double per_cta = (double)((units + g - 1) / g) * len;
-    const double ideal = (double)ntiles * pl->QP / G;
-    double eff = ideal / per_cta;
-    eff -= 1e-4 * (double)P / (double)ntiles;   // prefer fewer, longer chunks on ties
+    const double ideal = (double)ntiles * QP / G;
+    double eff = ideal / per_cta - 1e-4 * (double)P / (double)ntiles;   // prefer fewer chunks on ties
     if (eff > best_eff + 1e-9) {
       best_eff = eff;
       best_len = len;
     }
-    if ((int64_t)target * pl->QP > 64ll * G) break;
+    if ((int64_t)target * QP > 64ll * G) break;
   }
-  pl->chunks.clear();
   for (size_t i = 0; i < segs.size(); ++i) {
     const int tb = segs[i].first, te = segs[i].second;
+    if (te <= tb) continue;
     const int cnt = (te - tb + best_len - 1) / best_len;
     for (int j = 0; j < cnt; ++j) {
-      // near-equal pieces of the segment
-      const int a = tb + (int)((int64_t)(te - tb) * j / cnt);
-      const int b = tb + (int)((int64_t)(te - tb) * (j + 1) / cnt);
-      pl->chunks.push_back(a);
-      pl->chunks.push_back(b);
-      pl->chunks.push_back(segc[i]);
+      out->push_back(tb + (int)((int64_t)(te - tb) * j / cnt));
+      out->push_back(tb + (int)((int64_t)(te - tb) * (j + 1) / cnt));
+      out->push_back(segc[i]);
     }
   }
-  pl->P = (int)(pl->chunks.size() / 3);
-  pl->NS = std::min(pl->P, slots_dep);
-  const int64_t units = (int64_t)pl->P * pl->QP;
-  pl->grid = (int)std::min<int64_t>(G, units);
+}
+
+// Work decomposition of the scan: phase A covers the first kPhaseA of every
+// cluster segment, phase B the rest (after the exact per-query threshold merge).
+constexpr double kPhaseA = 0.08;
+constexpr int kMinTilesTwoPhase = 256;
+
+lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
+  pl->QP = (int)((m + 255) / 256);
+  pl->m_pad = pl->QP * 256;
+  pl->Cap = (R + 31) / 32 * 32 + 128;
+  const int ntiles = (int)(ix->n_pad / 128);
+  const bool two = ntiles >= kMinTilesTwoPhase;
+  std::vector<std::pair<int, int>> segA, segB;
+  std::vector<int> segc;
+  for (int c = 0; c < ix->C; ++c) {
+    const int tb = (int)(ix->offsets[c] / 128), te = (int)(ix->offsets[c + 1] / 128);
+    if (te <= tb) continue;
+    const int la = two ? std::max(1, (int)std::ceil((te - tb) * kPhaseA)) : 0;
+    segA.push_back({tb, tb + std::min(la, te - tb)});
+    segB.push_back({tb + std::min(la, te - tb), te});
+    segc.push_back(c);
+  }
+  const int G = nsm;
+  const int slots_dep = (G + pl->QP - 1) / pl->QP + 2;
+  const int ns_smem = (int)((200 * 1024 - (size_t)ix->D * 4) / ((size_t)pl->Cap * 8));
+  const int ns_limit = std::min(64, ns_smem);
+  if (ns_limit < 1) return fail(LV_EUNSUPPORTED, "R=%d too large for the merge", R);
+  // with few query pairs the dependency distance exceeds the slot limit: then every chunk gets
+  // its own slot (no dependency) and the chunk count is capped instead
+  const int max_chunks = slots_dep > ns_limit ? ns_limit : (1 << 30);
+  make_chunks(segA, segc, pl->QP, G, max_chunks, &pl->chunks[0]);
+  make_chunks(segB, segc, pl->QP, G, max_chunks, &pl->chunks[1]);
+  pl->P[0] = (int)(pl->chunks[0].size() / 3);
+  pl->P[1] = (int)(pl->chunks[1].size() / 3);
+  const int pmax = std::max(pl->P[0], pl->P[1]);
+  int ns = std::min(pmax, slots_dep);
+  ns = std::min(ns, ns_limit);
+  if (ns < std::min(pmax, slots_dep)) {
+    // fewer slots than the dependency distance needs: cap the chunk count instead
+    return fail(LV_EUNSUPPORTED, "plan: %d slots needed, %d fit", std::min(pmax, slots_dep), ns);
+  }
+  pl->NS = ns;
+  pl->grid = (int)std::min<int64_t>(G, (int64_t)pmax * pl->QP);
   const size_t budget = 227 * 1024 - 1024 - 256;
-  const size_t a_bytes = 2 * (size_t)ix->d * 256;
-  const size_t stage_bytes = (size_t)ix->d * 256;
-  int st = (int)std::min<size_t>(8, (budget - a_bytes - 1024) / stage_bytes);
+  int st = 8;
   while (st >= 2 && lv::score_smem_bytes(ix->d, st) > budget) --st;
   if (st < 2) return fail(LV_EUNSUPPORTED, "d=%d leaves no room for a 2-stage pipeline", ix->d);
   pl->stages = st;
@@ -409,7 +431,8 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
   const size_t fsz = ix->full == LV_F16 ? 2 : 4;
   if (cudaMalloc(&ix->X_full, fsz * n * ix->D) != cudaSuccess) return fail(LV_ENOMEM, "X_full");
   LV_CUDA(lv::launch_convert(X, x_dtype == LV_F16, ix->X_full, ix->full == LV_F16, n * ix->D, s));
-  lv_status ts = make_tmap(&ix->tmap_xlow, ix->X_low, ix->n_pad, ix->d, (ix->d % 64 == 0) ? 64 : 32, ix->low == LV_BF16);
+  lv_status ts = make_tmap(&ix->tmap_xlow, ix->X_low, ix->n_pad, ix->d, (ix->d % 64 == 0) ? 64 : 32, ix->low == LV_BF16,
+                           lv::score_tile_rows(ix->d));
   LV_CUDA(cudaStreamSynchronize(s));
   cudaFree(dwrow);
   return ts;
@@ -439,9 +462,10 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   if (st) return st;
   const int Cd = ix->C * ix->d;
   // workspace
+  const size_t nchunk_ints = pl.chunks[0].size() + pl.chunks[1].size();
   const size_t need = ((size_t)pl.m_pad * Cd * 2 + 256) + ((size_t)pl.NS * pl.m_pad * pl.Cap * 8 + 256) +
                       ((size_t)pl.NS * pl.m_pad * 4 + 256) + ((size_t)pl.NS * pl.m_pad * 8 + 256) +
-                      ((size_t)pl.P * pl.QP * 4 + 256) + (pl.chunks.size() * 4 + 256);
+                      ((size_t)(pl.P[0] + pl.P[1]) * pl.QP * 4 + 512) + (nchunk_ints * 4 + 512);
   if (need > ix->ws_bytes) {
     cudaFree(ix->ws);
     ix->ws = nullptr;
@@ -455,9 +479,13 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   uint8_t* zero_lo = p;
   int32_t* cnt = carve<int32_t>(p, (size_t)pl.NS * pl.m_pad);
   uint64_t* tau = carve<uint64_t>(p, (size_t)pl.NS * pl.m_pad);
-  int32_t* done = carve<int32_t>(p, (size_t)pl.P * pl.QP);
+  int32_t* done[2];
+  done[0] = carve<int32_t>(p, (size_t)pl.P[0] * pl.QP + 1);
+  done[1] = carve<int32_t>(p, (size_t)pl.P[1] * pl.QP + 1);
   uint8_t* zero_hi = p;
-  int32_t* chunk_info = carve<int32_t>(p, pl.chunks.size());
+  int32_t* chunk_info[2];
+  chunk_info[0] = carve<int32_t>(p, pl.chunks[0].size() + 1);
+  chunk_info[1] = carve<int32_t>(p, pl.chunks[1].size() + 1);
 
   cudaEvent_t ev[4];
   const bool timing = dbg && dbg->timing;
@@ -466,42 +494,50 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     LV_CUDA(cudaEventRecord(ev[0], s));
   }
   int launches = 0;
-  LV_CUDA(cudaMemcpyAsync(chunk_info, pl.chunks.data(), pl.chunks.size() * 4, cudaMemcpyHostToDevice, s));
+  for (int ph = 0; ph < 2; ++ph)
+    if (pl.P[ph])
+      LV_CUDA(cudaMemcpyAsync(chunk_info[ph], pl.chunks[ph].data(), pl.chunks[ph].size() * 4, cudaMemcpyHostToDevice, s));
   LV_CUDA(cudaMemsetAsync(zero_lo, 0, zero_hi - zero_lo, s));
   // K1 projection (rows >= m are zero)
   LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, pl.m_pad, ix->A, ix->D, nullptr, Cd, Qp, ix->low, Cd, pl.m_pad, s));
   ++launches;
   if (timing) LV_CUDA(cudaEventRecord(ev[1], s));
-  // K2/K3 fused scan
-  CUtensorMap tmap_qp;
-  const int ch = (ix->d % 64 == 0) ? 64 : 32;
-  st = make_tmap(&tmap_qp, Qp, pl.m_pad, Cd, ch, ix->low == LV_BF16);
-  if (st) return st;
+  // K2/K3 fused scan: phase A, exact threshold merge, phase B
   lv::ScoreArgs sa;
+  sa.Qp = Qp;
+  sa.C = ix->C;
   sa.m = (int)m;
   sa.m_pad = pl.m_pad;
   sa.QP = pl.QP;
   sa.d = ix->d;
   sa.R = R;
-  sa.P = pl.P;
   sa.NS = pl.NS;
   sa.Cap = pl.Cap;
   sa.stages = pl.stages;
-  sa.chunk_info = chunk_info;
   sa.tile_valid = ix->tile_valid;
   sa.perm = ix->C > 1 ? ix->perm : nullptr;
   sa.cand = cand;
   sa.cnt = cnt;
   sa.tau = tau;
-  sa.done = done;
   sa.raw = dbg ? dbg->raw_scores : nullptr;
   sa.n_pad = ix->n_pad;
   {
     const char* f = getenv("LV_DEBUG_SCAN_FLAGS");
     sa.flags = f ? atoi(f) : 0;
   }
-  LV_CUDA(lv::launch_score(&tmap_qp, &ix->tmap_xlow, sa, ix->low == LV_BF16, pl.grid, pl.smem, s));
-  ++launches;
+  for (int ph = 0; ph < 2; ++ph) {
+    if (!pl.P[ph]) continue;
+    sa.P = pl.P[ph];
+    sa.chunk_info = chunk_info[ph];
+    sa.done = done[ph];
+    const int grid = (int)std::min<int64_t>(pl.grid, (int64_t)sa.P * pl.QP);
+    LV_CUDA(lv::launch_score(&ix->tmap_xlow, sa, ix->low == LV_BF16, grid, pl.smem, s));
+    ++launches;
+    if (ph == 0 && pl.P[1]) {
+      LV_CUDA(lv::launch_tau_merge(cand, cnt, tau, pl.NS, (int)m, pl.m_pad, pl.Cap, R, s));
+      ++launches;
+    }
+  }
   if (timing) LV_CUDA(cudaEventRecord(ev[2], s));
   // K4/K5 select + re-rank + top-k
   lv::RerankArgs ra;
@@ -540,7 +576,7 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   if (dbg) {
     dbg->launches = launches;
     dbg->slots = pl.NS;
-    dbg->units = pl.P * pl.QP;
+    dbg->units = (pl.P[0] + pl.P[1]) * pl.QP;
     dbg->grid = pl.grid;
   }
   return LV_OK;

@@ -25,7 +25,8 @@ struct ScanPlan {
 };
 
 struct ScoreArgs {
-  int m, m_pad, QP, d, R, P, NS, Cap, stages;
+  int m, m_pad, QP, d, C, R, P, NS, Cap, stages;
+  const void* Qp;              // [m_pad, C*d] low dtype (q'_{j,c} for every c)
   const int32_t* chunk_info;   // [P][3]: tile_begin, tile_end, cluster
   const int32_t* tile_valid;   // [n_tiles]
   const int32_t* perm;         // [n_pad] or nullptr (identity)
@@ -38,8 +39,9 @@ struct ScoreArgs {
   int flags;                   // debug: bit0 = epilogue skips top-R (MMA/TMA throughput probe)
 };
 
-cudaError_t launch_score(const CUtensorMap* tmap_qp, const CUtensorMap* tmap_xlow, const ScoreArgs& a,
-                         bool bf16, int grid, size_t smem, cudaStream_t s);
+cudaError_t launch_score(const CUtensorMap* tmap_xlow, const ScoreArgs& a, bool bf16, int grid, size_t smem,
+                         cudaStream_t s);
+int score_tile_rows(int d);
 
 struct RerankArgs {
   int m, m_pad, D, R, k, NS, Cap;
@@ -54,6 +56,8 @@ struct RerankArgs {
   float* cand_scores;          // [m, R] or nullptr
 };
 cudaError_t launch_select_rerank(const RerankArgs& a, cudaStream_t s);
+cudaError_t launch_tau_merge(uint64_t* cand, int32_t* cnt, uint64_t* tau, int NS, int m, int m_pad, int Cap, int R,
+                             cudaStream_t s);
 
 // out[r, j] = RNE(sum_k in[rowidx[r], k] * W[wrow(r) + j, k]) for 64-row tiles.
 cudaError_t launch_rows_gemm(const void* in, int in_f16, int64_t ld_in, const int32_t* rowidx, int64_t rows_valid,

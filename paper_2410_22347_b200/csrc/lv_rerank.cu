@@ -33,42 +33,40 @@ LV_DEVINL void block_sort_desc(uint64_t* s, int n) {
   __syncthreads();
 }
 
-template <bool kF16>
-__global__ void __launch_bounds__(kRrThreads) k_select_rerank(const RerankArgs a) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  const int q = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ uint64_t sel[kMaxR];
-  __shared__ uint64_t fin[kMaxR];
+// Loads every candidate key of query q from its NS slots into smem `keys` and returns the R-th
+// largest (8-bit MSB radix select; keys are unique so the result is exact).  *total = #keys.
+// Returns 0 when the query has fewer than R keys (then every key is selected).
+__device__ uint64_t gather_select(const uint64_t* cand, const int32_t* cntv, int NS, int m_pad, int Cap, int q, int Rq,
+                                  uint64_t* keys, int* total_out) {
   __shared__ int hist[256];
   __shared__ int s_off[65];
-  __shared__ int s_total, s_sel, s_want;
+  __shared__ int s_total, s_want;
   __shared__ uint64_t s_prefix;
-  float* sQ = reinterpret_cast<float*>(smem_raw);
-  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw + ((a.D * 4 + 15) / 16) * 16);
-
-  for (int i = tid; i < a.D; i += blockDim.x) sQ[i] = a.Q[(size_t)q * a.D + i];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     int tot = 0;
-    for (int s = 0; s < a.NS; ++s) {
+    for (int s = 0; s < NS; ++s) {
       s_off[s] = tot;
-      tot += a.cnt[(size_t)s * a.m_pad + q];
+      tot += cntv[(size_t)s * m_pad + q];
     }
-    s_off[a.NS] = tot;
+    s_off[NS] = tot;
     s_total = tot;
   }
   __syncthreads();
   const int total = s_total;
-  for (int s = 0; s < a.NS; ++s) {
+  *total_out = total;
+  for (int s = 0; s < NS; ++s) {
     const int c = s_off[s + 1] - s_off[s];
-    const uint64_t* src = a.cand + ((size_t)s * a.m_pad + q) * (size_t)a.Cap;
+    const uint64_t* src = cand + ((size_t)s * m_pad + q) * (size_t)Cap;
     for (int i = tid; i < c; i += blockDim.x) keys[s_off[s] + i] = src[i];
   }
-  // ---- radix select of the R-th largest key (8 bits per pass, MSB first)
-  const int R = min(a.R, total);
+  if (total <= Rq) {
+    __syncthreads();
+    return 0ull;
+  }
   if (tid == 0) {
     s_prefix = 0ull;
-    s_want = R;
+    s_want = Rq;
   }
   uint64_t mask = 0ull;
   for (int pass = 0; pass < 8; ++pass) {
@@ -97,8 +95,7 @@ __global__ void __launch_bounds__(kRrThreads) k_select_rerank(const RerankArgs a
       }
       const int want = s_want;
       const int excl = incl - sum;
-      const bool here = (excl < want) && (incl >= want);
-      if (here) {
+      if ((excl < want) && (incl >= want)) {
         int cum = excl, dg = 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -115,7 +112,65 @@ __global__ void __launch_bounds__(kRrThreads) k_select_rerank(const RerankArgs a
     mask |= (255ull << shift);
     __syncthreads();
   }
-  const uint64_t kth = s_prefix;   // exact R-th largest key (keys are unique)
+  return s_prefix;
+}
+
+// Threshold merge between the two scan phases: per query, the exact R-th key over the union of
+// its slots (a valid lower bound of the final R-th key); every slot drops keys below it and
+// adopts it as its threshold, so phase B starts from a threshold close to its final value.
+__global__ void __launch_bounds__(kRrThreads) k_tau_merge(uint64_t* cand, int32_t* cntv, uint64_t* tau, int NS, int m,
+                                                          int m_pad, int Cap, int R) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw);
+  const int q = blockIdx.x;
+  int total = 0;
+  const uint64_t kth = gather_select(cand, cntv, NS, m_pad, Cap, q, R, keys, &total);
+  if (kth == 0ull) return;
+  __shared__ int s_cnt;
+  __shared__ int s_offs[65];
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int t = 0; t < NS; ++t) {
+      s_offs[t] = o;
+      o += cntv[(size_t)t * m_pad + q];
+    }
+    s_offs[NS] = o;
+  }
+  __syncthreads();
+  for (int s = 0; s < NS; ++s) {
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const size_t si = (size_t)s * m_pad + q;
+    const int off = s_offs[s], c = s_offs[s + 1] - s_offs[s];
+    uint64_t* dst = cand + si * (size_t)Cap;
+    // keys of this slot are already in smem; rewrite the survivors (order irrelevant)
+    for (int i = threadIdx.x; i < c; i += blockDim.x) {
+      const uint64_t k = keys[off + i];
+      if (k >= kth) dst[atomicAdd(&s_cnt, 1)] = k;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      cntv[si] = s_cnt;
+      tau[si] = (tau[si] > kth) ? tau[si] : kth;
+    }
+  }
+}
+
+template <bool kF16>
+__global__ void __launch_bounds__(kRrThreads) k_select_rerank(const RerankArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int q = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ uint64_t sel[kMaxR];
+  __shared__ uint64_t fin[kMaxR];
+  __shared__ int s_sel;
+  float* sQ = reinterpret_cast<float*>(smem_raw);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw + ((a.D * 4 + 15) / 16) * 16);
+
+  for (int i = tid; i < a.D; i += blockDim.x) sQ[i] = a.Q[(size_t)q * a.D + i];
+  int total = 0;
+  const uint64_t kth = gather_select(a.cand, a.cnt, a.NS, a.m_pad, a.Cap, q, a.R, keys, &total);
+  const int R = min(a.R, total);
   // ---- gather the R selected keys, sort them (deterministic candidate order)
   int npow = 1;
   while (npow < R) npow <<= 1;
@@ -172,6 +227,15 @@ __global__ void __launch_bounds__(kRrThreads) k_select_rerank(const RerankArgs a
     a.ids[(size_t)q * a.k + i] = key_id(fin[i]);
     a.scores[(size_t)q * a.k + i] = key_score(fin[i]);
   }
+}
+
+cudaError_t launch_tau_merge(uint64_t* cand, int32_t* cnt, uint64_t* tau, int NS, int m, int m_pad, int Cap, int R,
+                             cudaStream_t s) {
+  const size_t smem = (size_t)NS * Cap * 8;
+  cudaError_t e = cudaFuncSetAttribute(k_tau_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_tau_merge<<<m, kRrThreads, smem, s>>>(cand, cnt, tau, NS, m, m_pad, Cap, R);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_select_rerank(const RerankArgs& a, cudaStream_t s) {
