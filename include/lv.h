@@ -138,7 +138,7 @@ lv_status lv_project_queries(const lv_index* index, const float* Q, int64_t m, v
  *   Q       device fp32 [m, D]
  *   ids     device int32 [m, k] out (original database ids);  scores device fp32 [m, k] out (r_ji)
  *   dbg     NULL or lv_search_debug* (HOST struct; its pointers are device pointers)
- * Constraints: 1 <= k <= R <= n, R <= 512, m >= 1.  The index must be encoded.
+ * Constraints: 1 <= k <= R <= n, R <= 256, m >= 1.  The index must be encoded.
  * Not thread-safe per index (shared workspace).  Errors: LV_EINVAL, LV_ENOMEM, LV_ECUDA.
  */
 lv_status lv_search(lv_index* index, const float* Q, int64_t m, int32_t k, int32_t R,

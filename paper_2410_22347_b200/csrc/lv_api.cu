@@ -109,8 +109,8 @@ T* carve(uint8_t*& p, size_t count) {
 struct Plan {
   int m_pad, QP, NS, Cap, grid, stages;
   size_t smem;
-  std::vector<int32_t> chunks[2];   // phase A / phase B: P x {tile_begin, tile_end, cluster}
-  int P[2] = {0, 0};
+  std::vector<std::vector<int32_t>> chunks;   // per scan stage: P x {tile_begin, tile_end, cluster}
+  int total_units = 0;
 };
 
 // Chunks of the given segments (tile ranges) so that units = P * QP spread evenly over the grid.
@@ -152,47 +152,82 @@ void make_chunks(const std::vector<std::pair<int, int>>& segs, const std::vector
   }
 }
 
-// Work decomposition of the scan: phase A covers the first kPhaseA of every
-// cluster segment, phase B the rest (after the exact per-query threshold merge).
-constexpr double kPhaseA = 0.08;
-constexpr int kMinTilesTwoPhase = 256;
-
+// Work decomposition of the scan.  The database is scanned in stages of
+// geometrically growing size; between stages an exact merge gives every query the R-th best key
+// seen so far as its threshold.  Stage sizes are chosen so that a slot's expected appends within
+// a stage (g * R / NS) stay well below its capacity: thresholds are tight from the second stage
+// on and slot compactions are rare.
 lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
-  pl->QP = (int)((m + 255) / 256);
-  pl->m_pad = pl->QP * 256;
-  pl->Cap = (R + 31) / 32 * 32 + 128;
+  pl->QP = (int)((m + 127) / 128);   // 128-query tiles (units pair a tile with a database chunk)
+  pl->m_pad = pl->QP * 128;
+  pl->Cap = std::min(384, (R + 31) / 32 * 32 + 160);
+  if (pl->Cap < R + 96) return fail(LV_EUNSUPPORTED, "R=%d too large (R <= 256)", R);
   const int ntiles = (int)(ix->n_pad / 128);
-  const bool two = ntiles >= kMinTilesTwoPhase;
-  std::vector<std::pair<int, int>> segA, segB;
+  const int G = nsm;
+  const int slots_dep = (G + pl->QP - 1) / pl->QP + 2;
+  // every slot is split in four sub-slots (one per epilogue column quarter): 4*NS lists per query
+  const int ns_smem = (int)((200 * 1024 - (size_t)ix->D * 4) / ((size_t)pl->Cap * 8)) / 4;
+  const int ns_limit = std::min(16, ns_smem);
+  if (ns_limit < 1) return fail(LV_EUNSUPPORTED, "R=%d too large for the merge", R);
+  const int max_chunks = slots_dep > ns_limit ? ns_limit : (1 << 30);
+  const int ns_target = std::min(slots_dep, ns_limit);
+  // segment tile ranges
+  std::vector<std::pair<int, int>> seg;
   std::vector<int> segc;
+  int64_t ntot = 0;
   for (int c = 0; c < ix->C; ++c) {
     const int tb = (int)(ix->offsets[c] / 128), te = (int)(ix->offsets[c + 1] / 128);
     if (te <= tb) continue;
-    const int la = two ? std::max(1, (int)std::ceil((te - tb) * kPhaseA)) : 0;
-    segA.push_back({tb, tb + std::min(la, te - tb)});
-    segB.push_back({tb + std::min(la, te - tb), te});
+    seg.push_back({tb, te});
     segc.push_back(c);
+    ntot += te - tb;
   }
-  const int G = nsm;
-  const int slots_dep = (G + pl->QP - 1) / pl->QP + 2;
-  const int ns_smem = (int)((200 * 1024 - (size_t)ix->D * 4) / ((size_t)pl->Cap * 8));
-  const int ns_limit = std::min(64, ns_smem);
-  if (ns_limit < 1) return fail(LV_EUNSUPPORTED, "R=%d too large for the merge", R);
-  // with few query pairs the dependency distance exceeds the slot limit: then every chunk gets
-  // its own slot (no dependency) and the chunk count is capped instead
-  const int max_chunks = slots_dep > ns_limit ? ns_limit : (1 << 30);
-  make_chunks(segA, segc, pl->QP, G, max_chunks, &pl->chunks[0]);
-  make_chunks(segB, segc, pl->QP, G, max_chunks, &pl->chunks[1]);
-  pl->P[0] = (int)(pl->chunks[0].size() / 3);
-  pl->P[1] = (int)(pl->chunks[1].size() / 3);
-  const int pmax = std::max(pl->P[0], pl->P[1]);
-  int ns = std::min(pmax, slots_dep);
-  ns = std::min(ns, ns_limit);
-  if (ns < std::min(pmax, slots_dep)) {
-    // fewer slots than the dependency distance needs: cap the chunk count instead
-    return fail(LV_EUNSUPPORTED, "plan: %d slots needed, %d fit", std::min(pmax, slots_dep), ns);
+  // stage boundaries as cumulative fractions of every segment
+  std::vector<double> cum;   // cumulative fraction after each stage
+  if (ntiles >= 64) {
+    const double rows = (double)ntot * 128.0;
+    const double lists = 4.0 * ns_target;   // independent candidate lists per query
+    // stage 0 only has to produce R keys per query: keep it (and so the first merge) small
+    double c0 = std::max(2.0 * R, lists * 32.0);
+    // growth per stage: bounded by the slot capacity and kept small so that most of the
+    // database is scanned with a threshold close to the final R-th score
+    double g = std::min(6.0, std::max(2.0, 0.8 * (pl->Cap - 64) * lists / (double)R));
+    double acc = c0;
+    while (acc < rows * 0.999) {
+      cum.push_back(acc / rows);
+      acc = std::min(rows, acc * (1.0 + g));
+    }
   }
-  pl->NS = ns;
+  cum.push_back(1.0);
+  pl->chunks.clear();
+  std::vector<int> done_upto(seg.size());
+  for (size_t i = 0; i < seg.size(); ++i) done_upto[i] = seg[i].first;
+  for (size_t k = 0; k < cum.size(); ++k) {
+    std::vector<std::pair<int, int>> part;
+    std::vector<int> partc;
+    for (size_t i = 0; i < seg.size(); ++i) {
+      const int len = seg[i].second - seg[i].first;
+      int upto = (k + 1 == cum.size()) ? seg[i].second
+                                       : seg[i].first + std::max(1, (int)std::ceil(len * cum[k]));
+      upto = std::min(upto, seg[i].second);
+      if (upto > done_upto[i]) {
+        part.push_back({done_upto[i], upto});
+        partc.push_back(segc[i]);
+        done_upto[i] = upto;
+      }
+    }
+    if (part.empty()) continue;
+    std::vector<int32_t> ch;
+    make_chunks(part, partc, pl->QP, G, max_chunks, &ch);
+    if (!ch.empty()) pl->chunks.push_back(ch);
+  }
+  int pmax = 0;
+  pl->total_units = 0;
+  for (auto& ch : pl->chunks) {
+    pmax = std::max(pmax, (int)(ch.size() / 3));
+    pl->total_units += (int)(ch.size() / 3) * pl->QP;
+  }
+  pl->NS = std::min(std::min(pmax, slots_dep), ns_limit);
   pl->grid = (int)std::min<int64_t>(G, (int64_t)pmax * pl->QP);
   const size_t budget = 227 * 1024 - 1024 - 256;
   int st = 8;
@@ -454,7 +489,7 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   if (st) return st;
   if (!ix || !Q || !ids || !scores || m <= 0) return fail(LV_EINVAL, "lv_search: bad arguments");
   if (ix->n <= 0) return fail(LV_EINVAL, "lv_search: index not encoded");
-  if (k < 1 || k > R || R > 512 || R > ix->n) return fail(LV_EINVAL, "lv_search: need 1 <= k <= R <= min(n, 512)");
+  if (k < 1 || k > R || R > 256 || R > ix->n) return fail(LV_EINVAL, "lv_search: need 1 <= k <= R <= min(n, 256)");
   if (m > (1 << 24)) return fail(LV_EINVAL, "lv_search: m too large");
   cudaStream_t s = (cudaStream_t)stream;
   Plan pl;
@@ -462,10 +497,15 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   if (st) return st;
   const int Cd = ix->C * ix->d;
   // workspace
-  const size_t nchunk_ints = pl.chunks[0].size() + pl.chunks[1].size();
-  const size_t need = ((size_t)pl.m_pad * Cd * 2 + 256) + ((size_t)pl.NS * pl.m_pad * pl.Cap * 8 + 256) +
-                      ((size_t)pl.NS * pl.m_pad * 4 + 256) + ((size_t)pl.NS * pl.m_pad * 8 + 256) +
-                      ((size_t)(pl.P[0] + pl.P[1]) * pl.QP * 4 + 512) + (nchunk_ints * 4 + 512);
+  size_t nchunk_ints = 0, ndone = 0;
+  for (auto& ch : pl.chunks) {
+    nchunk_ints += ch.size() + 1;
+    ndone += ch.size() / 3 * pl.QP + 1;
+  }
+  const int NS2 = 4 * pl.NS;   // sub-slots per query
+  const size_t need = ((size_t)pl.m_pad * Cd * 2 + 256) + ((size_t)NS2 * pl.m_pad * pl.Cap * 8 + 256) +
+                      ((size_t)NS2 * pl.m_pad * 4 + 256) + ((size_t)NS2 * pl.m_pad * 8 + 256) +
+                      (ndone * 4 + 256 * (pl.chunks.size() + 1)) + (nchunk_ints * 4 + 256 * (pl.chunks.size() + 1));
   if (need > ix->ws_bytes) {
     cudaFree(ix->ws);
     ix->ws = nullptr;
@@ -475,17 +515,15 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   }
   uint8_t* p = reinterpret_cast<uint8_t*>(ix->ws);
   void* Qp = carve<uint16_t>(p, (size_t)pl.m_pad * Cd);
-  uint64_t* cand = carve<uint64_t>(p, (size_t)pl.NS * pl.m_pad * pl.Cap);
+  uint64_t* cand = carve<uint64_t>(p, (size_t)NS2 * pl.m_pad * pl.Cap);
   uint8_t* zero_lo = p;
-  int32_t* cnt = carve<int32_t>(p, (size_t)pl.NS * pl.m_pad);
-  uint64_t* tau = carve<uint64_t>(p, (size_t)pl.NS * pl.m_pad);
-  int32_t* done[2];
-  done[0] = carve<int32_t>(p, (size_t)pl.P[0] * pl.QP + 1);
-  done[1] = carve<int32_t>(p, (size_t)pl.P[1] * pl.QP + 1);
+  int32_t* cnt = carve<int32_t>(p, (size_t)NS2 * pl.m_pad);
+  uint64_t* tau = carve<uint64_t>(p, (size_t)NS2 * pl.m_pad);
+  std::vector<int32_t*> done(pl.chunks.size());
+  for (size_t k = 0; k < pl.chunks.size(); ++k) done[k] = carve<int32_t>(p, pl.chunks[k].size() / 3 * pl.QP + 1);
   uint8_t* zero_hi = p;
-  int32_t* chunk_info[2];
-  chunk_info[0] = carve<int32_t>(p, pl.chunks[0].size() + 1);
-  chunk_info[1] = carve<int32_t>(p, pl.chunks[1].size() + 1);
+  std::vector<int32_t*> chunk_info(pl.chunks.size());
+  for (size_t k = 0; k < pl.chunks.size(); ++k) chunk_info[k] = carve<int32_t>(p, pl.chunks[k].size() + 1);
 
   cudaEvent_t ev[4];
   const bool timing = dbg && dbg->timing;
@@ -494,9 +532,8 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     LV_CUDA(cudaEventRecord(ev[0], s));
   }
   int launches = 0;
-  for (int ph = 0; ph < 2; ++ph)
-    if (pl.P[ph])
-      LV_CUDA(cudaMemcpyAsync(chunk_info[ph], pl.chunks[ph].data(), pl.chunks[ph].size() * 4, cudaMemcpyHostToDevice, s));
+  for (size_t k = 0; k < pl.chunks.size(); ++k)
+    LV_CUDA(cudaMemcpyAsync(chunk_info[k], pl.chunks[k].data(), pl.chunks[k].size() * 4, cudaMemcpyHostToDevice, s));
   LV_CUDA(cudaMemsetAsync(zero_lo, 0, zero_hi - zero_lo, s));
   // K1 projection (rows >= m are zero)
   LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, pl.m_pad, ix->A, ix->D, nullptr, Cd, Qp, ix->low, Cd, pl.m_pad, s));
@@ -525,16 +562,15 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     const char* f = getenv("LV_DEBUG_SCAN_FLAGS");
     sa.flags = f ? atoi(f) : 0;
   }
-  for (int ph = 0; ph < 2; ++ph) {
-    if (!pl.P[ph]) continue;
-    sa.P = pl.P[ph];
-    sa.chunk_info = chunk_info[ph];
-    sa.done = done[ph];
+  for (size_t k = 0; k < pl.chunks.size(); ++k) {
+    sa.P = (int)(pl.chunks[k].size() / 3);
+    sa.chunk_info = chunk_info[k];
+    sa.done = done[k];
     const int grid = (int)std::min<int64_t>(pl.grid, (int64_t)sa.P * pl.QP);
     LV_CUDA(lv::launch_score(&ix->tmap_xlow, sa, ix->low == LV_BF16, grid, pl.smem, s));
     ++launches;
-    if (ph == 0 && pl.P[1]) {
-      LV_CUDA(lv::launch_tau_merge(cand, cnt, tau, pl.NS, (int)m, pl.m_pad, pl.Cap, R, s));
+    if (k + 1 < pl.chunks.size()) {
+      LV_CUDA(lv::launch_tau_merge(cand, cnt, tau, NS2, (int)m, pl.m_pad, pl.Cap, R, s));
       ++launches;
     }
   }
@@ -546,7 +582,7 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   ra.D = ix->D;
   ra.R = R;
   ra.k = k;
-  ra.NS = pl.NS;
+  ra.NS = NS2;
   ra.Cap = pl.Cap;
   ra.cand = cand;
   ra.cnt = cnt;
@@ -575,8 +611,8 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   }
   if (dbg) {
     dbg->launches = launches;
-    dbg->slots = pl.NS;
-    dbg->units = (pl.P[0] + pl.P[1]) * pl.QP;
+    dbg->slots = NS2;
+    dbg->units = pl.total_units;
     dbg->grid = pl.grid;
   }
   return LV_OK;

@@ -37,4 +37,14 @@ LV_DEVINL uint64_t make_key(float s, int32_t id) {
 LV_DEVINL int32_t key_id(uint64_t k) { return (int32_t)(~(uint32_t)(k & 0xffffffffu)); }
 LV_DEVINL float key_score(uint64_t k) { return unord_f32((uint32_t)(k >> 32)); }
 
+// Histogram increment aggregated over the active lanes of the warp that hit the same bin
+// (radix digits of similar scores collide heavily; one shared-memory atomic per distinct bin).
+// Every active lane must call it; bin < 0 means "no increment".
+LV_DEVINL void warp_hist_add(int* hist, int bin) {
+  const uint32_t act = __activemask();
+  const uint32_t same = __match_any_sync(act, bin);
+  const int lane = threadIdx.x & 31;
+  if (bin >= 0 && (same & ((1u << lane) - 1u)) == 0u) atomicAdd(&hist[bin], __popc(same));
+}
+
 }  // namespace lv

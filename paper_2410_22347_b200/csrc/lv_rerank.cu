@@ -37,7 +37,7 @@ LV_DEVINL void block_sort_desc(uint64_t* s, int n) {
 // largest (8-bit MSB radix select; keys are unique so the result is exact).  *total = #keys.
 // Returns 0 when the query has fewer than R keys (then every key is selected).
 __device__ uint64_t gather_select(const uint64_t* cand, const int32_t* cntv, int NS, int m_pad, int Cap, int q, int Rq,
-                                  uint64_t* keys, int* total_out) {
+                                  uint64_t* keys, int* total_out, int npasses = 8) {
   __shared__ int hist[256];
   __shared__ int s_off[65];
   __shared__ int s_total, s_want;
@@ -69,14 +69,15 @@ __device__ uint64_t gather_select(const uint64_t* cand, const int32_t* cntv, int
     s_want = Rq;
   }
   uint64_t mask = 0ull;
-  for (int pass = 0; pass < 8; ++pass) {
+  for (int pass = 0; pass < npasses; ++pass) {
     const int shift = 56 - 8 * pass;
     for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     const uint64_t prefix = s_prefix;
-    for (int i = tid; i < total; i += blockDim.x) {
-      const uint64_t k = keys[i];
-      if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1);
+    for (int i0 = 0; i0 < total; i0 += blockDim.x) {
+      const int i = i0 + tid;
+      const uint64_t k = i < total ? keys[i] : 0ull;
+      warp_hist_add(hist, (i < total && (k & mask) == prefix) ? (int)((k >> shift) & 255) : -1);
     }
     __syncthreads();
     if (warp == 0) {
@@ -115,19 +116,35 @@ __device__ uint64_t gather_select(const uint64_t* cand, const int32_t* cntv, int
   return s_prefix;
 }
 
-// Threshold merge between the two scan phases: per query, the exact R-th key over the union of
-// its slots (a valid lower bound of the final R-th key); every slot drops keys below it and
-// adopts it as its threshold, so phase B starts from a threshold close to its final value.
-__global__ void __launch_bounds__(kRrThreads) k_tau_merge(uint64_t* cand, int32_t* cntv, uint64_t* tau, int NS, int m,
-                                                          int m_pad, int Cap, int R) {
+// Threshold merge between scan stages (one CTA per query, keys staged in smem): the 16-bit key
+// prefix b of the bin holding the R-th largest key over the union of the query's lists (two
+// 8-bit radix passes).  At least R keys have prefix >= b, so (b << 48) - 1 is a valid threshold
+// (a lower bound of the final R-th key): every list drops keys below it and adopts it, so the
+// next stage starts tight.
+constexpr int kMergeThreads = 128;
+constexpr int kMergeMaxKeys = 2048;   // 16 KB staging per query
+__global__ void __launch_bounds__(kMergeThreads) k_tau_merge(uint64_t* cand, int32_t* cntv, uint64_t* tau, int NS, int m,
+                                                            int m_pad, int Cap, int R) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw);
-  const int q = blockIdx.x;
-  int total = 0;
-  const uint64_t kth = gather_select(cand, cntv, NS, m_pad, Cap, q, R, keys, &total);
-  if (kth == 0ull) return;
-  __shared__ int s_cnt;
   __shared__ int s_offs[65];
+  const int q = blockIdx.x;
+  // queries whose lists hold more keys than the staging buffer keep their thresholds (only the
+  // pruning of the next stage is lost, never correctness)
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int t = 0; t < NS; ++t) tot += cntv[(size_t)t * m_pad + q];
+    s_offs[64] = tot;
+  }
+  __syncthreads();
+  if (s_offs[64] > kMergeMaxKeys) return;
+  __syncthreads();
+  int total = 0;
+  const uint64_t pre = gather_select(cand, cntv, NS, m_pad, Cap, q, R, keys, &total, 2);
+  if (total <= R) return;
+  const uint32_t prefix = (uint32_t)(pre >> 48);
+  if (prefix == 0u) return;
+  const uint64_t thr = ((uint64_t)prefix << 48) - 1ull;
   if (threadIdx.x == 0) {
     int o = 0;
     for (int t = 0; t < NS; ++t) {
@@ -137,21 +154,25 @@ __global__ void __launch_bounds__(kRrThreads) k_tau_merge(uint64_t* cand, int32_
     s_offs[NS] = o;
   }
   __syncthreads();
-  for (int s = 0; s < NS; ++s) {
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
+  // each warp rewrites whole lists (stable, from smem)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int s = warp; s < NS; s += kMergeThreads / 32) {
     const size_t si = (size_t)s * m_pad + q;
-    const int off = s_offs[s], c = s_offs[s + 1] - s_offs[s];
     uint64_t* dst = cand + si * (size_t)Cap;
-    // keys of this slot are already in smem; rewrite the survivors (order irrelevant)
-    for (int i = threadIdx.x; i < c; i += blockDim.x) {
-      const uint64_t k = keys[off + i];
-      if (k >= kth) dst[atomicAdd(&s_cnt, 1)] = k;
+    const int off = s_offs[s], c = s_offs[s + 1] - s_offs[s];
+    int w = 0;
+    for (int i0 = 0; i0 < c; i0 += 32) {
+      const int i = i0 + lane;
+      const uint64_t k = i < c ? keys[off + i] : 0ull;
+      const bool keep = k > thr;
+      const uint32_t b = __ballot_sync(0xffffffffu, keep);
+      if (keep) dst[w + __popc(b & lt)] = k;
+      w += __popc(b);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      cntv[si] = s_cnt;
-      tau[si] = (tau[si] > kth) ? tau[si] : kth;
+    if (lane == 0) {
+      cntv[si] = w;
+      if (tau[si] < thr) tau[si] = thr;
     }
   }
 }
@@ -231,10 +252,8 @@ __global__ void __launch_bounds__(kRrThreads) k_select_rerank(const RerankArgs a
 
 cudaError_t launch_tau_merge(uint64_t* cand, int32_t* cnt, uint64_t* tau, int NS, int m, int m_pad, int Cap, int R,
                              cudaStream_t s) {
-  const size_t smem = (size_t)NS * Cap * 8;
-  cudaError_t e = cudaFuncSetAttribute(k_tau_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_tau_merge<<<m, kRrThreads, smem, s>>>(cand, cnt, tau, NS, m, m_pad, Cap, R);
+  const size_t smem = (size_t)kMergeMaxKeys * 8;
+  k_tau_merge<<<m, kMergeThreads, smem, s>>>(cand, cnt, tau, NS, m, m_pad, Cap, R);
   return cudaGetLastError();
 }
 

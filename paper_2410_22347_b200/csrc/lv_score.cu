@@ -24,12 +24,15 @@
 
 namespace lv {
 
-constexpr int kThreads = 320;          // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
-constexpr int kEpiThreads = 256;
-constexpr int kMaxKeysPerLane = 20;    // Cap <= 640
+constexpr int kEpiWarps = 16;          // 4 per SM sub-partition
+constexpr int kThreads = 64 + 32 * kEpiWarps;   // warps 0..15 epilogue, 16 TMA, 17 MMA
+// the producer warps get the highest ids: the warp scheduler favours high ids, so the
+// single-thread TMA/MMA issue loops are never starved by the 16 epilogue warps
+constexpr int kTmaWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kMaxKeysPerLane = 12;    // Cap <= 384
 
-constexpr int kStageStride = 36;                        // floats per staged row (conflict-free STS.128)
-constexpr uint32_t kEpiScratchBytes = (32 * kStageStride + 32 + 256) * 4;   // per warp: stage, ids, hist
+constexpr uint32_t kEpiScratchBytes = (32 + 256) * 4;   // per epilogue warp: ids[32], hist[256]
 
 struct ScoreSmemLayout {
   uint32_t b_off, epi_off, bar_off, total;
@@ -38,19 +41,19 @@ constexpr int kMaxAcc = 8;
 
 __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
-__host__ __device__ constexpr int score_tile_n(int d) { return (512 - 2 * d) / 128 >= 2 ? 64 : 32; }
+// TMEM: columns [0, d) hold the double-buffered A operand (one 128-query tile, d bf16 = d/2
+// columns per buffer); the rest holds NACC fp32 accumulator buffers of N = 128 columns.
+constexpr int kTileN = 128;
 __host__ __device__ constexpr int score_nacc(int d) {
-  const int n = score_tile_n(d);
-  const int k = (512 - 2 * d) / (2 * n);
-  return k > kMaxAcc ? kMaxAcc : k;
+  return (512 - d) / kTileN > kMaxAcc ? kMaxAcc : (512 - d) / kTileN;
 }
+__host__ __device__ constexpr int score_tile_n(int d) { return kTileN + 0 * d; }
 
 __host__ __device__ inline ScoreSmemLayout score_smem_layout(int d, int stages) {
   ScoreSmemLayout L;
-  const uint32_t n = (uint32_t)score_tile_n(d);
   L.b_off = 0;
-  L.epi_off = align_up((uint32_t)stages * n * (uint32_t)d * 2u, 1024);
-  L.bar_off = align_up(L.epi_off + 8u * kEpiScratchBytes, 16);
+  L.epi_off = align_up((uint32_t)stages * (uint32_t)kTileN * (uint32_t)d * 2u, 1024);
+  L.bar_off = align_up(L.epi_off + (uint32_t)kEpiWarps * kEpiScratchBytes, 16);
   // barriers: b_full[stages], b_empty[stages], acc_full[kMaxAcc], acc_empty[kMaxAcc], a_full[2], tmem ptr
   L.total = L.bar_off + 8u * (2 * stages + 2 * kMaxAcc + 2) + 16;
   return L;
@@ -132,7 +135,7 @@ __device__ __forceinline__ int warp_compact_fast(uint64_t* buf, int count, int R
 #pragma unroll
     for (int i = 0; i < kMaxKeysPerLane; ++i) {
       const uint64_t k = keys[i];
-      if (k != 0ull && (pass == 0 || (uint32_t)(k >> 56) == prefix)) atomicAdd(&hist[(k >> shift) & 255], 1);
+      warp_hist_add(hist, (k != 0ull && (pass == 0 || (uint32_t)(k >> 56) == prefix)) ? (int)((k >> shift) & 255) : -1);
     }
     __syncwarp();
     int loc[8], sum = 0;
@@ -200,13 +203,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int d = kD;
   constexpr int kCH = (kD % 64 == 0) ? 64 : 32;   // columns per swizzled TMA box (128 B or 64 B rows)
-  constexpr int kN = score_tile_n(kD);
+  constexpr int kN = kTileN;
   constexpr int nch = d / kCH;
   constexpr uint32_t box_bytes = (uint32_t)kN * kCH * 2u;
-  constexpr int kSub = 128 / kN;          // N-tiles per 128-row database tile
-  constexpr int kChunks = kN / 32;        // 32-column chunks per N-tile
-  const ScoreSmemLayout L = score_smem_layout(d, a.stages);
   constexpr int nacc = score_nacc(kD);
+  const ScoreSmemLayout L = score_smem_layout(d, a.stages);
   uint8_t* sB = smem + L.b_off;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* b_full = bars;
@@ -218,7 +219,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int nunits = a.P * a.QP;
+  const int QT = a.QP;                      // 128-query tiles
+  const int nunits = a.P * QT;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
@@ -227,29 +229,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < nacc; ++s) {
       tc::mbar_init(acc_full + s, 1);
-      tc::mbar_init(acc_empty + s, 8);
+      tc::mbar_init(acc_empty + s, kEpiWarps);
     }
-    tc::mbar_init(a_full + 0, 8);
-    tc::mbar_init(a_full + 1, 8);
+    tc::mbar_init(a_full + 0, kEpiWarps);
+    tc::mbar_init(a_full + 1, kEpiWarps);
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmap_xlow);
   }
-  if (warp == 1) tc::tmem_alloc(tmem_ptr, 512);
+  if (warp == kMmaWarp) tc::tmem_alloc(tmem_ptr, 512);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr;
-  const uint32_t acc_col0 = 2u * (uint32_t)d;     // A buffers occupy columns [0, 2d)
+  const uint32_t acc_col0 = (uint32_t)d;          // A buffers occupy columns [0, d)
 
-  if (warp == 0) {
+  if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer (X_low tiles)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const int c = u / a.QP;
+        const int c = u / QT;
         const int t0 = a.chunk_info[3 * c], t1 = a.chunk_info[3 * c + 1];
-        for (int t = t0 * kSub; t < t1 * kSub; ++t) {
+        for (int t = t0; t < t1; ++t) {
           tc::mbar_wait(b_empty + stage, phase ^ 1);
           tc::mbar_arrive_expect_tx(b_full + stage, nch * box_bytes);
           for (int k = 0; k < nch; ++k)
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer (A from TMEM)
     constexpr uint32_t idesc = tc::make_idesc_f16(128, kN, kBF16);
     const uint32_t sB_addr = tc::smem_u32(sB);
@@ -268,12 +270,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     int i = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
-      const int c = u / a.QP;
+      const int c = u / QT;
       const int t0 = a.chunk_info[3 * c], t1 = a.chunk_info[3 * c + 1];
       tc::mbar_wait(a_full + (i & 1), (uint32_t)(i >> 1) & 1u);
       tc::tc_fence_after();
-      const uint32_t abuf = tmem_base + (uint32_t)(i & 1) * (uint32_t)d;
-      for (int t = t0 * kSub; t < t1 * kSub; ++t) {
+      const uint32_t at = tmem_base + (uint32_t)(i & 1) * (uint32_t)(d / 2);
+      for (int t = t0; t < t1; ++t) {
         tc::mbar_wait(acc_empty + acc, acc_phase ^ 1);
         tc::mbar_wait(b_full + stage, phase);
         tc::tc_fence_after();
@@ -281,16 +283,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           // whole warp walks the issue loop (warp-uniform operands stay in uniform registers);
           // elect.sync picks the single issuing lane inside each instruction
           const uint64_t bd0 = tc::make_sdesc(sB_addr + (uint32_t)stage * nch * box_bytes, kCH * 2);
+          const uint32_t dt = tmem_base + acc_col0 + (uint32_t)acc * kN;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t dt = tmem_base + acc_col0 + (uint32_t)acc * (2u * kN) + (uint32_t)h * kN;
-            const uint32_t at = abuf + (uint32_t)h * (uint32_t)(d / 2);
-#pragma unroll
-            for (int kk = 0; kk < d / 16; ++kk) {
-              // K step kk: box kk*16/kCH, byte offset (kk*16 % kCH)*2 inside the swizzled row
-              const uint32_t off16 = (((uint32_t)((kk * 16) / kCH) * box_bytes) + (uint32_t)((kk * 16) % kCH) * 2u) >> 4;
-              tc::mma_f16_ts_elect(dt, at + (uint32_t)kk * 8u, bd0 + off16, idesc, kk > 0 ? 1u : 0u);
-            }
+          for (int kk = 0; kk < d / 16; ++kk) {
+            // K step kk: box kk*16/kCH, byte offset (kk*16 % kCH)*2 inside the swizzled row
+            const uint32_t off16 = (((uint32_t)((kk * 16) / kCH) * box_bytes) + (uint32_t)((kk * 16) % kCH) * 2u) >> 4;
+            tc::mma_f16_ts_elect(dt, at + (uint32_t)kk * 8u, bd0 + off16, idesc, kk > 0 ? 1u : 0u);
           }
           tc::mma_commit_elect(b_empty + stage);
           tc::mma_commit_elect(acc_full + acc);
@@ -301,36 +299,52 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue: 8 warps, thread = query
-    const int e = warp - 2;
-    const int h = e >> 2;            // which M=128 query tile of the pair
+    // ------------------------------------------------------------ epilogue: 16 warps
+    // warp -> (TMEM lane quarter, 32-column quarter of every tile); thread = one query x one
+    // column quarter, with its own candidate sub-slot (4 per slot and query).
+    const int e = warp;
+    const int cq = e >> 2;           // column quarter of each 128-column tile
     const int quarter = warp & 3;    // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
-    float* stg = reinterpret_cast<float*>(smem + L.epi_off + e * kEpiScratchBytes);
-    int* sid = reinterpret_cast<int*>(stg + 32 * kStageStride);
+    int* sid = reinterpret_cast<int*>(smem + L.epi_off + e * kEpiScratchBytes);
     int* hist = sid + 32;
-    float4* srow = reinterpret_cast<float4*>(stg + lane * kStageStride);
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const int ldq = a.C * d;         // Q' row length (elements)
-    // A operand of unit u (its cluster's view of the pair's 256 queries) -> TMEM buffer b
+    // A operand of unit u (its cluster's view of the tile's 128 queries) -> TMEM buffer b; this
+    // warp writes K range [cq*d/4, (cq+1)*d/4) of its 32 rows (d/8 TMEM columns)
     auto write_A = [&](int u, int b) {
-      const int c = u / a.QP, p = u % a.QP;
+      const int c = u / QT, qt = u % QT;
       const int cl = a.chunk_info[3 * c + 2];
-      const int qq = (2 * p + h) * 128 + row;
+      const int qq = qt * 128 + row;
       const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.Qp) +
-                                                       (size_t)qq * ldq + (size_t)cl * d);
-      const uint32_t dst = tmem_base + lane_base + (uint32_t)b * (uint32_t)d + (uint32_t)h * (uint32_t)(d / 2);
-      for (int c32 = 0; c32 < d / 32; ++c32) {
+                                                       (size_t)qq * ldq + (size_t)cl * d + cq * (d / 4));
+      const uint32_t dst = tmem_base + lane_base + (uint32_t)b * (uint32_t)(d / 2) + (uint32_t)cq * (uint32_t)(d / 8);
+      constexpr int ncols = d / 8;   // 4..24, a multiple of 4
+      int col = 0;
+#pragma unroll
+      for (; col + 16 <= ncols; col += 16) {
         uint32_t r[16];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint4 w = __ldg(src + c32 * 4 + j);
-          r[4 * j] = w.x;
-          r[4 * j + 1] = w.y;
-          r[4 * j + 2] = w.z;
-          r[4 * j + 3] = w.w;
+          const uint4 w = __ldg(src + col / 4 + j);
+          r[4 * j] = w.x; r[4 * j + 1] = w.y; r[4 * j + 2] = w.z; r[4 * j + 3] = w.w;
         }
-        tc::tmem_st_32x32b_x16(dst + (uint32_t)c32 * 16u, r);
+        tc::tmem_st_32x32b_x16(dst + (uint32_t)col, r);
+      }
+      if (col + 8 <= ncols) {
+        uint32_t r[8];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const uint4 w = __ldg(src + col / 4 + j);
+          r[4 * j] = w.x; r[4 * j + 1] = w.y; r[4 * j + 2] = w.z; r[4 * j + 3] = w.w;
+        }
+        tc::tmem_st_32x32b_x8(dst + (uint32_t)col, r);
+        col += 8;
+      }
+      if (col + 4 <= ncols) {
+        const uint4 w = __ldg(src + col / 4);
+        const uint32_t r[4] = {w.x, w.y, w.z, w.w};
+        tc::tmem_st_32x32b_x4(dst + (uint32_t)col, r);
       }
       tc::tmem_wait_st();
       tc::tc_fence_before();
@@ -343,15 +357,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     int i = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
       if (u + (int)gridDim.x < nunits) write_A(u + gridDim.x, (i + 1) & 1);
-      const int c = u / a.QP, p = u % a.QP;
+      const int c = u / QT, qt = u % QT;
       const int t0 = a.chunk_info[3 * c], t1 = a.chunk_info[3 * c + 1];
-      const int q0 = (2 * p + h) * 128 + quarter * 32;   // query of lane 0
+      const int q0 = qt * 128 + quarter * 32;   // query of lane 0
       const int q = q0 + lane;
       const bool qvalid = q < a.m;
-      const int slot = c % a.NS;
+      const int slot = (c % a.NS) * 4 + cq;
       if (c >= a.NS) {
         if (lane == 0) {
-          const int32_t* flag = a.done + (size_t)(c - a.NS) * a.QP + p;
+          const int32_t* flag = a.done + (size_t)(c - a.NS) * QT + qt;
           long long spins = 0;
           while (ld_acquire(flag) == 0) {
             __nanosleep(64);
@@ -360,112 +374,96 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       }
-      const size_t sbase = (size_t)slot * a.m_pad + q0;     // slot index of lane 0
+      const size_t sbase = (size_t)slot * a.m_pad + q0;     // sub-slot index of lane 0
       int cnt = a.cnt[sbase + lane];
       uint64_t tk = a.tau[sbase + lane];
       float ts = thr_score(tk);
+      const int tv_last = a.tile_valid[t1 - 1];
 
-      for (int t = t0 * kSub; t < t1 * kSub; ++t) {
+      for (int t = t0; t < t1; ++t) {
         tc::mbar_wait(acc_full + acc, acc_phase);
         tc::tc_fence_after();
-        const uint32_t taddr = tmem_base + lane_base + acc_col0 + (uint32_t)acc * (2u * kN) + (uint32_t)h * kN;
-        float v[kChunks][32];
-#pragma unroll
-        for (int ch = 0; ch < kChunks; ++ch) tc::tmem_ld_32x32b_x32(taddr + 32 * ch, v[ch]);
+        float v[32];
+        tc::tmem_ld_32x32b_x32(tmem_base + lane_base + acc_col0 + (uint32_t)acc * kN + (uint32_t)cq * 32u, v);
         tc::tmem_wait_ld();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(acc_empty + acc);
         if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
         if (a.flags & 1) continue;
-        const int tv = a.tile_valid[t / kSub] - (t % kSub) * kN;   // valid columns of this N-tile
-        const int64_t base_pos = (int64_t)t * kN;
-        if (tv < kN) {
+        const int64_t base_pos = (int64_t)t * kN + cq * 32;
+        const int tv = (t + 1 == t1 ? tv_last : kN) - cq * 32;   // valid columns of this chunk
+        if (tv < 32) {
 #pragma unroll
-          for (int ch = 0; ch < kChunks; ++ch)
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (32 * ch + j >= tv) v[ch][j] = -FLT_MAX;
+          for (int j = 0; j < 32; ++j)
+            if (j >= tv) v[j] = -FLT_MAX;
         }
         if (a.raw != nullptr) {
 #pragma unroll
-          for (int ch = 0; ch < kChunks; ++ch)
-#pragma unroll
-            for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + base_pos + 32 * ch + j] = v[ch][j];
+          for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + base_pos + j] = v[j];
         }
-        // fast path: per 32-column chunk one max, compared with the lane's threshold
-        float m8[kChunks][8];
-        uint32_t hitc = 0;
+        // fast path: one max over the 32 scores, compared with the lane's threshold
+        float m8[8];
 #pragma unroll
-        for (int ch = 0; ch < kChunks; ++ch) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            m8[ch][j] = fmaxf(fmaxf(v[ch][4 * j], v[ch][4 * j + 1]), fmaxf(v[ch][4 * j + 2], v[ch][4 * j + 3]));
-          const float mx = fmaxf(fmaxf(fmaxf(m8[ch][0], m8[ch][1]), fmaxf(m8[ch][2], m8[ch][3])),
-                                 fmaxf(fmaxf(m8[ch][4], m8[ch][5]), fmaxf(m8[ch][6], m8[ch][7])));
-          hitc |= (qvalid && mx >= ts && mx > -FLT_MAX) ? (1u << ch) : 0u;
+        for (int j = 0; j < 8; ++j) m8[j] = fmaxf(fmaxf(v[4 * j], v[4 * j + 1]), fmaxf(v[4 * j + 2], v[4 * j + 3]));
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        const bool hit = qvalid && mx >= ts && mx > -FLT_MAX;
+        const uint32_t hits = __ballot_sync(0xffffffffu, hit);
+        if (hits == 0u) continue;
+        // slow path: a lane whose sub-slot could overflow is compacted first by the warp, then
+        // every hit lane appends its own survivors (groups of 4 whose max passes)
+        uint32_t need = __ballot_sync(0xffffffffu, hit && cnt > a.Cap - 32);
+        while (need) {
+          const int Lz = __ffs(need) - 1;
+          need &= need - 1u;
+          const int cL = __shfl_sync(0xffffffffu, cnt, Lz);
+          uint64_t nthr;
+          const int ncnt = warp_compact_fast(a.cand + (sbase + Lz) * (size_t)a.Cap, cL, a.R, a.Cap, lane, hist, &nthr);
+          if (lane == Lz) {
+            cnt = ncnt;
+            tk = nthr;
+            ts = thr_score(nthr);
+          }
         }
-        if (__ballot_sync(0xffffffffu, hitc != 0u) == 0u) continue;
-        // slow path, one 32-column chunk at a time (single code copy): stage the chunk's scores
-        // in smem, then every hit lane extracts its own survivors in parallel.
-#pragma unroll 1
-        for (int ch = 0; ch < kChunks; ++ch) {
-          const uint32_t hits = __ballot_sync(0xffffffffu, (hitc >> ch) & 1u);
-          if (hits == 0u) continue;
-          const int col0 = 32 * ch;
-          float g8[8];
-          if (ch == 0) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              srow[j] = make_float4(v[0][4 * j], v[0][4 * j + 1], v[0][4 * j + 2], v[0][4 * j + 3]);
-              g8[j] = m8[0][j];
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              srow[j] = make_float4(v[kChunks - 1][4 * j], v[kChunks - 1][4 * j + 1], v[kChunks - 1][4 * j + 2],
-                                    v[kChunks - 1][4 * j + 3]);
-              g8[j] = m8[kChunks - 1][j];
-            }
-          }
-          uint32_t need = __ballot_sync(0xffffffffu, ((hits >> lane) & 1u) && cnt > a.Cap - 32);
-          while (need) {
-            const int Lz = __ffs(need) - 1;
-            need &= need - 1u;
-            const int cL = __shfl_sync(0xffffffffu, cnt, Lz);
-            uint64_t nthr;
-            const int ncnt =
-                warp_compact_fast(a.cand + (sbase + Lz) * (size_t)a.Cap, cL, a.R, a.Cap, lane, hist, &nthr);
-            if (lane == Lz) {
-              cnt = ncnt;
-              tk = nthr;
-              ts = thr_score(nthr);
-            }
-          }
-          if (a.perm) sid[lane] = a.perm[base_pos + col0 + lane];
+        if (a.perm) {
+          sid[lane] = a.perm[base_pos + lane];
           __syncwarp();
-          if ((hits >> lane) & 1u) {
-            uint64_t* bp = a.cand + (sbase + lane) * (size_t)a.Cap;
+        }
+        if (hit) {
+          // groups of 4 whose max passes, one at a time; the group's 4 scores are picked by a
+          // switch (no dynamic register indexing), survivors appended by the lane itself
+          uint64_t* bp = a.cand + (sbase + lane) * (size_t)a.Cap;
+          uint32_t gm = 0;
 #pragma unroll
-            for (int gi = 0; gi < 8; ++gi) {
-              if (g8[gi] >= ts) {
-                const float4 f = srow[gi];
-                const float fv[4] = {f.x, f.y, f.z, f.w};
+          for (int gi = 0; gi < 8; ++gi) gm |= (m8[gi] >= ts) ? (1u << gi) : 0u;
+          while (gm) {
+            const int gi = __ffs(gm) - 1;
+            gm &= gm - 1u;
+            float f[4];
+            switch (gi) {
+#define LV_PICK(G)                \
+  case G:                         \
+    f[0] = v[4 * G];              \
+    f[1] = v[4 * G + 1];          \
+    f[2] = v[4 * G + 2];          \
+    f[3] = v[4 * G + 3];          \
+    break;
+              LV_PICK(0) LV_PICK(1) LV_PICK(2) LV_PICK(3) LV_PICK(4) LV_PICK(5) LV_PICK(6)
+              default: LV_PICK(7)
+#undef LV_PICK
+            }
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
-                  const int j = 4 * gi + jj;
-                  const int32_t id = a.perm ? sid[j] : (int32_t)(base_pos + col0 + j);
-                  const uint64_t key = make_key(fv[jj], id);
-                  if (key > tk && fv[jj] > -FLT_MAX) {
-                    bp[cnt] = key;
-                    ++cnt;
-                  }
-                }
+            for (int jj = 0; jj < 4; ++jj) {
+              if (f[jj] >= ts && f[jj] > -FLT_MAX) {
+                const int j = 4 * gi + jj;
+                const int32_t id = a.perm ? sid[j] : (int32_t)(base_pos + j);
+                const uint64_t key = make_key(f[jj], id);
+                if (key > tk) bp[cnt++] = key;
               }
             }
           }
-          __syncwarp();
         }
+        __syncwarp();
       }
       if (qvalid) {
         a.cnt[sbase + lane] = cnt;
@@ -473,12 +471,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __threadfence();
       tc::named_bar_sync(1, kEpiThreads);
-      if (threadIdx.x == 64) st_release(a.done + (size_t)c * a.QP + p, 1);
+      if (threadIdx.x == 0) st_release(a.done + (size_t)c * QT + qt, 1);
     }
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tmem_base, 512);
+  if (warp == kMmaWarp) tc::tmem_dealloc(tmem_base, 512);
 }
 
 size_t score_smem_bytes(int d, int stages) { return score_smem_layout(d, stages).total + 1024; }

