@@ -65,6 +65,8 @@ typedef struct {
     int32_t  slots;        /* per-query candidate lists kept by the scan       */
     int32_t  units;        /* (query pair, database chunk) work units of the scan            */
     int32_t  grid;         /* CTAs of the scan                                               */
+    int32_t  path;         /* 0: staged thresholds, 1: sampled threshold + repair */
+    int32_t  failed[2];    /* sampled path, with timing: queries repaired in rounds 1 and 2     */
 } lv_search_debug;
 
 /* Human-readable message for the last non-OK status on this thread. */

@@ -17,6 +17,37 @@ namespace lv {
 size_t score_smem_bytes(int d, int stages);
 }
 
+// Work decomposition of one lv_search shape (m, R) and its carve of the index workspace.
+// Chunk records are lv::kChunkInts ints: tile_begin, tile_end, cluster, tile_stride, sample_base.
+struct Plan {
+  int m_pad, QP, NS, Cap, grid, stages;
+  size_t smem;
+  bool sampled = false;       // sampled-threshold path (else: staged path)
+  int stride = 1, nblk = 0, j1 = 0, j2 = 0;
+  std::vector<std::vector<int32_t>> chunks;   // staged: one list per stage; sampled: {sample, main}
+  std::vector<int32_t> repair_chunks;         // sampled: full database, planned for one query tile
+  int total_units = 0;
+};
+struct PlanCache {
+  bool valid = false;
+  int64_t m = -1;
+  int R = -1, nsm = -1;
+  Plan pl;
+  void* Qp = nullptr;
+  void* Qr = nullptr;          // repair: gathered Q' rows
+  uint64_t* cand = nullptr;
+  int32_t* cnt = nullptr;
+  uint64_t* tau = nullptr;
+  uint64_t* tau2 = nullptr;    // sampled: per-query repair threshold
+  float* bmax = nullptr;       // sampled: block maxima of the sample stage
+  int32_t* fail = nullptr;     // [4]: fail counts of the two checks, repair row counts
+  int32_t* fail_list = nullptr;   // [2][m_pad]
+  int32_t* slot_busy = nullptr;
+  uint8_t *zero_lo = nullptr, *zero_hi = nullptr;
+  std::vector<int32_t*> chunk_info;
+  int32_t* repair_info = nullptr;
+};
+
 struct lv_index {
   int32_t D = 0, d = 0, C = 0;
   lv_dtype low = LV_BF16, full = LV_F32;
@@ -32,6 +63,7 @@ struct lv_index {
   // search workspace
   void* ws = nullptr;
   size_t ws_bytes = 0;
+  PlanCache plan;               // last search shape: plan + device chunk tables (uploaded once)
   // host-buffer staging for lv_search_host
   void* hs = nullptr;
   size_t hs_bytes = 0;
@@ -57,15 +89,25 @@ lv_status fail(lv_status s, const char* fmt, ...) {
     if (e_ != cudaSuccess) return fail(LV_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
   } while (0)
 
+// Device check (cached per device: cudaGetDeviceProperties costs milliseconds per call).
 lv_status check_device(int* nsm = nullptr) {
+  static int cached_sm[64] = {0};   // 0 = unknown, -1 = unsupported, else SM count
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return fail(LV_EUNSUPPORTED, "no CUDA device");
-  cudaDeviceProp p;
-  if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return fail(LV_EUNSUPPORTED, "no CUDA device");
-  if (p.major != 10 || p.minor != 0)
-    return fail(LV_EUNSUPPORTED, "device sm_%d%d is not sm_100 (this library is built for sm_100a only)", p.major,
-                p.minor);
-  if (nsm) *nsm = p.multiProcessorCount;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return fail(LV_EUNSUPPORTED, "no CUDA device");
+  int& c = cached_sm[dev & 63];
+  if (c == 0) {
+    int major = 0, minor = 0, count = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return fail(LV_EUNSUPPORTED, "no CUDA device");
+    if (major != 10 || minor != 0) {
+      return fail(LV_EUNSUPPORTED, "device sm_%d%d is not sm_100 (this library is built for sm_100a only)", major,
+                  minor);
+    }
+    c = count;
+  }
+  if (nsm) *nsm = c;
   return LV_OK;
 }
 
@@ -97,6 +139,11 @@ lv_status make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t co
   return LV_OK;
 }
 
+double env_double(const char* name, double dflt) {
+  const char* v = getenv(name);
+  return v ? atof(v) : dflt;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 template <typename T>
@@ -106,18 +153,17 @@ T* carve(uint8_t*& p, size_t count) {
   return r;
 }
 
-struct Plan {
-  int m_pad, QP, NS, Cap, grid, stages;
-  size_t smem;
-  std::vector<std::vector<int32_t>> chunks;   // per scan stage: P x {tile_begin, tile_end, cluster}
-  int total_units = 0;
-};
-
 // Chunks of the given segments (tile ranges) so that units = P * QP spread evenly over the grid.
+// With stride > 1 only every stride-th tile of a segment is scanned (sample stage); the scanned
+// tiles are numbered consecutively from *sample_base (block-maximum rows, lv_score.cu).
 void make_chunks(const std::vector<std::pair<int, int>>& segs, const std::vector<int>& segc, int QP, int G,
-                 int maxChunks, std::vector<int32_t>* out) {
+                 int maxChunks, std::vector<int32_t>* out, int stride = 1, int* sample_base = nullptr) {
+  std::vector<int> cnts(segs.size());
   int ntiles = 0;
-  for (auto& s : segs) ntiles += s.second - s.first;
+  for (size_t i = 0; i < segs.size(); ++i) {
+    cnts[i] = std::max(0, (segs[i].second - segs[i].first + stride - 1) / stride);
+    ntiles += cnts[i];
+  }
   out->clear();
   if (ntiles == 0) return;
   double best_eff = -1;
@@ -126,7 +172,7 @@ void make_chunks(const std::vector<std::pair<int, int>>& segs, const std::vector
   for (int target = 1; target <= maxP; ++target) {
     const int len = (ntiles + target - 1) / target;
     int P = 0;
-    for (auto& s : segs) P += (s.second - s.first + len - 1) / len;
+    for (int c : cnts) P += (c + len - 1) / len;
     if (P > maxChunks) continue;
     const int64_t units = (int64_t)P * QP;
     const int g = (int)std::min<int64_t>(G, units);
@@ -140,16 +186,22 @@ void make_chunks(const std::vector<std::pair<int, int>>& segs, const std::vector
     }
     if ((int64_t)target * QP > 64ll * G) break;
   }
+  int sb = sample_base ? *sample_base : 0;
   for (size_t i = 0; i < segs.size(); ++i) {
-    const int tb = segs[i].first, te = segs[i].second;
-    if (te <= tb) continue;
-    const int cnt = (te - tb + best_len - 1) / best_len;
-    for (int j = 0; j < cnt; ++j) {
-      out->push_back(tb + (int)((int64_t)(te - tb) * j / cnt));
-      out->push_back(tb + (int)((int64_t)(te - tb) * (j + 1) / cnt));
+    const int tb = segs[i].first, te = segs[i].second, ct = cnts[i];
+    if (ct <= 0) continue;
+    const int nc = (ct + best_len - 1) / best_len;
+    for (int j = 0; j < nc; ++j) {
+      const int s0 = (int)((int64_t)ct * j / nc), s1 = (int)((int64_t)ct * (j + 1) / nc);
+      out->push_back(tb + s0 * stride);
+      out->push_back(std::min(te, tb + s1 * stride));
       out->push_back(segc[i]);
+      out->push_back(stride);
+      out->push_back(sb + s0);
     }
+    sb += ct;
   }
+  if (sample_base) *sample_base = sb;
 }
 
 // Work decomposition of the scan.  The database is scanned in stages of
@@ -164,13 +216,13 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   if (pl->Cap < R + 96) return fail(LV_EUNSUPPORTED, "R=%d too large (R <= 256)", R);
   const int ntiles = (int)(ix->n_pad / 128);
   const int G = nsm;
-  const int slots_dep = (G + pl->QP - 1) / pl->QP + 2;
-  // every slot is split in four sub-slots (one per epilogue column quarter): 4*NS lists per query
-  const int ns_smem = (int)((200 * 1024 - (size_t)ix->D * 4) / ((size_t)pl->Cap * 8)) / 4;
-  const int ns_limit = std::min(16, ns_smem);
-  if (ns_limit < 1) return fail(LV_EUNSUPPORTED, "R=%d too large for the merge", R);
-  const int max_chunks = slots_dep > ns_limit ? ns_limit : (1 << 30);
-  const int ns_target = std::min(slots_dep, ns_limit);
+  // every slot is split in two sub-lists (one per epilogue column half): 2*NS lists per query;
+  // a query tile's concurrently running units claim distinct slots (lv_score.cu)
+  const int ns_smem = (int)((200 * 1024 - (size_t)ix->D * 4) / ((size_t)pl->Cap * 8)) / 2;
+  const int ns = std::min((int)env_double("LV_SLOTS", 8.0), ns_smem);
+  if (ns < 1) return fail(LV_EUNSUPPORTED, "R=%d too large for the merge", R);
+  const int max_chunks = 1 << 30;
+  const int ns_target = ns;
   // segment tile ranges
   std::vector<std::pair<int, int>> seg;
   std::vector<int> segc;
@@ -186,12 +238,12 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   std::vector<double> cum;   // cumulative fraction after each stage
   if (ntiles >= 64) {
     const double rows = (double)ntot * 128.0;
-    const double lists = 4.0 * ns_target;   // independent candidate lists per query
+    const double lists = 2.0 * ns_target;   // independent candidate lists per query
     // stage 0 only has to produce R keys per query: keep it (and so the first merge) small
-    double c0 = std::max(2.0 * R, lists * 32.0);
+    double c0 = std::max(2.0 * R, lists * 32.0) * env_double("LV_STAGE_C0", 1.0);
     // growth per stage: bounded by the slot capacity and kept small so that most of the
     // database is scanned with a threshold close to the final R-th score
-    double g = std::min(6.0, std::max(2.0, 0.8 * (pl->Cap - 64) * lists / (double)R));
+    double g = std::min(env_double("LV_STAGE_GMAX", 6.0), std::max(2.0, 0.8 * (pl->Cap - 64) * lists / (double)R));
     double acc = c0;
     while (acc < rows * 0.999) {
       cum.push_back(acc / rows);
@@ -221,13 +273,37 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
     make_chunks(part, partc, pl->QP, G, max_chunks, &ch);
     if (!ch.empty()) pl->chunks.push_back(ch);
   }
+  // sampled-threshold path: a sample stage over every stride-th tile records
+  // block maxima, a per-query threshold with >= j1 rows above it is selected, one main stage
+  // scans everything with it; queries left with < R candidates are repaired exactly.
+  const int stride = (int)env_double("LV_SAMPLE_STRIDE", 16.0);
+  const double gamma = env_double("LV_SAMPLE_GAMMA", 3.0);
+  int nsamp = 0;
+  for (auto& sg : seg) nsamp += (sg.second - sg.first + stride - 1) / stride;
+  const int j1 = (int)std::ceil(gamma * R / stride);
+  pl->sampled = env_double("LV_SAMPLED", 1.0) != 0.0 && stride >= 2 && nsamp >= 64 && 4 * nsamp >= 16 * j1 &&
+                4 * nsamp <= 65535;
+  if (pl->sampled) {
+    pl->stride = stride;
+    pl->nblk = 4 * nsamp;
+    pl->j1 = std::max(4, j1);
+    pl->j2 = std::min(pl->nblk, 4 * pl->j1);
+    pl->chunks.clear();
+    std::vector<int32_t> ch;
+    int sbase = 0;
+    make_chunks(seg, segc, pl->QP, G, max_chunks, &ch, stride, &sbase);
+    pl->chunks.push_back(ch);
+    make_chunks(seg, segc, pl->QP, G, max_chunks, &ch);
+    pl->chunks.push_back(ch);
+    make_chunks(seg, segc, 1, G, max_chunks, &pl->repair_chunks);
+  }
   int pmax = 0;
   pl->total_units = 0;
   for (auto& ch : pl->chunks) {
-    pmax = std::max(pmax, (int)(ch.size() / 3));
-    pl->total_units += (int)(ch.size() / 3) * pl->QP;
+    pmax = std::max(pmax, (int)(ch.size() / lv::kChunkInts));
+    pl->total_units += (int)(ch.size() / lv::kChunkInts) * pl->QP;
   }
-  pl->NS = std::min(std::min(pmax, slots_dep), ns_limit);
+  pl->NS = ns;
   pl->grid = (int)std::min<int64_t>(G, (int64_t)pmax * pl->QP);
   const size_t budget = 227 * 1024 - 1024 - 256;
   int st = 8;
@@ -391,6 +467,7 @@ static void free_db(lv_index* ix) {
   ix->X_low = ix->X_full = nullptr;
   ix->perm = ix->tile_valid = nullptr;
   ix->n = ix->n_pad = 0;
+  ix->plan.valid = false;
 }
 
 lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int64_t n, const int32_t* assign,
@@ -492,38 +569,65 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   if (k < 1 || k > R || R > 256 || R > ix->n) return fail(LV_EINVAL, "lv_search: need 1 <= k <= R <= min(n, 256)");
   if (m > (1 << 24)) return fail(LV_EINVAL, "lv_search: m too large");
   cudaStream_t s = (cudaStream_t)stream;
-  Plan pl;
-  st = plan_search(ix, m, R, nsm, &pl);
-  if (st) return st;
   const int Cd = ix->C * ix->d;
-  // workspace
-  size_t nchunk_ints = 0, ndone = 0;
-  for (auto& ch : pl.chunks) {
-    nchunk_ints += ch.size() + 1;
-    ndone += ch.size() / 3 * pl.QP + 1;
+  PlanCache& pc = ix->plan;
+  if (!(pc.valid && pc.m == m && pc.R == R && pc.nsm == nsm)) {
+    // new search shape: plan the scan, (re)size the workspace, upload the chunk tables once
+    pc.valid = false;
+    Plan pl;
+    st = plan_search(ix, m, R, nsm, &pl);
+    if (st) return st;
+    size_t nchunk_ints = pl.repair_chunks.size() + 1;
+    for (auto& ch : pl.chunks) nchunk_ints += ch.size() + 1;
+    const int NS2 = 4 * pl.NS;   // sub-lists per query
+    const size_t mp = pl.m_pad;
+    size_t need = (mp * Cd * 2 + 256) + ((size_t)NS2 * mp * pl.Cap * 8 + 256) + ((size_t)NS2 * mp * 4 + 256) +
+                  ((size_t)NS2 * mp * 8 + 256) + ((size_t)pl.QP * 4 + 256) + (16 * 4 + 256) +
+                  (nchunk_ints * 4 + 256 * (pl.chunks.size() + 2));
+    if (pl.sampled)
+      need += (mp * Cd * 2 + 256) + (mp * 8 + 256) + ((size_t)pl.nblk * mp * 4 + 256) + (2 * mp * 4 + 256);
+    if (need > ix->ws_bytes) {
+      LV_CUDA(cudaStreamSynchronize(s));   // the old workspace may still be in use on s
+      cudaFree(ix->ws);
+      ix->ws = nullptr;
+      ix->ws_bytes = 0;
+      if (cudaMalloc(&ix->ws, need) != cudaSuccess) return fail(LV_ENOMEM, "lv_search: workspace %zu bytes", need);
+      ix->ws_bytes = need;
+    }
+    uint8_t* p = reinterpret_cast<uint8_t*>(ix->ws);
+    pc.Qp = carve<uint16_t>(p, mp * Cd);
+    pc.cand = carve<uint64_t>(p, (size_t)NS2 * mp * pl.Cap);
+    pc.zero_lo = p;
+    pc.cnt = carve<int32_t>(p, (size_t)NS2 * mp);
+    pc.tau = carve<uint64_t>(p, (size_t)NS2 * mp);
+    pc.slot_busy = carve<int32_t>(p, (size_t)pl.QP);
+    pc.fail = carve<int32_t>(p, 16);
+    pc.zero_hi = p;
+    if (pl.sampled) {
+      pc.Qr = carve<uint16_t>(p, mp * Cd);
+      pc.tau2 = carve<uint64_t>(p, mp);
+      pc.bmax = carve<float>(p, (size_t)pl.nblk * mp);
+      pc.fail_list = carve<int32_t>(p, 2 * mp);
+    }
+    pc.chunk_info.assign(pl.chunks.size(), nullptr);
+    for (size_t k = 0; k < pl.chunks.size(); ++k) pc.chunk_info[k] = carve<int32_t>(p, pl.chunks[k].size() + 1);
+    pc.repair_info = carve<int32_t>(p, pl.repair_chunks.size() + 1);
+    for (size_t k = 0; k < pl.chunks.size(); ++k)
+      LV_CUDA(cudaMemcpyAsync(pc.chunk_info[k], pl.chunks[k].data(), pl.chunks[k].size() * 4, cudaMemcpyHostToDevice, s));
+    if (!pl.repair_chunks.empty())
+      LV_CUDA(cudaMemcpyAsync(pc.repair_info, pl.repair_chunks.data(), pl.repair_chunks.size() * 4,
+                              cudaMemcpyHostToDevice, s));
+    LV_CUDA(cudaStreamSynchronize(s));   // host vectors are the copy sources
+    pc.pl = std::move(pl);
+    pc.m = m;
+    pc.R = R;
+    pc.nsm = nsm;
+    pc.valid = true;
   }
-  const int NS2 = 4 * pl.NS;   // sub-slots per query
-  const size_t need = ((size_t)pl.m_pad * Cd * 2 + 256) + ((size_t)NS2 * pl.m_pad * pl.Cap * 8 + 256) +
-                      ((size_t)NS2 * pl.m_pad * 4 + 256) + ((size_t)NS2 * pl.m_pad * 8 + 256) +
-                      (ndone * 4 + 256 * (pl.chunks.size() + 1)) + (nchunk_ints * 4 + 256 * (pl.chunks.size() + 1));
-  if (need > ix->ws_bytes) {
-    cudaFree(ix->ws);
-    ix->ws = nullptr;
-    ix->ws_bytes = 0;
-    if (cudaMalloc(&ix->ws, need) != cudaSuccess) return fail(LV_ENOMEM, "lv_search: workspace %zu bytes", need);
-    ix->ws_bytes = need;
-  }
-  uint8_t* p = reinterpret_cast<uint8_t*>(ix->ws);
-  void* Qp = carve<uint16_t>(p, (size_t)pl.m_pad * Cd);
-  uint64_t* cand = carve<uint64_t>(p, (size_t)NS2 * pl.m_pad * pl.Cap);
-  uint8_t* zero_lo = p;
-  int32_t* cnt = carve<int32_t>(p, (size_t)NS2 * pl.m_pad);
-  uint64_t* tau = carve<uint64_t>(p, (size_t)NS2 * pl.m_pad);
-  std::vector<int32_t*> done(pl.chunks.size());
-  for (size_t k = 0; k < pl.chunks.size(); ++k) done[k] = carve<int32_t>(p, pl.chunks[k].size() / 3 * pl.QP + 1);
-  uint8_t* zero_hi = p;
-  std::vector<int32_t*> chunk_info(pl.chunks.size());
-  for (size_t k = 0; k < pl.chunks.size(); ++k) chunk_info[k] = carve<int32_t>(p, pl.chunks[k].size() + 1);
+  const Plan& pl = pc.pl;
+  const int NS2 = 4 * pl.NS;
+  void* Qp = pc.Qp;
+  const std::vector<int32_t*>& chunk_info = pc.chunk_info;
 
   cudaEvent_t ev[4];
   const bool timing = dbg && dbg->timing;
@@ -532,14 +636,11 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     LV_CUDA(cudaEventRecord(ev[0], s));
   }
   int launches = 0;
-  for (size_t k = 0; k < pl.chunks.size(); ++k)
-    LV_CUDA(cudaMemcpyAsync(chunk_info[k], pl.chunks[k].data(), pl.chunks[k].size() * 4, cudaMemcpyHostToDevice, s));
-  LV_CUDA(cudaMemsetAsync(zero_lo, 0, zero_hi - zero_lo, s));
+  LV_CUDA(cudaMemsetAsync(pc.zero_lo, 0, pc.zero_hi - pc.zero_lo, s));
   // K1 projection (rows >= m are zero)
   LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, pl.m_pad, ix->A, ix->D, nullptr, Cd, Qp, ix->low, Cd, pl.m_pad, s));
   ++launches;
   if (timing) LV_CUDA(cudaEventRecord(ev[1], s));
-  // K2/K3 fused scan: phase A, exact threshold merge, phase B
   lv::ScoreArgs sa;
   sa.Qp = Qp;
   sa.C = ix->C;
@@ -553,29 +654,46 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   sa.stages = pl.stages;
   sa.tile_valid = ix->tile_valid;
   sa.perm = ix->C > 1 ? ix->perm : nullptr;
-  sa.cand = cand;
-  sa.cnt = cnt;
-  sa.tau = tau;
+  sa.cand = pc.cand;
+  sa.cnt = pc.cnt;
+  sa.tau = pc.tau;
   sa.raw = dbg ? dbg->raw_scores : nullptr;
+  sa.bmax = nullptr;
+  sa.m_dev = nullptr;
   sa.n_pad = ix->n_pad;
+  sa.slot_busy = pc.slot_busy;
   {
     const char* f = getenv("LV_DEBUG_SCAN_FLAGS");
     sa.flags = f ? atoi(f) : 0;
   }
-  for (size_t k = 0; k < pl.chunks.size(); ++k) {
-    sa.P = (int)(pl.chunks[k].size() / 3);
-    sa.chunk_info = chunk_info[k];
-    sa.done = done[k];
-    const int grid = (int)std::min<int64_t>(pl.grid, (int64_t)sa.P * pl.QP);
+  static unsigned long long* dstats = nullptr;
+  sa.stats = nullptr;
+  if (sa.flags & 2) {
+    if (!dstats) LV_CUDA(cudaMalloc(&dstats, 8 * sizeof(unsigned long long)));
+    sa.stats = dstats;
+  }
+  auto scan = [&](const int32_t* info, const std::vector<int32_t>& host_chunks, int qtiles, const char* what) -> lv_status {
+    sa.P = (int)(host_chunks.size() / lv::kChunkInts);
+    sa.chunk_info = info;
+    const int grid = (int)std::min<int64_t>(nsm, (int64_t)sa.P * qtiles);
+    if (grid <= 0) return LV_OK;
+    if (sa.stats) LV_CUDA(cudaMemsetAsync(sa.stats, 0, 8 * sizeof(unsigned long long), s));
     LV_CUDA(lv::launch_score(&ix->tmap_xlow, sa, ix->low == LV_BF16, grid, pl.smem, s));
     ++launches;
-    if (k + 1 < pl.chunks.size()) {
-      LV_CUDA(lv::launch_tau_merge(cand, cnt, tau, NS2, (int)m, pl.m_pad, pl.Cap, R, s));
-      ++launches;
+    if (sa.stats) {
+      unsigned long long h[8];
+      LV_CUDA(cudaMemcpyAsync(h, sa.stats, sizeof h, cudaMemcpyDeviceToHost, s));
+      LV_CUDA(cudaStreamSynchronize(s));
+      int64_t tiles = 0;
+      for (int c = 0; c < sa.P; ++c) {
+        const int32_t* ci = host_chunks.data() + lv::kChunkInts * c;
+        tiles += (ci[1] - ci[0] + ci[3] - 1) / ci[3];
+      }
+      fprintf(stderr, "[lv] %s: P=%d tiles=%lld grid=%d hit_warp_tiles=%llu appends=%llu compactions=%llu wait_spins=%llu\n",
+              what, sa.P, (long long)tiles, grid, h[0], h[1], h[2], h[3]);
     }
-  }
-  if (timing) LV_CUDA(cudaEventRecord(ev[2], s));
-  // K4/K5 select + re-rank + top-k
+    return LV_OK;
+  };
   lv::RerankArgs ra;
   ra.m = (int)m;
   ra.m_pad = pl.m_pad;
@@ -584,8 +702,8 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   ra.k = k;
   ra.NS = NS2;
   ra.Cap = pl.Cap;
-  ra.cand = cand;
-  ra.cnt = cnt;
+  ra.cand = pc.cand;
+  ra.cnt = pc.cnt;
   ra.Q = Q;
   ra.X = ix->X_full;
   ra.full_f16 = ix->full == LV_F16;
@@ -593,8 +711,72 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   ra.scores = scores;
   ra.cand_ids = dbg ? dbg->cand_ids : nullptr;
   ra.cand_scores = dbg ? dbg->cand_scores : nullptr;
-  LV_CUDA(lv::launch_select_rerank(ra, s));
-  ++launches;
+  ra.qmap = nullptr;
+  ra.m_dev = nullptr;
+  ra.checked = 0;
+  ra.fail_count = nullptr;
+  ra.fail_list = nullptr;
+  if (!pl.sampled) {
+    // staged path: geometric stages with exact threshold merges in between
+    for (size_t k = 0; k < pl.chunks.size(); ++k) {
+      char nm[32];
+      snprintf(nm, sizeof nm, "stage %zu", k);
+      st = scan(chunk_info[k], pl.chunks[k], pl.QP, nm);
+      if (st) return st;
+      if (k + 1 < pl.chunks.size()) {
+        LV_CUDA(lv::launch_tau_merge(pc.cand, pc.cnt, pc.tau, NS2, (int)m, pl.m_pad, pl.Cap, R, s));
+        ++launches;
+      }
+    }
+    if (timing) LV_CUDA(cudaEventRecord(ev[2], s));
+    LV_CUDA(lv::launch_select_rerank(ra, s));
+    ++launches;
+  } else {
+    // sampled path: (1) sample stage -> block maxima; (2) per-query threshold with >= j1 rows
+    // above it; (3) one main stage with that threshold; (4) exactness check in the re-rank;
+    // (5) repair of the failed queries with the looser j2 threshold, then with none
+    sa.bmax = pc.bmax;
+    st = scan(chunk_info[0], pl.chunks[0], pl.QP, "sample");
+    if (st) return st;
+    sa.bmax = nullptr;
+    LV_CUDA(lv::launch_bmax_select(pc.bmax, pl.nblk, (int)m, pl.m_pad, pl.j1, pl.j2, pc.tau, pc.cnt, NS2, pc.tau2, s));
+    ++launches;
+    st = scan(chunk_info[1], pl.chunks[1], pl.QP, "main");
+    if (st) return st;
+    if (timing) LV_CUDA(cudaEventRecord(ev[2], s));
+    ra.checked = 1;
+    ra.fail_count = pc.fail + 0;
+    ra.fail_list = pc.fail_list;
+    LV_CUDA(lv::launch_select_rerank(ra, s));
+    ++launches;
+    for (int round = 0; round < 2; ++round) {
+      int32_t* flist = pc.fail_list + (size_t)round * pl.m_pad;
+      int32_t* fcount = pc.fail + round;
+      int32_t* mdev = pc.fail + 4 + round;
+      LV_CUDA(lv::launch_repair_setup(Qp, Cd, flist, fcount, pc.Qr, round == 0 ? pc.tau2 : nullptr, pc.tau, pc.cnt,
+                                      NS2, pl.m_pad, (int)m, mdev, s));
+      sa.Qp = pc.Qr;
+      sa.m_dev = mdev;
+      st = scan(pc.repair_info, pl.repair_chunks, 1, round == 0 ? "repair-1" : "repair-2");
+      if (st) return st;
+      ra.qmap = flist;
+      ra.m_dev = mdev;
+      ra.checked = round == 0 ? 1 : 0;
+      ra.fail_count = pc.fail + 1;
+      ra.fail_list = pc.fail_list + pl.m_pad;
+      LV_CUDA(lv::launch_select_rerank(ra, s));
+      launches += 2;
+    }
+    sa.Qp = Qp;
+    sa.m_dev = nullptr;
+    if (sa.stats) {
+      int32_t hf[2];
+      LV_CUDA(cudaMemcpyAsync(hf, pc.fail, sizeof hf, cudaMemcpyDeviceToHost, s));
+      LV_CUDA(cudaStreamSynchronize(s));
+      fprintf(stderr, "[lv] sampled: stride=%d nblk=%d j1=%d j2=%d failed=%d then %d\n", pl.stride, pl.nblk, pl.j1,
+              pl.j2, hf[0], hf[1]);
+    }
+  }
   if (timing) {
     LV_CUDA(cudaEventRecord(ev[3], s));
     LV_CUDA(cudaEventSynchronize(ev[3]));
@@ -610,6 +792,15 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
   }
   if (dbg) {
+    dbg->path = pl.sampled ? 1 : 0;
+    dbg->failed[0] = dbg->failed[1] = 0;
+    if (timing && pl.sampled) {
+      int32_t hf[2];
+      LV_CUDA(cudaMemcpyAsync(hf, pc.fail, sizeof hf, cudaMemcpyDeviceToHost, s));
+      LV_CUDA(cudaStreamSynchronize(s));
+      dbg->failed[0] = hf[0];
+      dbg->failed[1] = hf[1];
+    }
     dbg->launches = launches;
     dbg->slots = NS2;
     dbg->units = pl.total_units;

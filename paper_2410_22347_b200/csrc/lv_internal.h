@@ -13,6 +13,8 @@ namespace lv {
 
 void set_error(const char* fmt, ...);
 
+constexpr int kChunkInts = 5;   // chunk_info record: tile_begin, tile_end, cluster, tile_stride, sample_base
+
 // Work decomposition of the fused scan.
 struct ScanPlan {
   int QP = 0;          // query pairs (256 queries each)
@@ -27,16 +29,20 @@ struct ScanPlan {
 struct ScoreArgs {
   int m, m_pad, QP, d, C, R, P, NS, Cap, stages;
   const void* Qp;              // [m_pad, C*d] low dtype (q'_{j,c} for every c)
-  const int32_t* chunk_info;   // [P][3]: tile_begin, tile_end, cluster
+  const int32_t* chunk_info;   // [P][kChunkInts]: tile_begin, tile_end, cluster, tile_stride, sample_base
   const int32_t* tile_valid;   // [n_tiles]
   const int32_t* perm;         // [n_pad] or nullptr (identity)
   uint64_t* cand;              // [NS][m_pad][Cap]
   int32_t* cnt;                // [NS][m_pad]
   uint64_t* tau;               // [NS][m_pad]
-  int32_t* done;               // [P][QP]
+  int32_t* slot_busy;          // [QP] bitmask of claimed slots per query tile (zero between launches)
   float* raw;                  // [m_pad][n_pad] or nullptr
+  float* bmax;                 // sample stage: [n_sample_tiles * 4][m_pad] block maxima, else nullptr
+  const int32_t* m_dev;        // device query count (repair passes; overrides m and QP), or nullptr
   int64_t n_pad;
-  int flags;                   // debug: bit0 = epilogue skips top-R (MMA/TMA throughput probe)
+  int flags;                   // debug: bit0 = epilogue skips top-R (MMA/TMA throughput probe),
+                               //        bit1 = count events into stats, bit2 = detect hits but drop them
+  unsigned long long* stats;   // debug counters [8] or nullptr: hit warp-tiles, appends, compactions, wait spins
 };
 
 cudaError_t launch_score(const CUtensorMap* tmap_xlow, const ScoreArgs& a, bool bf16, int grid, size_t smem,
@@ -54,7 +60,17 @@ struct RerankArgs {
   float* scores;               // [m, k]
   int32_t* cand_ids;           // [m, R] or nullptr
   float* cand_scores;          // [m, R] or nullptr
+  const int32_t* qmap;         // list row -> query (Q row, output row), or nullptr (identity)
+  const int32_t* m_dev;        // device row count (rows >= it exit), or nullptr (m)
+  int checked;                 // rows with < R keys are not answered but appended to fail_list
+  int32_t* fail_count;
+  int32_t* fail_list;
 };
+cudaError_t launch_bmax_select(const float* bmax, int nblk, int m, int m_pad, int j1, int j2, uint64_t* tau,
+                               int32_t* cnt, int NS, uint64_t* tau2, cudaStream_t s);
+cudaError_t launch_repair_setup(const void* Qp, int Cd, const int32_t* fail_list, const int32_t* fail_count, void* Qr,
+                                const uint64_t* tau_src, uint64_t* tau, int32_t* cnt, int NS, int m_pad, int m_max,
+                                int32_t* m_out, cudaStream_t s);
 cudaError_t launch_select_rerank(const RerankArgs& a, cudaStream_t s);
 cudaError_t launch_tau_merge(uint64_t* cand, int32_t* cnt, uint64_t* tau, int NS, int m, int m_pad, int Cap, int R,
                              cudaStream_t s);

@@ -2,20 +2,20 @@
 //
 // s_ji = <q'_{j,c_i}, x_low_i>  (Eq.(15); C = 1 gives Eq.(9)) for every
 // database row i (exhaustive main step of Alg. 1), on tcgen05 tensor cores:
-//   A operand = 256 queries of one "query pair" (2 x M=128 tiles) held in TMEM (written with
-//     tcgen05.st by the epilogue warps, double-buffered across units), so the MMA reads only B
-//     from shared memory;
-//   B operand = N-row tiles (N = 64, or 32 for d >= 160) of X_low streamed by TMA through a
-//     STAGES-deep mbarrier ring;
-//   D = fp32 accumulators in TMEM, NACC buffers x 2 query tiles x N columns (512 - 2d columns).
-// Epilogue: one thread per query (TMEM lane), tcgen05.ld 32 columns at a time, max-reduce,
-// compare with the query's running threshold; survivors (rare) are appended as 64-bit keys
-// (ordered score, ~original id) to a per-(slot, query) buffer in global memory (L2); a full
-// buffer is compacted by the warp to its exact top-R, raising the threshold.  The m x n score
-// matrix never reaches HBM.
+//   A operand = the 128 queries of one query tile, held in TMEM (written with tcgen05.st by the
+//     fast epilogue warps, double-buffered across units), so the MMA reads only B from smem;
+//   B operand = 128-row tiles of X_low streamed by TMA through a STAGES-deep mbarrier ring;
+//   D = fp32 accumulators in TMEM, NACC buffers of 128 columns (the 512 - d columns left by A).
+// Epilogue (16 warps, 4 per SM sub-partition): thread = (query = TMEM lane, 32-column quarter
+// of the tile); tcgen05.ld.32x32b.x32 gives 32 scores whose max is compared with the thread's
+// threshold.  A warp with hitting lanes broadcasts each hitting lane's 32 scores through a
+// 128-byte shared-memory row; lane j tests column j and the survivors are appended as 64-bit keys
+// (ordered score, ~original id) to the hitting lane's sub-list in global memory (L2) with
+// coalesced stores; a full sub-list is compacted by the warp to its top-R, raising its threshold.
+// The m x n score matrix never reaches HBM.
 //
-// Work: units (database chunk c, query pair p), chunk-major, round-robin over a persistent grid.
-// Unit (c, p) continues the candidate list of slot c % NS left by unit (c - NS, p) (flag wait).
+// Work: units (database chunk c, query tile p), chunk-major, round-robin over a persistent grid;
+// a unit claims a free candidate slot of its query tile (slot lists persist across units).
 #include <cfloat>
 
 #include "lv_common.cuh"
@@ -24,15 +24,21 @@
 
 namespace lv {
 
-constexpr int kEpiWarps = 16;          // 4 per SM sub-partition
-constexpr int kThreads = 64 + 32 * kEpiWarps;   // warps 0..15 epilogue, 16 TMA, 17 MMA
+constexpr int kEpiWarps = 16;          // 4 per SM sub-partition (latency hiding of the hit path)
 // the producer warps get the highest ids: the warp scheduler favours high ids, so the
-// single-thread TMA/MMA issue loops are never starved by the 16 epilogue warps
+// single-thread TMA/MMA issue loops are never starved by the epilogue warps
 constexpr int kTmaWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
+constexpr int kThreads = 32 * (kEpiWarps + 2);
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kMaxKeysPerLane = 12;    // Cap <= 384
 
-constexpr uint32_t kEpiScratchBytes = (32 + 256) * 4;   // per epilogue warp: ids[32], hist[256]
+// Shared-memory epilogue state.
+struct EpiShared {
+  float rows[kEpiWarps][32][32];       // hitting lanes' 32 scores (row = lane), read column-wise
+  int hist[kEpiWarps][256];            // radix scratch of the compaction
+  int slot;                            // candidate slot of the current unit
+  int pad_[3];
+};
 
 struct ScoreSmemLayout {
   uint32_t b_off, epi_off, bar_off, total;
@@ -53,7 +59,7 @@ __host__ __device__ inline ScoreSmemLayout score_smem_layout(int d, int stages) 
   ScoreSmemLayout L;
   L.b_off = 0;
   L.epi_off = align_up((uint32_t)stages * (uint32_t)kTileN * (uint32_t)d * 2u, 1024);
-  L.bar_off = align_up(L.epi_off + (uint32_t)kEpiWarps * kEpiScratchBytes, 16);
+  L.bar_off = align_up(L.epi_off + (uint32_t)sizeof(EpiShared), 16);
   // barriers: b_full[stages], b_empty[stages], acc_full[kMaxAcc], acc_empty[kMaxAcc], a_full[2], tmem ptr
   L.total = L.bar_off + 8u * (2 * stages + 2 * kMaxAcc + 2) + 16;
   return L;
@@ -209,6 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int nacc = score_nacc(kD);
   const ScoreSmemLayout L = score_smem_layout(d, a.stages);
   uint8_t* sB = smem + L.b_off;
+  EpiShared& S = *reinterpret_cast<EpiShared*>(smem + L.epi_off);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* b_full = bars;
   uint64_t* b_empty = bars + a.stages;
@@ -219,8 +226,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int QT = a.QP;                      // 128-query tiles
+  const int m_eff = a.m_dev ? *a.m_dev : a.m;                  // repair passes read their size
+  const int QT = a.m_dev ? (m_eff + 127) / 128 : a.QP;         // 128-query tiles
   const int nunits = a.P * QT;
+  const bool skip_topr = (a.flags & 1) != 0;
+  const bool count_stats = (a.flags & 2) != 0 && a.stats != nullptr;
+  const bool fast_only = (a.flags & 4) != 0;   // debug: detect hits but drop them (fast-path cost probe)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
@@ -250,8 +261,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int c = u / QT;
-        const int t0 = a.chunk_info[3 * c], t1 = a.chunk_info[3 * c + 1];
-        for (int t = t0; t < t1; ++t) {
+        const int* ci = a.chunk_info + kChunkInts * c;
+        const int t0 = ci[0], t1 = ci[1], ts_ = ci[3];
+        for (int t = t0; t < t1; t += ts_) {
           tc::mbar_wait(b_empty + stage, phase ^ 1);
           tc::mbar_arrive_expect_tx(b_full + stage, nch * box_bytes);
           for (int k = 0; k < nch; ++k)
@@ -271,11 +283,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     int i = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
       const int c = u / QT;
-      const int t0 = a.chunk_info[3 * c], t1 = a.chunk_info[3 * c + 1];
+      const int* ci = a.chunk_info + kChunkInts * c;
+      const int t0 = ci[0], t1 = ci[1], ts_ = ci[3];
       tc::mbar_wait(a_full + (i & 1), (uint32_t)(i >> 1) & 1u);
       tc::tc_fence_after();
       const uint32_t at = tmem_base + (uint32_t)(i & 1) * (uint32_t)(d / 2);
-      for (int t = t0; t < t1; ++t) {
+      for (int t = t0; t < t1; t += ts_) {
         tc::mbar_wait(acc_empty + acc, acc_phase ^ 1);
         tc::mbar_wait(b_full + stage, phase);
         tc::tc_fence_after();
@@ -301,20 +314,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue: 16 warps
     // warp -> (TMEM lane quarter, 32-column quarter of every tile); thread = one query x one
-    // column quarter, with its own candidate sub-slot (4 per slot and query).
-    const int e = warp;
-    const int cq = e >> 2;           // column quarter of each 128-column tile
+    // column quarter, with its own candidate sub-list (4 per slot and query).
+    const int cq = warp >> 2;        // column quarter of each 128-column tile
     const int quarter = warp & 3;    // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
-    int* sid = reinterpret_cast<int*>(smem + L.epi_off + e * kEpiScratchBytes);
-    int* hist = sid + 32;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t lt = (1u << lane) - 1u;
     const int ldq = a.C * d;         // Q' row length (elements)
+    float (*srows)[32] = S.rows[warp];
+    int* hist = S.hist[warp];
     // A operand of unit u (its cluster's view of the tile's 128 queries) -> TMEM buffer b; this
     // warp writes K range [cq*d/4, (cq+1)*d/4) of its 32 rows (d/8 TMEM columns)
     auto write_A = [&](int u, int b) {
       const int c = u / QT, qt = u % QT;
-      const int cl = a.chunk_info[3 * c + 2];
+      const int cl = a.chunk_info[kChunkInts * c + 2];
       const int qq = qt * 128 + row;
       const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.Qp) +
                                                        (size_t)qq * ldq + (size_t)cl * d + cq * (d / 4));
@@ -358,29 +371,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
       if (u + (int)gridDim.x < nunits) write_A(u + gridDim.x, (i + 1) & 1);
       const int c = u / QT, qt = u % QT;
-      const int t0 = a.chunk_info[3 * c], t1 = a.chunk_info[3 * c + 1];
-      const int q0 = qt * 128 + quarter * 32;   // query of lane 0
-      const int q = q0 + lane;
-      const bool qvalid = q < a.m;
-      const int slot = (c % a.NS) * 4 + cq;
-      if (c >= a.NS) {
-        if (lane == 0) {
-          const int32_t* flag = a.done + (size_t)(c - a.NS) * QT + qt;
-          long long spins = 0;
-          while (ld_acquire(flag) == 0) {
-            __nanosleep(64);
-            if (++spins > (1ll << 27)) __trap();   // a lost dependency would otherwise hang the GPU
+      const int* ci = a.chunk_info + kChunkInts * c;
+      const int t0 = ci[0], t1 = ci[1], tstride = ci[3], sbase = ci[4];
+      const int t_last = t0 + (t1 - 1 - t0) / tstride * tstride;
+      const int q = qt * 128 + row;
+      const bool qvalid = q < m_eff;
+      // ---- unit start: claim a free candidate slot of query tile qt (units of one tile that run
+      // concurrently on different CTAs use different slots; a slot's lists carry over)
+      if (threadIdx.x == 0) {
+        int32_t* busy = a.slot_busy + qt;
+        long long spins = 0;
+        int got = -1;
+        while (got < 0) {
+          const int32_t cur = ld_acquire(busy);
+          const uint32_t freem = ~(uint32_t)cur & ((1u << a.NS) - 1u);
+          if (freem) {
+            const int sl = __ffs(freem) - 1;
+            if (atomicCAS(busy, cur, cur | (1 << sl)) == cur) got = sl;
+          } else {
+            __nanosleep(128);
+            if (count_stats) atomicAdd(a.stats + 3, 1ull);
+            if (++spins > (1ll << 27)) __trap();   // a lost release would otherwise hang the GPU
           }
         }
-        __syncwarp();
+        __threadfence();
+        S.slot = got;
       }
-      const size_t sbase = (size_t)slot * a.m_pad + q0;     // sub-slot index of lane 0
-      int cnt = a.cnt[sbase + lane];
-      uint64_t tk = a.tau[sbase + lane];
-      float ts = thr_score(tk);
-      const int tv_last = a.tile_valid[t1 - 1];
+      tc::named_bar_sync(1, kEpiThreads);
+      const int my_slot = S.slot;
+      const size_t si = (size_t)(my_slot * 4 + cq) * a.m_pad + q;   // this thread's sub-list
+      int cnt = a.cnt[si];
+      uint64_t tk = a.tau[si];
+      float ts = qvalid ? thr_score(tk) : FLT_MAX;   // padded queries never hit
+      uint64_t* const bp = a.cand + si * (size_t)a.Cap;
+      const int tv_last = a.tile_valid[t_last] - cq * 32;   // valid columns of the chunk's last tile
 
-      for (int t = t0; t < t1; ++t) {
+      for (int t = t0; t < t1; t += tstride) {
         tc::mbar_wait(acc_full + acc, acc_phase);
         tc::tc_fence_after();
         float v[32];
@@ -390,88 +416,79 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(acc_empty + acc);
         if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
-        if (a.flags & 1) continue;
-        const int64_t base_pos = (int64_t)t * kN + cq * 32;
-        const int tv = (t + 1 == t1 ? tv_last : kN) - cq * 32;   // valid columns of this chunk
-        if (tv < 32) {
+        if (skip_topr) continue;
+        const int base_pos = t * kN + cq * 32;
+        if (t == t_last && tv_last < 32) {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (j >= tv) v[j] = -FLT_MAX;
+            if (j >= tv_last) v[j] = -FLT_MAX;
         }
         if (a.raw != nullptr) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + base_pos + j] = v[j];
         }
-        // fast path: one max over the 32 scores, compared with the lane's threshold
-        float m8[8];
+        float mx = v[0];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) m8[j] = fmaxf(fmaxf(v[4 * j], v[4 * j + 1]), fmaxf(v[4 * j + 2], v[4 * j + 3]));
-        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-        const bool hit = qvalid && mx >= ts && mx > -FLT_MAX;
-        const uint32_t hits = __ballot_sync(0xffffffffu, hit);
-        if (hits == 0u) continue;
-        // slow path: a lane whose sub-slot could overflow is compacted first by the warp, then
-        // every hit lane appends its own survivors (groups of 4 whose max passes)
-        uint32_t need = __ballot_sync(0xffffffffu, hit && cnt > a.Cap - 32);
-        while (need) {
-          const int Lz = __ffs(need) - 1;
-          need &= need - 1u;
-          const int cL = __shfl_sync(0xffffffffu, cnt, Lz);
-          uint64_t nthr;
-          const int ncnt = warp_compact_fast(a.cand + (sbase + Lz) * (size_t)a.Cap, cL, a.R, a.Cap, lane, hist, &nthr);
-          if (lane == Lz) {
-            cnt = ncnt;
-            tk = nthr;
-            ts = thr_score(nthr);
-          }
+        for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
+        if (a.bmax != nullptr) {
+          // sample stage: record the block maximum (query q, 32 database rows); no top-R here
+          a.bmax[(size_t)((sbase + (t - t0) / tstride) * 4 + cq) * a.m_pad + q] = mx;
+          continue;
         }
-        if (a.perm) {
-          sid[lane] = a.perm[base_pos + lane];
-          __syncwarp();
-        }
+        const bool hit = mx >= ts && mx > -FLT_MAX;
+        uint32_t hb = __ballot_sync(0xffffffffu, hit);
+        if (hb == 0u) continue;
+        if (count_stats && lane == 0) atomicAdd(a.stats + 0, 1ull);
+        if (fast_only) continue;
+        // hit path (divergence-free): each hitting lane's 32 scores are broadcast through shared
+        // memory, lane j tests column j, survivors are appended to the hitting lane's sub-list with
+        // coalesced stores
+        const int my_pos = base_pos + lane;
+        const int32_t my_id = a.perm ? __ldg(a.perm + my_pos) : my_pos;
         if (hit) {
-          // groups of 4 whose max passes, one at a time; the group's 4 scores are picked by a
-          // switch (no dynamic register indexing), survivors appended by the lane itself
-          uint64_t* bp = a.cand + (sbase + lane) * (size_t)a.Cap;
-          uint32_t gm = 0;
 #pragma unroll
-          for (int gi = 0; gi < 8; ++gi) gm |= (m8[gi] >= ts) ? (1u << gi) : 0u;
-          while (gm) {
-            const int gi = __ffs(gm) - 1;
-            gm &= gm - 1u;
-            float f[4];
-            switch (gi) {
-#define LV_PICK(G)                \
-  case G:                         \
-    f[0] = v[4 * G];              \
-    f[1] = v[4 * G + 1];          \
-    f[2] = v[4 * G + 2];          \
-    f[3] = v[4 * G + 3];          \
-    break;
-              LV_PICK(0) LV_PICK(1) LV_PICK(2) LV_PICK(3) LV_PICK(4) LV_PICK(5) LV_PICK(6)
-              default: LV_PICK(7)
-#undef LV_PICK
-            }
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-              if (f[jj] >= ts && f[jj] > -FLT_MAX) {
-                const int j = 4 * gi + jj;
-                const int32_t id = a.perm ? sid[j] : (int32_t)(base_pos + j);
-                const uint64_t key = make_key(f[jj], id);
-                if (key > tk) bp[cnt++] = key;
-              }
-            }
-          }
+          for (int j = 0; j < 8; ++j)
+            reinterpret_cast<float4*>(srows[lane])[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         }
+        __syncwarp();
+        do {
+          const int Lz = __ffs(hb) - 1;
+          hb &= hb - 1u;
+          const float f = srows[Lz][lane];
+          const float tsz = __shfl_sync(0xffffffffu, ts, Lz);
+          uint64_t tkz = __shfl_sync(0xffffffffu, tk, Lz);
+          int cz = __shfl_sync(0xffffffffu, cnt, Lz);
+          const uint64_t key = make_key(f, my_id);
+          bool keep = f >= tsz && f > -FLT_MAX && key > tkz;
+          uint32_t kb = __ballot_sync(0xffffffffu, keep);
+          if (kb == 0u) continue;
+          uint64_t* bz = reinterpret_cast<uint64_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(bp), Lz));
+          if (cz + __popc(kb) > a.Cap) {
+            // full sub-list: compact it to its top-R (raises its threshold), then re-filter
+            uint64_t nthr;
+            cz = warp_compact_fast(bz, cz, a.R, a.Cap, lane, hist, &nthr);
+            tkz = nthr;
+            if (lane == Lz) {
+              tk = nthr;
+              ts = thr_score(nthr);
+            }
+            if (count_stats && lane == 0) atomicAdd(a.stats + 2, 1ull);
+            keep = keep && key > tkz;
+            kb = __ballot_sync(0xffffffffu, keep);
+          }
+          if (keep) bz[cz + __popc(kb & lt)] = key;
+          if (lane == Lz) cnt = cz + __popc(kb);
+          if (count_stats && lane == 0) atomicAdd(a.stats + 1, (unsigned long long)__popc(kb));
+        } while (hb != 0u);
         __syncwarp();
       }
       if (qvalid) {
-        a.cnt[sbase + lane] = cnt;
-        a.tau[sbase + lane] = tk;
+        a.cnt[si] = cnt;
+        a.tau[si] = tk;
       }
       __threadfence();
       tc::named_bar_sync(1, kEpiThreads);
-      if (threadIdx.x == 0) st_release(a.done + (size_t)c * QT + qt, 1);
+      if (threadIdx.x == 0) atomicAnd(a.slot_busy + qt, ~(1 << my_slot));   // release the slot
     }
   }
   tc::tc_fence_before();

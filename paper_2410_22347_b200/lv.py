@@ -31,7 +31,8 @@ class LVError(RuntimeError):
 class SearchDebug(ctypes.Structure):
     _fields_ = [("cand_ids", ctypes.c_void_p), ("cand_scores", ctypes.c_void_p), ("raw_scores", ctypes.c_void_p),
                 ("timing", ctypes.c_int32), ("phase_ms", ctypes.c_float * 4), ("launches", ctypes.c_int32),
-                ("slots", ctypes.c_int32), ("units", ctypes.c_int32), ("grid", ctypes.c_int32)]
+                ("slots", ctypes.c_int32), ("units", ctypes.c_int32), ("grid", ctypes.c_int32),
+                ("path", ctypes.c_int32), ("failed", ctypes.c_int32 * 2)]
 
 
 _lib = None
@@ -189,7 +190,7 @@ def lv_search(index: Index, Q: torch.Tensor, k: int, R: int, cand: bool = False,
     _check(lib().lv_search(index.h, _ptr(Q), m, k, R, _ptr(ids), _ptr(sc), ctypes.byref(dbg), _stream()),
            "lv_search")
     keep.update({"phase_ms": list(dbg.phase_ms), "launches": dbg.launches, "slots": dbg.slots,
-                 "units": dbg.units, "grid": dbg.grid})
+                 "units": dbg.units, "grid": dbg.grid, "path": dbg.path, "failed": list(dbg.failed)})
     return ids, sc, keep
 
 

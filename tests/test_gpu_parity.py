@@ -145,10 +145,10 @@ def test_mma_exact_operands(lv, d, low):
     assert np.all(raw[:m, n:] < -1e30)          # padded tail columns are masked
 
 
-def _check_search(lv, c, X, Q, A32, B32, assign, R, k, C, check_recall=True):
+def _check_search(lv, c, X, Q, A32, B32, assign, R, k, C, check_recall=True, timing=False):
     ix = _gpu_index(lv, c, X, A32, B32, assign, C)
     Qt = torch.from_numpy(Q).cuda()
-    ids, sc, dbg = lv.lv_search(ix, Qt, k, R, cand=True)
+    ids, sc, dbg = lv.lv_search(ix, Qt, k, R, cand=True, timing=timing)
     ids = ids.cpu().numpy().astype(np.int64)
     sc = sc.cpu().numpy().astype(np.float64)
     cid = dbg["cand_ids"].cpu().numpy().astype(np.int64)
@@ -316,3 +316,29 @@ def test_deterministic(lv):
     a = lv.lv_search(ix, Qt, k, R, cand=True)
     b = lv.lv_search(ix, Qt, k, R, cand=True)
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and torch.equal(a[2]["cand_ids"], b[2]["cand_ids"])
+
+
+def test_sampled_path_parity(lv):
+    """A database large enough (>= 64 sampled tiles) for the sampled-threshold path: sample stage
+    of block maxima, per-query threshold, one thresholded main scan, exactness check."""
+    c, X, Q, A32, B32, assign, R, k = _case(1, n=150_000, m=300, d=64)
+    dbg = _check_search(lv, c, X, Q, A32, B32, assign, R, k, 1, timing=True)
+    assert dbg["path"] == 1
+
+
+def test_sampled_path_repairs(lv, monkeypatch):
+    """A deliberately far too high sampled threshold (gamma 0.05: ~64 survivors for R = 256) makes
+    every query fail the exactness check; round 1 repairs with the looser bound (about half fail
+    again), round 2 without a threshold.  Results must still be the exact top-R / top-k."""
+    monkeypatch.setenv("LV_SAMPLE_GAMMA", "0.05")
+    c, X, Q, A32, B32, assign, _, k = _case(1, n=150_000, m=200, d=32)
+    dbg = _check_search(lv, c, X, Q, A32, B32, assign, 256, k, 1, check_recall=False, timing=True)
+    assert dbg["path"] == 1 and dbg["failed"][0] == Q.shape[0] and dbg["failed"][1] > 0, dbg["failed"]
+
+
+def test_sampled_path_gleanvec(lv):
+    """Sampled path on a cluster-sorted GleanVec index (C = 4): the sample is stratified per
+    cluster segment, block maxima are indexed across segments."""
+    c, X, Q, A32, B32, assign, R, k = _case(3, n=150_000, m=200, d=96, C=4)
+    dbg = _check_search(lv, c, X, Q, A32, B32, assign, R, k, 4, timing=True)
+    assert dbg["path"] == 1
