@@ -206,7 +206,9 @@ template <bool kBF16, int kD>
 __global__ void __launch_bounds__(kThreads, 1)
     k_score_topr(const __grid_constant__ CUtensorMap tmap_xlow, const ScoreArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base (SWIZZLE_128B atoms) as an offset into the shared array, so that every
+  // access through it stays in the shared address space (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int d = kD;
   constexpr int kCH = (kD % 64 == 0) ? 64 : 32;   // columns per swizzled TMA box (128 B or 64 B rows)
   constexpr int kN = kTileN;
@@ -378,7 +380,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool qvalid = q < m_eff;
       // ---- unit start: claim a free candidate slot of query tile qt (units of one tile that run
       // concurrently on different CTAs use different slots; a slot's lists carry over)
-      if (threadIdx.x == 0) {
+      const bool lists = a.bmax == nullptr;   // the sample stage keeps no candidate lists
+      if (lists && threadIdx.x == 0) {
         int32_t* busy = a.slot_busy + qt;
         long long spins = 0;
         int got = -1;
@@ -397,11 +400,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         __threadfence();
         S.slot = got;
       }
-      tc::named_bar_sync(1, kEpiThreads);
-      const int my_slot = S.slot;
+      if (lists) tc::named_bar_sync(1, kEpiThreads);
+      const int my_slot = lists ? S.slot : 0;
       const size_t si = (size_t)(my_slot * 4 + cq) * a.m_pad + q;   // this thread's sub-list
-      int cnt = a.cnt[si];
-      uint64_t tk = a.tau[si];
+      int cnt = lists ? a.cnt[si] : 0;
+      uint64_t tk = lists ? a.tau[si] : 0ull;
       float ts = qvalid ? thr_score(tk) : FLT_MAX;   // padded queries never hit
       uint64_t* const bp = a.cand + si * (size_t)a.Cap;
       const int tv_last = a.tile_valid[t_last] - cq * 32;   // valid columns of the chunk's last tile
@@ -482,13 +485,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         } while (hb != 0u);
         __syncwarp();
       }
-      if (qvalid) {
-        a.cnt[si] = cnt;
-        a.tau[si] = tk;
+      if (lists) {
+        if (qvalid) {
+          a.cnt[si] = cnt;
+          a.tau[si] = tk;
+        }
+        __threadfence();
+        tc::named_bar_sync(1, kEpiThreads);
+        if (threadIdx.x == 0) atomicAnd(a.slot_busy + qt, ~(1 << my_slot));   // release the slot
       }
-      __threadfence();
-      tc::named_bar_sync(1, kEpiThreads);
-      if (threadIdx.x == 0) atomicAnd(a.slot_busy + qt, ~(1 << my_slot));   // release the slot
     }
   }
   tc::tc_fence_before();
