@@ -27,10 +27,11 @@ __global__ void __launch_bounds__(256) k_rows_gemm(const TIn* __restrict__ in, i
   __shared__ float As[GK][GT + 4];
   __shared__ float Bs[GK][GT + 4];
   const int tid = threadIdx.x;
-  const int64_t r0 = (int64_t)blockIdx.y * GT;
-  const int c0 = blockIdx.x * GT;
+  // grid.x = row tiles (up to 2^31 - 1: n = 10^7 needs 156 250), grid.y = column tiles
+  const int64_t r0 = (int64_t)blockIdx.x * GT;
+  const int c0 = blockIdx.y * GT;
   if (c0 >= ncols) return;
-  const int wrow = tile_wrow64 ? tile_wrow64[blockIdx.y] : 0;
+  const int wrow = tile_wrow64 ? tile_wrow64[blockIdx.x] : 0;
   const int lr = tid >> 2, lk = (tid & 3) * 8;     // loader: one row (col), 8 consecutive k
   int64_t src = r0 + lr;
   if (rowidx) src = rowidx[r0 + lr];
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(256) k_rows_gemm(const TIn* __restrict__ in, i
 cudaError_t launch_rows_gemm(const void* in, int in_f16, int64_t ld_in, const int32_t* rowidx, int64_t rows_valid,
                              int64_t nrows, const float* W, int K, const int32_t* tile_wrow64, int ncols, void* out,
                              int out_dtype, int64_t ld_out, int64_t rows_store, cudaStream_t s) {
-  dim3 grid((ncols + GT - 1) / GT, (unsigned)((nrows + GT - 1) / GT));
+  dim3 grid((unsigned)((nrows + GT - 1) / GT), (ncols + GT - 1) / GT);
 #define LV_GEMM_CASE(TI, TO) \
   k_rows_gemm<TI, TO><<<grid, 256, 0, s>>>((const TI*)in, ld_in, rowidx, rows_valid, W, K, tile_wrow64, ncols, (TO*)out, ld_out, rows_store)
   if (in_f16) {
