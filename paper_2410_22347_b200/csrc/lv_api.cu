@@ -38,6 +38,8 @@ struct PlanCache {
   uint64_t* cand = nullptr;
   int32_t* cnt = nullptr;
   uint64_t* tau = nullptr;
+  void* Qplanes = nullptr;     // bf16 [3][m_pad][Kp]: Q split for the K1 GEMM
+  CUtensorMap tmap_q;
   uint64_t* tau2 = nullptr;    // sampled: per-query repair threshold
   float* bmax = nullptr;       // sampled: block maxima of the sample stage
   int32_t* fail = nullptr;     // [4]: fail counts of the two checks, repair row counts
@@ -53,6 +55,9 @@ struct lv_index {
   lv_dtype low = LV_BF16, full = LV_F32;
   float* A = nullptr;          // [C*d, D]
   float* B = nullptr;          // [C*d, D]
+  int32_t Kp = 0;              // D rounded up to 64 (K1 operand planes)
+  void* A_planes = nullptr;    // bf16 [3][C*d][Kp]: A split v = h + m + l (lv_proj.cu)
+  CUtensorMap tmap_a;          // A planes, 128-row x 64-column boxes
   int64_t n = 0, n_pad = 0;
   void* X_low = nullptr;       // [n_pad, d] low dtype, cluster-sorted, 128-row padded segments
   int32_t* perm = nullptr;     // [n_pad] sorted position -> original id (-1 padding)
@@ -142,6 +147,12 @@ lv_status make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t co
 double env_double(const char* name, double dflt) {
   const char* v = getenv(name);
   return v ? atof(v) : dflt;
+}
+
+// K1 on tensor cores (lv_proj.cu) unless LV_K1=simt (fp32 CUDA-core GEMM)
+bool k1_tensor() {
+  const char* v = getenv("LV_K1");
+  return !(v && v[0] == 's');
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -455,6 +466,23 @@ lv_status lv_index_create(lv_index** out, int32_t D, int32_t d, int32_t C, lv_dt
     lv_index_destroy(ix);
     return fail(LV_ECUDA, "lv_index_create: copy failed");
   }
+  // K1 operand: A split into three bf16 planes once per index
+  ix->Kp = (D + 63) / 64 * 64;
+  const int64_t Nc = (int64_t)C * d;
+  if (cudaMalloc(&ix->A_planes, (size_t)3 * Nc * ix->Kp * 2) != cudaSuccess) {
+    lv_index_destroy(ix);
+    return fail(LV_ENOMEM, "lv_index_create: cudaMalloc failed");
+  }
+  if (lv::launch_split3(ix->A, Nc, Nc, D, ix->Kp, ix->A_planes, 0) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
+    lv_index_destroy(ix);
+    return fail(LV_ECUDA, "lv_index_create: split failed");
+  }
+  st = make_tmap(&ix->tmap_a, ix->A_planes, 3 * Nc, ix->Kp, 64, true, 128);
+  if (st) {
+    lv_index_destroy(ix);
+    return st;
+  }
   *out = ix;
   return LV_OK;
 }
@@ -554,8 +582,26 @@ lv_status lv_project_queries(const lv_index* ix, const float* Q, int64_t m, void
   lv_status st = check_device();
   if (st) return st;
   if (!ix || !Q || !Qp || m <= 0) return fail(LV_EINVAL, "lv_project_queries: bad arguments");
-  LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, m, ix->A, ix->D, nullptr, ix->C * ix->d, Qp, ix->low,
-                               (int64_t)ix->C * ix->d, m, (cudaStream_t)stream));
+  if (m > (1 << 24)) return fail(LV_EINVAL, "lv_project_queries: m too large");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!k1_tensor()) {
+    LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, m, ix->A, ix->D, nullptr, ix->C * ix->d, Qp, ix->low,
+                                 (int64_t)ix->C * ix->d, m, s));
+    return LV_OK;
+  }
+  const int64_t m_pad = (m + 127) / 128 * 128;
+  void* planes = nullptr;
+  LV_CUDA(cudaMallocAsync(&planes, (size_t)3 * m_pad * ix->Kp * 2, s));
+  CUtensorMap tq;
+  st = make_tmap(&tq, planes, 3 * m_pad, ix->Kp, 64, true, 128);
+  if (st) {
+    cudaFreeAsync(planes, s);
+    return st;
+  }
+  LV_CUDA(lv::launch_split3(Q, m, m_pad, ix->D, ix->Kp, planes, s));
+  LV_CUDA(lv::launch_proj_tc(&tq, &ix->tmap_a, (int)m_pad, ix->C * ix->d, ix->Kp, Qp, (int64_t)ix->C * ix->d, (int)m,
+                             ix->low == LV_BF16, s));
+  LV_CUDA(cudaFreeAsync(planes, s));
   return LV_OK;
 }
 
@@ -581,7 +627,8 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     for (auto& ch : pl.chunks) nchunk_ints += ch.size() + 1;
     const int NS2 = 4 * pl.NS;   // sub-lists per query
     const size_t mp = pl.m_pad;
-    size_t need = (mp * Cd * 2 + 256) + ((size_t)NS2 * mp * pl.Cap * 8 + 256) + ((size_t)NS2 * mp * 4 + 256) +
+    size_t need = (mp * Cd * 2 + 256) + ((size_t)3 * mp * ix->Kp * 2 + 256) + ((size_t)NS2 * mp * pl.Cap * 8 + 256) +
+                  ((size_t)NS2 * mp * 4 + 256) +
                   ((size_t)NS2 * mp * 8 + 256) + ((size_t)pl.QP * 4 + 256) + (16 * 4 + 256) +
                   (nchunk_ints * 4 + 256 * (pl.chunks.size() + 2));
     if (pl.sampled)
@@ -596,6 +643,9 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     }
     uint8_t* p = reinterpret_cast<uint8_t*>(ix->ws);
     pc.Qp = carve<uint16_t>(p, mp * Cd);
+    pc.Qplanes = carve<uint16_t>(p, (size_t)3 * mp * ix->Kp);
+    st = make_tmap(&pc.tmap_q, pc.Qplanes, 3 * (int64_t)mp, ix->Kp, 64, true, 128);
+    if (st) return st;
     pc.cand = carve<uint64_t>(p, (size_t)NS2 * mp * pl.Cap);
     pc.zero_lo = p;
     pc.cnt = carve<int32_t>(p, (size_t)NS2 * mp);
@@ -638,8 +688,15 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   int launches = 0;
   LV_CUDA(cudaMemsetAsync(pc.zero_lo, 0, pc.zero_hi - pc.zero_lo, s));
   // K1 projection (rows >= m are zero)
-  LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, pl.m_pad, ix->A, ix->D, nullptr, Cd, Qp, ix->low, Cd, pl.m_pad, s));
-  ++launches;
+  if (k1_tensor()) {
+    LV_CUDA(lv::launch_split3(Q, m, pl.m_pad, ix->D, ix->Kp, pc.Qplanes, s));
+    LV_CUDA(lv::launch_proj_tc(&pc.tmap_q, &ix->tmap_a, pl.m_pad, Cd, ix->Kp, Qp, Cd, pl.m_pad, ix->low == LV_BF16, s));
+    launches += 2;
+  } else {
+    LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, pl.m_pad, ix->A, ix->D, nullptr, Cd, Qp, ix->low, Cd,
+                                 pl.m_pad, s));
+    ++launches;
+  }
   if (timing) LV_CUDA(cudaEventRecord(ev[1], s));
   lv::ScoreArgs sa;
   sa.Qp = Qp;
@@ -873,6 +930,7 @@ void lv_index_destroy(lv_index* ix) {
   free_db(ix);
   cudaFree(ix->A);
   cudaFree(ix->B);
+  cudaFree(ix->A_planes);
   cudaFree(ix->ws);
   cudaFree(ix->hs);
   delete ix;

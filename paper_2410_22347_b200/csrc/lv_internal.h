@@ -79,6 +79,11 @@ cudaError_t launch_tau_merge(uint64_t* cand, int32_t* cnt, uint64_t* tau, int NS
 cudaError_t launch_rows_gemm(const void* in, int in_f16, int64_t ld_in, const int32_t* rowidx, int64_t rows_valid,
                              int64_t nrows, const float* W, int K, const int32_t* tile_wrow64, int ncols,
                              void* out, int out_dtype, int64_t ld_out, int64_t rows_store, cudaStream_t s);
+// K1 on tensor cores (lv_proj.cu): three-plane bf16 split and the six-product GEMM.
+cudaError_t launch_split3(const float* in, int64_t rows_valid, int64_t rows_pad, int D, int Kp, void* out,
+                          cudaStream_t s);
+cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a, int m_pad, int Nc, int Kp, void* out,
+                           int64_t ld_out, int rows_store, bool out_bf16, cudaStream_t s);
 cudaError_t launch_iota_perm(int32_t* perm, int64_t n, int64_t n_pad, cudaStream_t s);
 
 cudaError_t launch_stats(const void* in, int in_f16, int64_t ld, const int32_t* rowidx, int nchunks,
