@@ -45,6 +45,8 @@ struct PlanCache {
   int32_t* fail = nullptr;     // [4]: fail counts of the two checks, repair row counts
   int32_t* fail_list = nullptr;   // [2][m_pad]
   int32_t* slot_busy = nullptr;
+  int32_t* sel_ids = nullptr;  // [m_pad][R]
+  int32_t* sel_n = nullptr;    // [m_pad]
   uint8_t *zero_lo = nullptr, *zero_hi = nullptr;
   std::vector<int32_t*> chunk_info;
   int32_t* repair_info = nullptr;
@@ -630,6 +632,7 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     size_t need = (mp * Cd * 2 + 256) + ((size_t)3 * mp * ix->Kp * 2 + 256) + ((size_t)NS2 * mp * pl.Cap * 8 + 256) +
                   ((size_t)NS2 * mp * 4 + 256) +
                   ((size_t)NS2 * mp * 8 + 256) + ((size_t)pl.QP * 4 + 256) + (16 * 4 + 256) +
+                  (mp * (size_t)R * 4 + 256) + (mp * 4 + 256) +
                   (nchunk_ints * 4 + 256 * (pl.chunks.size() + 2));
     if (pl.sampled)
       need += (mp * Cd * 2 + 256) + (mp * 8 + 256) + ((size_t)pl.nblk * mp * 4 + 256) + (2 * mp * 4 + 256);
@@ -651,6 +654,8 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     pc.cnt = carve<int32_t>(p, (size_t)NS2 * mp);
     pc.tau = carve<uint64_t>(p, (size_t)NS2 * mp);
     pc.slot_busy = carve<int32_t>(p, (size_t)pl.QP);
+    pc.sel_ids = carve<int32_t>(p, mp * (size_t)R);
+    pc.sel_n = carve<int32_t>(p, mp);
     pc.fail = carve<int32_t>(p, 16);
     pc.zero_hi = p;
     if (pl.sampled) {
@@ -773,6 +778,8 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   ra.checked = 0;
   ra.fail_count = nullptr;
   ra.fail_list = nullptr;
+  ra.sel_ids = pc.sel_ids;
+  ra.sel_n = pc.sel_n;
   if (!pl.sampled) {
     // staged path: geometric stages with exact threshold merges in between
     for (size_t k = 0; k < pl.chunks.size(); ++k) {

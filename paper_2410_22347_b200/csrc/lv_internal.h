@@ -65,6 +65,8 @@ struct RerankArgs {
   int checked;                 // rows with < R keys are not answered but appended to fail_list
   int32_t* fail_count;
   int32_t* fail_list;
+  int32_t* sel_ids;            // [m_pad][R] workspace: N_low of each list row (K4 -> K5)
+  int32_t* sel_n;              // [m_pad] its size (0: row failed the check)
 };
 cudaError_t launch_bmax_select(const float* bmax, int nblk, int m, int m_pad, int j1, int j2, uint64_t* tau,
                                int32_t* cnt, int NS, uint64_t* tau2, cudaStream_t s);

@@ -145,177 +145,292 @@ cudaError_t launch_tau_merge(uint64_t* cand, int32_t* cnt, uint64_t* tau, int NS
 // List row r belongs to query q = qmap ? qmap[r] : r (Q row and output row).  With `checked`, a
 // row holding fewer than R keys is not answered: its q is appended to fail_list (the thresholded
 // scan missed part of its top-R, see lv_api.cu) and a later repair pass answers it.
-template <bool kF16>
-__global__ void __launch_bounds__(kRrThreads) k_select_rerank(const RerankArgs a) {
-  __shared__ uint64_t sel[kMaxR];
-  __shared__ uint64_t fin[kMaxR];
-  __shared__ int s_off[65];
-  __shared__ int hist[256];
-  __shared__ int s_sel, s_want;
-  __shared__ uint64_t s_prefix;
-  __shared__ float sQ[1024];
-  const int r = blockIdx.x;
-  if (a.m_dev != nullptr && r >= *a.m_dev) return;
+
+// K4: N_low(j) = the R largest keys over the union of the row's candidate lists (an unordered set
+// is enough for K5; the debug output is sorted).  One warp per list row: the keys are staged in
+// shared memory (up to kStageKeys, else read from L2 in every pass), the R-th largest key is found
+// by an MSB-first 8-bit radix select that stops as soon as the boundary bin holds exactly the keys
+// still wanted (keys are unique, so the selection is exact), and the keys >= it are compacted.
+constexpr int kSelW = 4;              // warps (list rows) per CTA
+constexpr int kStageKeys = 1024;      // keys staged per warp
+__global__ void __launch_bounds__(kSelW * 32) k_select_topr(const RerankArgs a) {
+  __shared__ uint64_t s_keys[kSelW][kStageKeys];
+  __shared__ int s_hist[kSelW][256];
+  __shared__ uint64_t s_dbg[kSelW][kMaxR > 256 ? 256 : kMaxR];   // debug: sorted N_low
+  __shared__ int s_offs[kSelW][65];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kSelW + warp;
+  const int mrows = a.m_dev ? *a.m_dev : a.m;
+  if (r >= mrows) return;
   const int q = a.qmap ? a.qmap[r] : r;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t* keys = s_keys[warp];
+  int* hist = s_hist[warp];
+  const uint32_t lt = (1u << lane) - 1u;
   // list sizes and offsets (NS <= 64: lane l holds lists l and l + 32)
-  if (warp == 0) {
-    const int c0 = lane < a.NS ? a.cnt[(size_t)lane * a.m_pad + r] : 0;
-    const int c1 = lane + 32 < a.NS ? a.cnt[(size_t)(lane + 32) * a.m_pad + r] : 0;
-    int i0 = c0, i1 = c1;
+  const int c0 = lane < a.NS ? a.cnt[(size_t)lane * a.m_pad + r] : 0;
+  const int c1 = lane + 32 < a.NS ? a.cnt[(size_t)(lane + 32) * a.m_pad + r] : 0;
+  int e0 = c0, e1 = c1;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t0 = __shfl_up_sync(0xffffffffu, i0, o), t1 = __shfl_up_sync(0xffffffffu, i1, o);
-      if (lane >= o) { i0 += t0; i1 += t1; }
-    }
-    const int tot0 = __shfl_sync(0xffffffffu, i0, 31);
-    s_off[lane + 1] = i0;
-    s_off[lane + 33] = tot0 + i1;
-    if (lane == 0) s_off[0] = 0;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t0 = __shfl_up_sync(0xffffffffu, e0, o), t1 = __shfl_up_sync(0xffffffffu, e1, o);
+    if (lane >= o) { e0 += t0; e1 += t1; }
   }
-  for (int i = tid; i < a.D; i += blockDim.x) sQ[i] = a.Q[(size_t)q * a.D + i];
-  __syncthreads();
-  const int total = s_off[a.NS];
+  const int tot0 = __shfl_sync(0xffffffffu, e0, 31);
+  const int total = tot0 + __shfl_sync(0xffffffffu, e1, 31);
+  e0 -= c0;                  // exclusive offsets
+  e1 = tot0 + e1 - c1;
   if (a.checked && total < a.R) {
-    if (tid == 0) a.fail_list[atomicAdd(a.fail_count, 1)] = q;
+    if (lane == 0) {
+      a.fail_list[atomicAdd(a.fail_count, 1)] = q;
+      a.sel_n[r] = 0;
+    }
     return;
   }
   const int R = min(a.R, total);
-  // key i of the concatenated lists (binary search of the list)
+  const bool staged = total <= kStageKeys;
+  if (staged) {
+    // lane l copies lists l and l + 32 (lists are short: ~total / NS keys; loads pipelined)
+    const uint64_t* src0 = a.cand + ((size_t)lane * a.m_pad + r) * (size_t)a.Cap;
+    const uint64_t* src1 = a.cand + ((size_t)(lane + 32) * a.m_pad + r) * (size_t)a.Cap;
+#pragma unroll 4
+    for (int i = 0; i < c0; ++i) keys[e0 + i] = src0[i];
+#pragma unroll 4
+    for (int i = 0; i < c1; ++i) keys[e1 + i] = src1[i];
+    __syncwarp();
+  }
+  // key i of the concatenated lists (staged: shared memory; else: L2, list found by a per-lane
+  // binary search of the offset table)
+  int* offs = s_offs[warp];
+  if (!staged) {
+    offs[lane] = e0;
+    offs[lane + 32] = e1;
+    if (lane == 0) offs[64] = total;
+    __syncwarp();
+  }
   auto key_at = [&](int i) -> uint64_t {
-    int lo = 0, hi = a.NS;   // s_off[lo] <= i < s_off[hi]
+    if (staged) return keys[i];
+    int lo = 0, hi = a.NS;   // offs[lo] <= i < offs[hi]
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (s_off[mid] <= i) lo = mid; else hi = mid;
+      if (offs[mid] <= i) lo = mid; else hi = mid;
     }
-    return a.cand[((size_t)lo * a.m_pad + r) * (size_t)a.Cap + (i - s_off[lo])];
+    return a.cand[((size_t)lo * a.m_pad + r) * (size_t)a.Cap + (i - offs[lo])];
   };
-  // ---- R-th largest key: 8-bit MSB radix select (keys are unique, the result is exact)
-  uint64_t kth = 0ull;
+  uint64_t kth = 0ull;   // keys >= kth are N_low
   if (total > R) {
-    if (tid == 0) {
-      s_prefix = 0ull;
-      s_want = R;
-    }
-    uint64_t mask = 0ull;
+    uint64_t prefix = 0ull, mask = 0ull;
+    int want = R;
     for (int pass = 0; pass < 8; ++pass) {
       const int shift = 56 - 8 * pass;
-      for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
-      __syncthreads();
-      const uint64_t prefix = s_prefix;
-      for (int i0 = 0; i0 < total; i0 += blockDim.x) {
-        const int i = i0 + tid;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) hist[lane + 32 * j] = 0;
+      __syncwarp();
+      for (int i0 = 0; i0 < total; i0 += 32) {
+        const int i = i0 + lane;
         const uint64_t k = i < total ? key_at(i) : 0ull;
         warp_hist_add(hist, (i < total && (k & mask) == prefix) ? (int)((k >> shift) & 255) : -1);
       }
-      __syncthreads();
-      if (warp == 0) {
-        int loc[8], sum = 0;
+      __syncwarp();
+      int loc[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        loc[j] = hist[255 - 8 * lane - j];
+        sum += loc[j];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int excl = incl - sum;
+      const uint32_t who = __ballot_sync(0xffffffffu, excl < want && incl >= want);
+      const int src = __ffs(who) - 1;
+      int dg = 0, cum = excl, binc = 0;
+      if (lane == src) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          loc[j] = hist[255 - 8 * lane - j];
-          sum += loc[j];
-        }
-        int incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        const int want = s_want;
-        const int excl = incl - sum;
-        if ((excl < want) && (incl >= want)) {
-          int cum = excl, dg = 0;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (cum + loc[j] >= want) {
-              dg = 255 - 8 * lane - j;
-              break;
-            }
-            cum += loc[j];
+          if (cum + loc[j] >= want) {
+            dg = 255 - 8 * lane - j;
+            binc = loc[j];
+            break;
           }
-          s_prefix = prefix | ((uint64_t)dg << shift);
-          s_want = want - cum;
+          cum += loc[j];
         }
       }
-      mask |= (255ull << shift);
-      __syncthreads();
+      dg = __shfl_sync(0xffffffffu, dg, src);
+      cum = __shfl_sync(0xffffffffu, cum, src);
+      binc = __shfl_sync(0xffffffffu, binc, src);
+      prefix |= (uint64_t)dg << shift;
+      mask |= 255ull << shift;
+      want -= cum;
+      __syncwarp();
+      if (binc == want) break;   // every key of the boundary bin is selected: its lower edge is exact
     }
-    kth = s_prefix;
+    kth = prefix;   // lower edge of the resolved bin (remaining low bits zero)
   }
-  // ---- gather the R selected keys, sort them (deterministic candidate order)
-  int npow = 1;
-  while (npow < R) npow <<= 1;
-  for (int i = tid; i < npow; i += blockDim.x) sel[i] = 0ull;
-  if (tid == 0) s_sel = 0;
-  __syncthreads();
-  for (int i = tid; i < total; i += blockDim.x) {
-    const uint64_t k = key_at(i);
-    if (k >= kth) sel[atomicAdd(&s_sel, 1)] = k;
+  // compact the selected keys (>= kth) to the front of the staging buffer / straight to sel_ids
+  int32_t* out = a.sel_ids + (size_t)r * a.R;
+  int w = 0;
+  for (int i0 = 0; i0 < total; i0 += 32) {
+    const int i = i0 + lane;
+    const uint64_t k = i < total ? key_at(i) : 0ull;
+    const bool take = i < total && k >= kth;
+    const uint32_t b = __ballot_sync(0xffffffffu, take);
+    if (take) out[w + __popc(b & lt)] = key_id(k);
+    if (take && a.cand_ids != nullptr) s_dbg[warp][w + __popc(b & lt)] = k;   // debug copy
+    w += __popc(b);
   }
-  block_sort_desc(sel, npow);
+  if (lane == 0) a.sel_n[r] = R;
   if (a.cand_ids != nullptr) {
-    for (int i = tid; i < a.R; i += blockDim.x) {
-      a.cand_ids[(size_t)q * a.R + i] = (i < R) ? key_id(sel[i]) : -1;
-      if (a.cand_scores) a.cand_scores[(size_t)q * a.R + i] = (i < R) ? key_score(sel[i]) : 0.f;
+    // debug: N_low sorted by (reduced score desc, id asc) -- warp bitonic sort of the R keys
+    uint64_t* sk = s_dbg[warp];
+    __syncwarp();
+    // move the R keys to the front, pad to a power of two with zeros, sort descending
+    int npow = 1;
+    while (npow < R) npow <<= 1;
+    for (int i = R + lane; i < npow; i += 32) sk[i] = 0ull;
+    __syncwarp();
+    for (int size = 2; size <= npow; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = lane; t < npow / 2; t += 32) {
+          const int lo = 2 * t - (t & (stride - 1));
+          const int hi = lo + stride;
+          const bool desc = ((lo & size) == 0);
+          const uint64_t x = sk[lo], y = sk[hi];
+          if ((x < y) == desc) {
+            sk[lo] = y;
+            sk[hi] = x;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    for (int i = lane; i < a.R; i += 32) {
+      a.cand_ids[(size_t)q * a.R + i] = (i < R) ? key_id(sk[i]) : -1;
+      if (a.cand_scores) a.cand_scores[(size_t)q * a.R + i] = (i < R) ? key_score(sk[i]) : 0.f;
     }
   }
-  // ---- re-rank: one warp per candidate row (two rows in flight), fp32 FMA, 16-byte loads
-  for (int i = tid; i < npow; i += blockDim.x) fin[i] = 0ull;
-  __syncthreads();
+}
+
+// K5: r_ji = <q_j, x_i> in fp32 for the R candidates of list row r (Alg. 1 line 3) and the
+// top-k by (r desc, id asc).  One warp per row; lane l holds the 16-byte vectors l, l + 32, ... of
+// q and of each database row; G rows are loaded before their FMAs (G * kVPL 16-byte loads in flight
+// per lane); candidate i's key lands in lane i % 32, slot i / 32; top-k by k warp-wide maxima.
+template <bool kF16, int kVPL>
+__global__ void __launch_bounds__(128) k_rerank_topk(const RerankArgs a) {
   constexpr int vec = kF16 ? 8 : 4;
+  constexpr int G = kVPL >= 4 ? 2 : (kVPL == 3 ? 2 : 4);   // rows in flight per warp
+  constexpr int kSlots = kMaxR / 32 > 8 ? 8 : kMaxR / 32;   // R <= 256
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 4 + warp;
+  const int mrows = a.m_dev ? *a.m_dev : a.m;
+  if (r >= mrows) return;
+  const int R = a.sel_n[r];
+  if (R <= 0) return;   // failed the exactness check: answered by the repair pass
+  const int q = a.qmap ? a.qmap[r] : r;
   const int nvec = a.D / vec;
-  auto dot = [&](int32_t id) -> float {
-    float acc = 0.f;
-    if (kF16) {
-      const uint4* row = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(a.X) + (size_t)id * a.D);
-      for (int v = lane; v < nvec; v += 32) {
-        const uint4 u = __ldg(row + v);
-        const __half2* hp = reinterpret_cast<const __half2*>(&u);
+  float qv[kVPL * vec];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = __half22float2(hp[j]);
-          acc = fmaf(f.x, sQ[v * 8 + 2 * j], acc);
-          acc = fmaf(f.y, sQ[v * 8 + 2 * j + 1], acc);
+  for (int j = 0; j < kVPL; ++j) {
+    const int v = lane + 32 * j;
+#pragma unroll
+    for (int e = 0; e < vec; ++e) qv[j * vec + e] = v < nvec ? a.Q[(size_t)q * a.D + v * vec + e] : 0.f;
+  }
+  const int32_t* ids = a.sel_ids + (size_t)r * a.R;
+  const size_t rowbytes = (size_t)a.D * (kF16 ? 2 : 4);
+  uint64_t kk[kSlots];
+#pragma unroll
+  for (int sl = 0; sl < kSlots; ++sl) {
+    kk[sl] = 0ull;
+    if (sl * 32 >= R) continue;
+#pragma unroll 1
+    for (int i0 = sl * 32; i0 < min(R, sl * 32 + 32); i0 += G) {
+      int32_t id[G];
+      uint4 u[G][kVPL];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        id[g] = i0 + g < R ? ids[i0 + g] : ids[i0];
+        const uint4* row = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(a.X) + (size_t)id[g] * rowbytes);
+#pragma unroll
+        for (int j = 0; j < kVPL; ++j) {
+          const int v = lane + 32 * j;
+          u[g][j] = v < nvec ? __ldg(row + v) : make_uint4(0u, 0u, 0u, 0u);
         }
       }
-    } else {
-      const float4* row = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.X) + (size_t)id * a.D);
-      for (int v = lane; v < nvec; v += 32) {
-        const float4 f = __ldg(row + v);
-        acc = fmaf(f.x, sQ[v * 4 + 0], acc);
-        acc = fmaf(f.y, sQ[v * 4 + 1], acc);
-        acc = fmaf(f.z, sQ[v * 4 + 2], acc);
-        acc = fmaf(f.w, sQ[v * 4 + 3], acc);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < kVPL; ++j) {
+          if (kF16) {
+            const __half2* h = reinterpret_cast<const __half2*>(&u[g][j]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __half22float2(h[e]);
+              acc = fmaf(f.x, qv[j * 8 + 2 * e], acc);
+              acc = fmaf(f.y, qv[j * 8 + 2 * e + 1], acc);
+            }
+          } else {
+            const float4 f = *reinterpret_cast<const float4*>(&u[g][j]);
+            acc = fmaf(f.x, qv[j * 4 + 0], acc);
+            acc = fmaf(f.y, qv[j * 4 + 1], acc);
+            acc = fmaf(f.z, qv[j * 4 + 2], acc);
+            acc = fmaf(f.w, qv[j * 4 + 3], acc);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        const int i = i0 + g;
+        if (i < R && lane == (i & 31)) kk[sl] = make_key(acc, id[g]);
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    return acc;
-  };
-  constexpr int kRW = kRrThreads / 32;
-  for (int i = warp; i < R; i += 2 * kRW) {
-    const int i2 = i + kRW;
-    const int32_t id = key_id(sel[i]);
-    const int32_t id2 = i2 < R ? key_id(sel[i2]) : id;
-    const float r1 = dot(id);
-    const float r2 = dot(id2);
-    if (lane == 0) {
-      fin[i] = make_key(r1, id);
-      if (i2 < R) fin[i2] = make_key(r2, id2);
-    }
   }
-  block_sort_desc(fin, npow);
-  for (int i = tid; i < a.k; i += blockDim.x) {
-    a.ids[(size_t)q * a.k + i] = key_id(fin[i]);
-    a.scores[(size_t)q * a.k + i] = key_score(fin[i]);
+  // top-k: k rounds of a warp-wide maximum of the lanes' best keys
+  for (int t = 0; t < a.k; ++t) {
+    uint64_t best = 0ull;
+    int bs = -1;
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl)
+      if (kk[sl] > best) {
+        best = kk[sl];
+        bs = sl;
+      }
+    uint64_t w = best;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t x = __shfl_xor_sync(0xffffffffu, w, o);
+      w = x > w ? x : w;
+    }
+    if (best == w && w != 0ull) {
+#pragma unroll
+      for (int sl = 0; sl < kSlots; ++sl)
+        if (sl == bs) kk[sl] = 0ull;
+    }
+    if (lane == 0) {
+      a.ids[(size_t)q * a.k + t] = w ? key_id(w) : -1;
+      a.scores[(size_t)q * a.k + t] = w ? key_score(w) : 0.f;
+    }
   }
 }
 
 cudaError_t launch_select_rerank(const RerankArgs& a, cudaStream_t s) {
-  if (a.D > 1024 || a.NS > 64 || a.R > kMaxR) return cudaErrorInvalidValue;
-  auto kern = a.full_f16 ? k_select_rerank<true> : k_select_rerank<false>;
-  kern<<<a.m, kRrThreads, 0, s>>>(a);
+  const int vec = a.full_f16 ? 8 : 4;
+  const int vpl = (a.D / vec + 31) / 32;
+  if (a.NS > 64 || a.R > kMaxR || a.R > 256 || vpl > 6 || a.D % vec) return cudaErrorInvalidValue;
+  k_select_topr<<<(a.m + kSelW - 1) / kSelW, kSelW * 32, 0, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const dim3 grid((unsigned)((a.m + 3) / 4));
+#define LV_RR(F, V) k_rerank_topk<F, V><<<grid, 128, 0, s>>>(a)
+  if (a.full_f16) {
+    if (vpl <= 1) LV_RR(true, 1); else if (vpl <= 2) LV_RR(true, 2); else if (vpl <= 3) LV_RR(true, 3);
+    else if (vpl <= 4) LV_RR(true, 4); else LV_RR(true, 6);
+  } else {
+    if (vpl <= 1) LV_RR(false, 1); else if (vpl <= 2) LV_RR(false, 2); else if (vpl <= 3) LV_RR(false, 3);
+    else if (vpl <= 4) LV_RR(false, 4); else LV_RR(false, 6);
+  }
+#undef LV_RR
   return cudaGetLastError();
 }
 
@@ -332,37 +447,43 @@ constexpr int kSelWarps = 16;
 __global__ void __launch_bounds__(kSelWarps * 32) k_bmax_select(const float* __restrict__ bmax, int nblk, int m, int m_pad,
                                                                int j1, int j2, uint64_t* tau, int32_t* cnt, int NS,
                                                                uint64_t* tau2) {
-  __shared__ uint32_t h[128 * 32];
-  __shared__ uint32_t s_dig[4];
+  __shared__ uint32_t h[2][128 * 32];   // pass 1: h[0] = top byte; pass 2: h[k] = next byte under d_k
+  __shared__ int s_ab[2][32];
+  __shared__ uint32_t s_d[2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = blockIdx.x * 32 + lane;
   const bool qv = q < m;
-  auto hist_pass = [&](int shift, bool filt, uint32_t pre_lane) {
-    for (int i = threadIdx.x; i < 128 * 32; i += blockDim.x) h[i] = 0u;
+  auto hist_pass = [&](bool second) {
+    for (int i = threadIdx.x; i < 2 * 128 * 32; i += blockDim.x) (&h[0][0])[i] = 0u;
     __syncthreads();
+    const uint32_t d1 = second ? s_d[0][lane] : 0u, d2 = second ? s_d[1][lane] : 0u;
     auto add = [&](float x) {
       const uint32_t o = ord_f32(x);
-      if (!filt || (o >> 24) == pre_lane) {
-        const uint32_t dg = (o >> shift) & 255u;
-        atomicAdd(&h[(dg >> 1) * 32 + lane], (dg & 1u) ? 65536u : 1u);
+      if (!second) {
+        const uint32_t dg = o >> 24;
+        atomicAdd(&h[0][(dg >> 1) * 32 + lane], (dg & 1u) ? 65536u : 1u);
+      } else {
+        const uint32_t dg = (o >> 16) & 255u, inc = (dg & 1u) ? 65536u : 1u;
+        if ((o >> 24) == d1) atomicAdd(&h[0][(dg >> 1) * 32 + lane], inc);
+        if ((o >> 24) == d2) atomicAdd(&h[1][(dg >> 1) * 32 + lane], inc);
       }
     };
     int i = warp;
-    for (; i + 3 * kSelWarps < nblk; i += 4 * kSelWarps) {
-      float x[4];
+    for (; i + 7 * kSelWarps < nblk; i += 8 * kSelWarps) {
+      float x[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = qv ? __ldg(bmax + (size_t)(i + u * kSelWarps) * m_pad + q) : -FLT_MAX;
+      for (int u = 0; u < 8; ++u) x[u] = qv ? __ldg(bmax + (size_t)(i + u * kSelWarps) * m_pad + q) : -FLT_MAX;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) add(x[u]);
+      for (int u = 0; u < 8; ++u) add(x[u]);
     }
     for (; i < nblk; i += kSelWarps) add(qv ? __ldg(bmax + (size_t)i * m_pad + q) : -FLT_MAX);
     __syncthreads();
   };
-  // bin of the want-th largest (scan from the top); *above = count strictly above the bin
-  auto find = [&](int want, int* above) -> uint32_t {
+  // bin of the want-th largest in histogram hk (scan from the top); *above = count above the bin
+  auto find = [&](const uint32_t* hk, int want, int* above) -> uint32_t {
     int cum = 0;
     for (int dg = 255; dg >= 0; --dg) {
-      const uint32_t w = h[(dg >> 1) * 32 + lane];
+      const uint32_t w = hk[(dg >> 1) * 32 + lane];
       const int c = (dg & 1) ? (int)(w >> 16) : (int)(w & 0xffffu);
       if (cum + c >= want) {
         *above = cum;
@@ -373,28 +494,19 @@ __global__ void __launch_bounds__(kSelWarps * 32) k_bmax_select(const float* __r
     *above = cum;
     return 0u;
   };
-  __shared__ int s_ab[2][32];
-  __shared__ uint32_t s_d[2][32];
-  hist_pass(24, false, 0u);
+  hist_pass(false);
   if (warp < 2) {
     int ab = 0;
-    s_d[warp][lane] = find(warp == 0 ? j1 : j2, &ab);
+    s_d[warp][lane] = find(h[0], warp == 0 ? j1 : j2, &ab);
     s_ab[warp][lane] = ab;
   }
   __syncthreads();
-  uint32_t e[2];
-  for (int k = 0; k < 2; ++k) {
-    hist_pass(16, true, s_d[k][lane]);
-    if (warp == 0) {
-      int ab = 0;
-      e[k] = find((k == 0 ? j1 : j2) - s_ab[k][lane], &ab);
-      s_dig[k] = 0;
-    }
-    __syncthreads();
-  }
-  (void)s_dig;
+  hist_pass(true);
   if (warp != 0 || !qv) return;
-  const uint32_t p1 = (s_d[0][lane] << 8) | e[0], p2 = (s_d[1][lane] << 8) | e[1];
+  int ab = 0;
+  const uint32_t e1 = find(h[0], j1 - s_ab[0][lane], &ab);
+  const uint32_t e2 = find(h[1], j2 - s_ab[1][lane], &ab);
+  const uint32_t p1 = (s_d[0][lane] << 8) | e1, p2 = (s_d[1][lane] << 8) | e2;
   const uint64_t t1 = p1 ? ((uint64_t)p1 << 48) - 1ull : 0ull;
   const uint64_t t2 = p2 ? ((uint64_t)p2 << 48) - 1ull : 0ull;
   for (int sl = 0; sl < NS; ++sl) {

@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int* ci = a.chunk_info + kChunkInts * c;
         const int t0 = ci[0], t1 = ci[1], ts_ = ci[3];
         for (int t = t0; t < t1; t += ts_) {
-          tc::mbar_wait(b_empty + stage, phase ^ 1);
+          tc::mbar_wait_sleep(b_empty + stage, phase ^ 1);
           tc::mbar_arrive_expect_tx(b_full + stage, nch * box_bytes);
           for (int k = 0; k < nch; ++k)
             tc::tma_load_2d(sB + (stage * nch + k) * box_bytes, &tmap_xlow, b_full + stage, k * kCH, t * kN);
@@ -283,30 +283,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int i = 0;
+    const bool issuer = tc::elect_one();   // the single lane that issues tcgen05.mma / commit
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
       const int c = u / QT;
       const int* ci = a.chunk_info + kChunkInts * c;
       const int t0 = ci[0], t1 = ci[1], ts_ = ci[3];
-      tc::mbar_wait(a_full + (i & 1), (uint32_t)(i >> 1) & 1u);
+      tc::mbar_wait_sleep(a_full + (i & 1), (uint32_t)(i >> 1) & 1u);
       tc::tc_fence_after();
       const uint32_t at = tmem_base + (uint32_t)(i & 1) * (uint32_t)(d / 2);
       for (int t = t0; t < t1; t += ts_) {
-        tc::mbar_wait(acc_empty + acc, acc_phase ^ 1);
-        tc::mbar_wait(b_full + stage, phase);
+        tc::mbar_wait_sleep(acc_empty + acc, acc_phase ^ 1);
+        tc::mbar_wait_sleep(b_full + stage, phase);
         tc::tc_fence_after();
-        {
-          // whole warp walks the issue loop (warp-uniform operands stay in uniform registers);
-          // elect.sync picks the single issuing lane inside each instruction
+        if (issuer) {
           const uint64_t bd0 = tc::make_sdesc(sB_addr + (uint32_t)stage * nch * box_bytes, kCH * 2);
           const uint32_t dt = tmem_base + acc_col0 + (uint32_t)acc * kN;
 #pragma unroll
           for (int kk = 0; kk < d / 16; ++kk) {
             // K step kk: box kk*16/kCH, byte offset (kk*16 % kCH)*2 inside the swizzled row
             const uint32_t off16 = (((uint32_t)((kk * 16) / kCH) * box_bytes) + (uint32_t)((kk * 16) % kCH) * 2u) >> 4;
-            tc::mma_f16_ts_elect(dt, at + (uint32_t)kk * 8u, bd0 + off16, idesc, kk > 0 ? 1u : 0u);
+            tc::mma_f16_ts(dt, at + (uint32_t)kk * 8u, bd0 + off16, idesc, kk > 0 ? 1u : 0u);
           }
-          tc::mma_commit_elect(b_empty + stage);
-          tc::mma_commit_elect(acc_full + acc);
+          tc::mma_commit(b_empty + stage);
+          tc::mma_commit(acc_full + acc);
         }
         __syncwarp();
         if (++stage == a.stages) { stage = 0; phase ^= 1; }
@@ -410,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tv_last = a.tile_valid[t_last] - cq * 32;   // valid columns of the chunk's last tile
 
       for (int t = t0; t < t1; t += tstride) {
-        tc::mbar_wait(acc_full + acc, acc_phase);
+        tc::mbar_wait_sleep(acc_full + acc, acc_phase);
         tc::tc_fence_after();
         float v[32];
         tc::tmem_ld_32x32b_x32(tmem_base + lane_base + acc_col0 + (uint32_t)acc * kN + (uint32_t)cq * 32u, v);

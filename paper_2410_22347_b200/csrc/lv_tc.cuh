@@ -52,6 +52,37 @@ LV_TC_INL void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Blocking-style wait: try_wait with a suspend-time hint, so a waiting warp sleeps until the phase
+// completes (NANOSLEEP.SYNCS) instead of spinning on issue slots shared with the MMA/TMA warps.
+LV_TC_INL bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+LV_TC_INL void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+#ifndef LV_NO_HANG_TRAP
+  long long spins = 0;
+  while (!mbar_try_wait_sleep(bar, parity)) {
+    if (++spins > (1ll << 26)) __trap();
+  }
+#else
+  while (!mbar_try_wait_sleep(bar, parity)) {
+  }
+#endif
+}
+// One lane of the warp (elect.sync); the other lanes get false.
+LV_TC_INL bool elect_one() {
+  uint32_t e;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 rl;\n\telect.sync rl|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(e));
+  return e != 0;
+}
+
 // ------------------------------------------------------------------ TMA
 LV_TC_INL void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
