@@ -56,10 +56,14 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "10"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:   # sampler running before the timed region
+                time.sleep(0.01)
+            self.skip = len(self.lines)
         except Exception:
             self.proc = None
         return self
@@ -79,7 +83,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[getattr(self, "skip", 0):]:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
@@ -96,7 +100,7 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_index(cfg, dev_rank=0, log=print):
+def build_index(cfg, rank=0, world=1, log=print):
     """Generate the config's data, fit with the product path (lv_fit_stats + host eig, GPU k-means
     for GleanVec), encode.  Returns dict with index, device Q, host Q, data."""
     import torch
@@ -104,7 +108,8 @@ def build_index(cfg, dev_rank=0, log=print):
     from paper_2410_22347_b200 import fit, lv
     t0 = time.time()
     X = lvgen.database(cfg)
-    Q = lvgen.queries(cfg, "test")
+    lo, hi = shard_queries(cfg.m_test, rank, world)
+    Q = lvgen.queries(cfg, "test", m=hi)[lo:hi]
     Ql = lvgen.queries(cfg, "learn")
     lr = lvgen.learn_rows(cfg)
     log(f"[bench] generated n={cfg.n} D={cfg.D} in {time.time() - t0:.1f}s")
@@ -136,33 +141,65 @@ def build_index(cfg, dev_rank=0, log=print):
             "fit_s": t_fit, "encode_ms": t_enc, "gaps": f.get("gaps")}
 
 
-def roofline_scan(cfg, ms):
+def roofline_scan(cfg, ms, m):
+    """Dominant kernel: the main k_score_topr launch (every database row x every query, 2 d flop
+    per score).  ms = its average launch time over the timed region (CUDA events)."""
     pk = _peaks()
-    flops = 2.0 * cfg.m_test * cfg.n * cfg.d
+    flops = 2.0 * m * cfg.n * cfg.d
     ach = flops / (ms * 1e-3) / 1e12
     return {"bound": "tensor", "achieved": round(ach, 1), "peak": pk["bf16"], "unit": "TFLOP/s",
             "frac": round(ach / pk["bf16"], 4), "frac_of_sustained": round(ach / pk["bf16_sus"], 4) if pk["bf16_sus"] else None,
-            "peak_source": pk["src"], "kernel": "k_score_topr (K2/K3 fused scan)",
-            "algorithmic": f"2*m*n*d = {flops:.3e} flop per launch", "traffic": _ncu_traffic()}
+            "peak_source": pk["src"] + ", bf16 dense burst (sustained alongside)",
+            "kernel": "k_score_topr main stage (K2/K3 fused scoring + top-R)", "launch_ms": round(ms, 4),
+            "algorithmic": f"2*m*n*d = {flops:.3e} flop per launch", "traffic": _ncu_traffic(cfg.cfg_id)}
 
 
-def roofline_rerank(cfg, ms):
+def roofline_rerank(cfg, ms, m):
+    """K5 re-rank: every candidate's full row once (plus q, candidate ids, results).  Candidate rows
+    shared by several queries are partly served from L2, so frac can exceed 1; `traffic` is the
+    DRAM bytes ncu measured for one launch (profiles/ncu_traffic.json)."""
     pk = _peaks()
     b = 4 if cfg.full_dtype == "fp32" else 2
-    byts = cfg.m_test * cfg.R * cfg.D * b + cfg.m_test * cfg.D * 4 + cfg.m_test * cfg.R * 8 + cfg.m_test * cfg.k * 8
+    byts = m * cfg.R * cfg.D * b + m * cfg.D * 4 + m * cfg.R * 4 + m * cfg.k * 8
     ach = byts / (ms * 1e-3) / 1e9
+    traffic = None
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        traffic = json.load(open(p)).get(f"cfg{cfg.cfg_id}", {}).get("rerank_K5_dram_bytes_per_launch")
     return {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s", "frac": round(ach / pk["hbm"], 4),
-            "algorithmic": f"{byts:.3e} B per launch"}
+            "kernel": "k_rerank_topk (K5 gather + fp32 dot + top-k)", "launch_ms": round(ms, 4),
+            "algorithmic": f"{byts:.3e} B per launch", "traffic": traffic,
+            "dram_frac": round(traffic / (ms * 1e-3) / 1e9 / pk["hbm"], 4) if traffic else None}
 
 
-def _ncu_traffic():
+def _ncu_traffic(cfg_id):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the main scan launch, from the committed
+    ncu capture summary (profiles/ncu_traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("k_score_topr_bytes_per_launch")
+            return json.load(open(p)).get(f"cfg{cfg_id}", {}).get("main_scan_dram_bytes_per_launch")
         except Exception:
             return None
     return None
+
+
+def shard_queries(m, rank, world):
+    """Query rows [rank * m, (rank + 1) * m) of the config's test stream: each rank searches its own
+    batch of the same size (weak scaling, no data-path collective)."""
+    return rank * m, (rank + 1) * m
+
+
+def reduce_max_ms(ms, world):
+    """Max over ranks of a per-rank device time (the slowest rank defines the job time)."""
+    if world <= 1:
+        return ms
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def cpu_baseline(cfg, data, nq, log=print):
@@ -260,7 +297,7 @@ def main():
         dist.init_process_group("nccl")
     from paper_2410_22347_b200 import lv
 
-    data = build_index(cfg, log=log)
+    data = build_index(cfg, rank=rank, world=world, log=log)
     ix, Qd = data["ix"], data["Qd"]
     m = Qd.shape[0]
     ids = torch.empty((m, cfg.k), dtype=torch.int32, device="cuda")
@@ -274,6 +311,7 @@ def main():
         lv.lv_search(ix, Qd, cfg.k, cfg.R, out=(ids, sc))
     torch.cuda.synchronize()
     launches_per_step = lv.lv_search(ix, Qd, cfg.k, cfg.R, out=(ids, sc))[2]["launches"]
+    lv.lv_timing_collect(ix)   # drop anything recorded before the timed region
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -281,22 +319,14 @@ def main():
         torch.cuda.synchronize()
         e0.record(st)
         for _ in range(args.steps):
-            lv.lv_search(ix, Qd, cfg.k, cfg.R, out=(ids, sc))
+            # timing=2: per-kernel CUDA events on the launch stream, no synchronisation
+            lv.lv_search(ix, Qd, cfg.k, cfg.R, out=(ids, sc), timing=2)
         e1.record(st)
         torch.cuda.synchronize()
         barrier()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = reduce_max_ms(e0.elapsed_time(e1), world)
     value = world * m * args.steps / (ms * 1e-3)
-
-    # per-phase device times (separate, synchronising runs; CUDA events on the launch stream)
-    ph = []
-    for _ in range(max(3, min(args.steps, 10))):
-        ph.append(lv.lv_search(ix, Qd, cfg.k, cfg.R, out=(ids, sc), timing=True)[2]["phase_ms"])
-    ph = np.median(np.array(ph), axis=0)
+    kms, ncalls = lv.lv_timing_collect(ix)   # per-kernel averages over the timed region
 
     # e2e: public API with HOST buffers (pinned), H2D of Q and D2H of results inside the region
     Qh = torch.from_numpy(data["Q"]).pin_memory()
@@ -311,12 +341,8 @@ def main():
         lv.lv_search_host(ix, Qh, cfg.k, cfg.R, ih, sh)
     e1.record(st)
     torch.cuda.synchronize()
-    ms_e2e = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms_e2e], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_e2e = float(t.item())
-        barrier()
+    ms_e2e = reduce_max_ms(e0.elapsed_time(e1), world)
+    barrier()
     if rank != 0:
         torch.distributed.destroy_process_group()
         return
@@ -325,10 +351,13 @@ def main():
            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": cfg.low_dtype, "data": "synthetic",
            "config": dict(conf, parallelism=f"query-sharded replicas x{world}" if world > 1 else "single GPU"),
-           "phases_ms": {"project_K1": round(float(ph[0]), 4), "scan_K2K3": round(float(ph[1]), 4),
-                         "select_rerank_K4K5": round(float(ph[2]), 4), "total": round(float(ph[3]), 4)},
-           "roofline": roofline_scan(cfg, float(ph[1])),
-           "roofline_rerank": roofline_rerank(cfg, float(ph[2])),
+           "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
+           "kernel_ms_source": f"CUDA events on the launch stream, average over the {ncalls} timed steps",
+           "roofline": roofline_scan(cfg, kms["main_scan"], m),
+           "roofline_rerank": roofline_rerank(cfg, kms["rerank_K5"], m),
+           "scan_phase": {"ms": round(kms["sample_stage"] + kms["threshold_select"] + kms["main_scan"], 4),
+                          "frac_of_bf16_peak": round(2.0 * m * cfg.n * cfg.d / ((kms["sample_stage"] + kms["threshold_select"] + kms["main_scan"]) * 1e-3) / 1e12 / _peaks()["bf16"], 4),
+                          "note": "sample stage + threshold select + main scan (the whole K2/K3 phase)"},
            "e2e": {"value": round(world * m * args.steps / (ms_e2e * 1e-3), 1), "unit": "queries/s",
                    "h2d_bytes_per_step": int(m * cfg.D * 4), "d2h_bytes_per_step": int(m * cfg.k * 8)},
            "gpu_launches": int(launches_per_step * args.steps),

@@ -58,16 +58,29 @@ typedef struct {
     float*   cand_scores;  /* device [m, R] or NULL: their reduced scores <q'_{c_i}, x_low_i>  */
     float*   raw_scores;   /* device [m_pad, n_pad] or NULL: EVERY reduced score, in sorted
                               (padded) database order; tiny shapes only (kernel self-test)   */
-    int32_t  timing;       /* nonzero: fill phase_ms (synchronises the stream)               */
-    float    phase_ms[4];  /* [0] project (K1), [1] score+top-R (K2/K3), [2] select+re-rank
-                              (K4/K5), [3] whole call                                       */
+    int32_t  timing;       /* 1: fill phase_ms and kernel_ms (synchronises the stream);
+                              2: record per-kernel CUDA events without synchronising, to be read
+                              by lv_timing_collect (averages over many calls)                 */
+    float    phase_ms[4];  /* timing 1: [0] project (K1), [1] score+top-R (K2/K3 incl. sample
+                              stage and threshold select), [2] select+re-rank (K4/K5 + repairs),
+                              [3] whole call                                                */
     int32_t  launches;     /* number of kernels this call launched                          */
     int32_t  slots;        /* per-query candidate lists kept by the scan       */
     int32_t  units;        /* (query pair, database chunk) work units of the scan            */
     int32_t  grid;         /* CTAs of the scan                                               */
     int32_t  path;         /* 0: staged thresholds, 1: sampled threshold + repair */
     int32_t  failed[2];    /* sampled path, with timing: queries repaired in rounds 1 and 2     */
+    float    kernel_ms[8]; /* timing 1: [0] K1 projection, [1] sample stage, [2] threshold
+                              select, [3] main scan (staged path: all stages and merges),
+                              [4] K4 top-R select, [5] K5 re-rank + top-k, [6] repairs, [7] total */
 } lv_search_debug;
+
+/*
+ * lv_timing_collect — averages of kernel_ms over the lv_search calls made with timing = 2 since
+ * the last collect (synchronises on their events).  kernel_ms HOST float[8] out (see
+ * lv_search_debug); *calls = number of calls averaged (0: nothing recorded).
+ */
+lv_status lv_timing_collect(lv_index* index, float* kernel_ms, int32_t* calls);
 
 /* Human-readable message for the last non-OK status on this thread. */
 const char* lv_last_error(void);

@@ -71,6 +71,9 @@ struct lv_index {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   PlanCache plan;               // last search shape: plan + device chunk tables (uploaded once)
+  // per-kernel timing (lv_search timing = 2): event groups of 8 marks, pending until collected
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::vector<cudaEvent_t>> ev_pending;
   // host-buffer staging for lv_search_host
   void* hs = nullptr;
   size_t hs_bytes = 0;
@@ -684,12 +687,26 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   void* Qp = pc.Qp;
   const std::vector<int32_t*>& chunk_info = pc.chunk_info;
 
-  cudaEvent_t ev[4];
-  const bool timing = dbg && dbg->timing;
+  // phase marks: 0 start, 1 after K1, 2 after the sample stage, 3 after the threshold select,
+  // 4 after the main scan, 5 after K4, 6 after K5, 7 end (after the repairs)
+  const int timing = dbg ? dbg->timing : 0;
+  std::vector<cudaEvent_t> ev;
   if (timing) {
-    for (int i = 0; i < 4; ++i) LV_CUDA(cudaEventCreate(&ev[i]));
-    LV_CUDA(cudaEventRecord(ev[0], s));
+    for (int i = 0; i < 8; ++i) {
+      if (ix->ev_pool.empty()) {
+        cudaEvent_t e;
+        LV_CUDA(cudaEventCreate(&e));
+        ix->ev_pool.push_back(e);
+      }
+      ev.push_back(ix->ev_pool.back());
+      ix->ev_pool.pop_back();
+    }
   }
+  auto mark = [&](int i) -> lv_status {
+    if (timing) LV_CUDA(cudaEventRecord(ev[i], s));
+    return LV_OK;
+  };
+  if ((st = mark(0))) return st;
   int launches = 0;
   LV_CUDA(cudaMemsetAsync(pc.zero_lo, 0, pc.zero_hi - pc.zero_lo, s));
   // K1 projection (rows >= m are zero)
@@ -702,7 +719,7 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
                                  pl.m_pad, s));
     ++launches;
   }
-  if (timing) LV_CUDA(cudaEventRecord(ev[1], s));
+  if ((st = mark(1))) return st;
   lv::ScoreArgs sa;
   sa.Qp = Qp;
   sa.C = ix->C;
@@ -782,6 +799,7 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   ra.sel_n = pc.sel_n;
   if (!pl.sampled) {
     // staged path: geometric stages with exact threshold merges in between
+    if ((st = mark(2)) || (st = mark(3))) return st;
     for (size_t k = 0; k < pl.chunks.size(); ++k) {
       char nm[32];
       snprintf(nm, sizeof nm, "stage %zu", k);
@@ -792,9 +810,12 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
         ++launches;
       }
     }
-    if (timing) LV_CUDA(cudaEventRecord(ev[2], s));
-    LV_CUDA(lv::launch_select_rerank(ra, s));
-    ++launches;
+    if ((st = mark(4))) return st;
+    LV_CUDA(lv::launch_select_topr(ra, s));
+    if ((st = mark(5))) return st;
+    LV_CUDA(lv::launch_rerank_topk(ra, s));
+    if ((st = mark(6))) return st;
+    launches += 2;
   } else {
     // sampled path: (1) sample stage -> block maxima; (2) per-query threshold with >= j1 rows
     // above it; (3) one main stage with that threshold; (4) exactness check in the re-rank;
@@ -803,16 +824,21 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     st = scan(chunk_info[0], pl.chunks[0], pl.QP, "sample");
     if (st) return st;
     sa.bmax = nullptr;
+    if ((st = mark(2))) return st;
     LV_CUDA(lv::launch_bmax_select(pc.bmax, pl.nblk, (int)m, pl.m_pad, pl.j1, pl.j2, pc.tau, pc.cnt, NS2, pc.tau2, s));
     ++launches;
+    if ((st = mark(3))) return st;
     st = scan(chunk_info[1], pl.chunks[1], pl.QP, "main");
     if (st) return st;
-    if (timing) LV_CUDA(cudaEventRecord(ev[2], s));
+    if ((st = mark(4))) return st;
     ra.checked = 1;
     ra.fail_count = pc.fail + 0;
     ra.fail_list = pc.fail_list;
-    LV_CUDA(lv::launch_select_rerank(ra, s));
-    ++launches;
+    LV_CUDA(lv::launch_select_topr(ra, s));
+    if ((st = mark(5))) return st;
+    LV_CUDA(lv::launch_rerank_topk(ra, s));
+    if ((st = mark(6))) return st;
+    launches += 2;
     for (int round = 0; round < 2; ++round) {
       int32_t* flist = pc.fail_list + (size_t)round * pl.m_pad;
       int32_t* fcount = pc.fail + round;
@@ -828,8 +854,9 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
       ra.checked = round == 0 ? 1 : 0;
       ra.fail_count = pc.fail + 1;
       ra.fail_list = pc.fail_list + pl.m_pad;
-      LV_CUDA(lv::launch_select_rerank(ra, s));
-      launches += 2;
+      LV_CUDA(lv::launch_select_topr(ra, s));
+      LV_CUDA(lv::launch_rerank_topk(ra, s));
+      launches += 3;
     }
     sa.Qp = Qp;
     sa.m_dev = nullptr;
@@ -841,19 +868,20 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
               pl.j2, hf[0], hf[1]);
     }
   }
-  if (timing) {
-    LV_CUDA(cudaEventRecord(ev[3], s));
-    LV_CUDA(cudaEventSynchronize(ev[3]));
-    float t01, t12, t23, t03;
-    cudaEventElapsedTime(&t01, ev[0], ev[1]);
-    cudaEventElapsedTime(&t12, ev[1], ev[2]);
-    cudaEventElapsedTime(&t23, ev[2], ev[3]);
-    cudaEventElapsedTime(&t03, ev[0], ev[3]);
-    dbg->phase_ms[0] = t01;
-    dbg->phase_ms[1] = t12;
-    dbg->phase_ms[2] = t23;
-    dbg->phase_ms[3] = t03;
-    for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
+  if ((st = mark(7))) return st;
+  if (timing == 1) {
+    LV_CUDA(cudaEventSynchronize(ev[7]));
+    float t[7];
+    for (int i = 0; i < 7; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+    for (int i = 0; i < 7; ++i) dbg->kernel_ms[i] = t[i];
+    cudaEventElapsedTime(&dbg->kernel_ms[7], ev[0], ev[7]);
+    dbg->phase_ms[0] = t[0];
+    dbg->phase_ms[1] = t[1] + t[2] + t[3];
+    dbg->phase_ms[2] = t[4] + t[5] + t[6];
+    dbg->phase_ms[3] = dbg->kernel_ms[7];
+    for (auto e : ev) ix->ev_pool.push_back(e);
+  } else if (timing == 2) {
+    ix->ev_pending.push_back(ev);
   }
   if (dbg) {
     dbg->path = pl.sampled ? 1 : 0;
@@ -870,6 +898,27 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     dbg->units = pl.total_units;
     dbg->grid = pl.grid;
   }
+  return LV_OK;
+}
+
+lv_status lv_timing_collect(lv_index* ix, float* kernel_ms, int32_t* calls) {
+  if (!ix || !kernel_ms) return fail(LV_EINVAL, "lv_timing_collect: bad arguments");
+  double acc[8] = {0};
+  const int n = (int)ix->ev_pending.size();
+  for (auto& g : ix->ev_pending) {
+    LV_CUDA(cudaEventSynchronize(g[7]));
+    float t;
+    for (int i = 0; i < 7; ++i) {
+      cudaEventElapsedTime(&t, g[i], g[i + 1]);
+      acc[i] += t;
+    }
+    cudaEventElapsedTime(&t, g[0], g[7]);
+    acc[7] += t;
+    for (auto e : g) ix->ev_pool.push_back(e);
+  }
+  ix->ev_pending.clear();
+  for (int i = 0; i < 8; ++i) kernel_ms[i] = n ? (float)(acc[i] / n) : 0.f;
+  if (calls) *calls = n;
   return LV_OK;
 }
 
@@ -938,6 +987,9 @@ void lv_index_destroy(lv_index* ix) {
   cudaFree(ix->A);
   cudaFree(ix->B);
   cudaFree(ix->A_planes);
+  for (auto& g : ix->ev_pending)
+    for (auto e : g) cudaEventDestroy(e);
+  for (auto e : ix->ev_pool) cudaEventDestroy(e);
   cudaFree(ix->ws);
   cudaFree(ix->hs);
   delete ix;

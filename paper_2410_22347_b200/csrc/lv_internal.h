@@ -73,7 +73,8 @@ cudaError_t launch_bmax_select(const float* bmax, int nblk, int m, int m_pad, in
 cudaError_t launch_repair_setup(const void* Qp, int Cd, const int32_t* fail_list, const int32_t* fail_count, void* Qr,
                                 const uint64_t* tau_src, uint64_t* tau, int32_t* cnt, int NS, int m_pad, int m_max,
                                 int32_t* m_out, cudaStream_t s);
-cudaError_t launch_select_rerank(const RerankArgs& a, cudaStream_t s);
+cudaError_t launch_select_topr(const RerankArgs& a, cudaStream_t s);   // K4
+cudaError_t launch_rerank_topk(const RerankArgs& a, cudaStream_t s);   // K5
 cudaError_t launch_tau_merge(uint64_t* cand, int32_t* cnt, uint64_t* tau, int NS, int m, int m_pad, int Cap, int R,
                              cudaStream_t s);
 

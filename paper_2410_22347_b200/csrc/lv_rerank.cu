@@ -414,13 +414,16 @@ __global__ void __launch_bounds__(128) k_rerank_topk(const RerankArgs a) {
   }
 }
 
-cudaError_t launch_select_rerank(const RerankArgs& a, cudaStream_t s) {
+cudaError_t launch_select_topr(const RerankArgs& a, cudaStream_t s) {
+  if (a.NS > 64 || a.R > kMaxR || a.R > 256) return cudaErrorInvalidValue;
+  k_select_topr<<<(a.m + kSelW - 1) / kSelW, kSelW * 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rerank_topk(const RerankArgs& a, cudaStream_t s) {
   const int vec = a.full_f16 ? 8 : 4;
   const int vpl = (a.D / vec + 31) / 32;
-  if (a.NS > 64 || a.R > kMaxR || a.R > 256 || vpl > 6 || a.D % vec) return cudaErrorInvalidValue;
-  k_select_topr<<<(a.m + kSelW - 1) / kSelW, kSelW * 32, 0, s>>>(a);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (a.R > 256 || vpl > 6 || a.D % vec) return cudaErrorInvalidValue;
   const dim3 grid((unsigned)((a.m + 3) / 4));
 #define LV_RR(F, V) k_rerank_topk<F, V><<<grid, 128, 0, s>>>(a)
   if (a.full_f16) {

@@ -20,8 +20,8 @@ _DT = {"fp32": LV_F32, "f32": LV_F32, "fp16": LV_F16, "f16": LV_F16, "bf16": LV_
 _TORCH_DT = {LV_F32: torch.float32, LV_F16: torch.float16, LV_BF16: torch.bfloat16}
 
 EXPORTS = ["lv_last_error", "lv_version", "lv_fit_stats", "lv_index_create", "lv_encode_database",
-           "lv_project_queries", "lv_search", "lv_search_host", "lv_assign_tags", "lv_index_info",
-           "lv_index_export", "lv_index_destroy"]
+           "lv_project_queries", "lv_search", "lv_search_host", "lv_timing_collect", "lv_assign_tags",
+           "lv_index_info", "lv_index_export", "lv_index_destroy"]
 
 
 class LVError(RuntimeError):
@@ -32,7 +32,10 @@ class SearchDebug(ctypes.Structure):
     _fields_ = [("cand_ids", ctypes.c_void_p), ("cand_scores", ctypes.c_void_p), ("raw_scores", ctypes.c_void_p),
                 ("timing", ctypes.c_int32), ("phase_ms", ctypes.c_float * 4), ("launches", ctypes.c_int32),
                 ("slots", ctypes.c_int32), ("units", ctypes.c_int32), ("grid", ctypes.c_int32),
-                ("path", ctypes.c_int32), ("failed", ctypes.c_int32 * 2)]
+                ("path", ctypes.c_int32), ("failed", ctypes.c_int32 * 2), ("kernel_ms", ctypes.c_float * 8)]
+
+KERNEL_PHASES = ["project_K1", "sample_stage", "threshold_select", "main_scan", "select_K4", "rerank_K5",
+                 "repairs", "total"]
 
 
 _lib = None
@@ -55,6 +58,7 @@ def lib():
             "lv_project_queries": [vp, vp, i64, vp, vp],
             "lv_search": [vp, vp, i64, i32, i32, vp, vp, ctypes.POINTER(SearchDebug), vp],
             "lv_search_host": [vp, vp, i64, i32, i32, vp, vp, vp],
+            "lv_timing_collect": [vp, vp, ctypes.POINTER(i32)],
             "lv_assign_tags": [vp, i32, i64, i32, vp, i32, vp, vp],
             "lv_index_info": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32),
                               ctypes.POINTER(i32), ctypes.POINTER(i32)],
@@ -165,7 +169,7 @@ def lv_project_queries(index: Index, Q: torch.Tensor) -> torch.Tensor:
 
 
 def lv_search(index: Index, Q: torch.Tensor, k: int, R: int, cand: bool = False, raw: bool = False,
-              timing: bool = False, out=None):
+              timing: int = 0, out=None):
     """Alg. 1 hot path.  Returns (ids int32 [m,k], scores fp32 [m,k], debug dict)."""
     Q = _dev(Q, torch.float32)
     m = Q.shape[0]
@@ -186,12 +190,21 @@ def lv_search(index: Index, Q: torch.Tensor, k: int, R: int, cand: bool = False,
         m_pad = (m + 255) // 256 * 256
         keep["raw"] = torch.full((m_pad, info["n_pad"]), float("nan"), dtype=torch.float32, device=Q.device)
         dbg.raw_scores = keep["raw"].data_ptr()
-    dbg.timing = 1 if timing else 0
+    dbg.timing = int(timing)   # 0 none, 1 synchronous (phase_ms / kernel_ms), 2 deferred (lv_timing_collect)
     _check(lib().lv_search(index.h, _ptr(Q), m, k, R, _ptr(ids), _ptr(sc), ctypes.byref(dbg), _stream()),
            "lv_search")
     keep.update({"phase_ms": list(dbg.phase_ms), "launches": dbg.launches, "slots": dbg.slots,
-                 "units": dbg.units, "grid": dbg.grid, "path": dbg.path, "failed": list(dbg.failed)})
+                 "units": dbg.units, "grid": dbg.grid, "path": dbg.path, "failed": list(dbg.failed),
+                 "kernel_ms": dict(zip(KERNEL_PHASES, list(dbg.kernel_ms)))})
     return ids, sc, keep
+
+
+def lv_timing_collect(index: Index):
+    """Average per-kernel times (ms) of the lv_search calls made with timing=2 since the last collect."""
+    ms = (ctypes.c_float * 8)()
+    calls = ctypes.c_int32()
+    _check(lib().lv_timing_collect(index.h, ms, ctypes.byref(calls)), "lv_timing_collect")
+    return dict(zip(KERNEL_PHASES, list(ms))), calls.value
 
 
 def lv_search_host(index: Index, Q_host: torch.Tensor, k: int, R: int, ids_host=None, scores_host=None):
