@@ -210,7 +210,9 @@ def cpu_baseline(cfg, data, nq, log=print):
     assign = None if data["assign"] is None else data["assign"].cpu().numpy()
     X = data["X"]
     t0 = time.time()
-    X_low = O.encode(X, B, assign, store=cfg.low_dtype)
+    ch = 1 << 19   # chunked so a 10M x 768 database is never converted to fp64 at once
+    X_low = np.concatenate([O.encode(X[lo:lo + ch], B, None if assign is None else assign[lo:lo + ch],
+                                     store=cfg.low_dtype) for lo in range(0, X.shape[0], ch)])
     t_enc = time.time() - t0
     Qs = data["Q"][:nq]
     t0 = time.time()
@@ -262,8 +264,10 @@ def main():
         else:
             g = O.gleanvec_fit(Ql, Xl, cfg.C, cfg.d, lvgen.kmeanspp_draws(cfg))
             A, B = g["A"], g["B"]
-            assign = O.assign_tags(X, g["centres"])
-        X_low = O.encode(X, B, assign, store=cfg.low_dtype)
+            assign = np.concatenate([O.assign_tags(X[lo:lo + (1 << 19)], g["centres"])
+                                     for lo in range(0, X.shape[0], 1 << 19)])
+        X_low = np.concatenate([O.encode(X[lo:lo + (1 << 19)], B, None if assign is None else assign[lo:lo + (1 << 19)],
+                                         store=cfg.low_dtype) for lo in range(0, X.shape[0], 1 << 19)])
         per = max(1, args.oracle_queries // 4)
         def step(i):
             lo = (i * per) % cfg.m_test

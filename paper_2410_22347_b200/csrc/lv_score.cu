@@ -37,6 +37,7 @@ struct EpiShared {
   float rows[kEpiWarps][32][32];       // hitting lanes' 32 scores (row = lane), read column-wise
   int hist[kEpiWarps][256];            // radix scratch of the compaction
   int slot;                            // candidate slot of the current unit
+  int jc[4];                           // per TMEM lane quarter: next (tile, column-quarter) job
   int pad_[3];
 };
 
@@ -202,7 +203,9 @@ __device__ __forceinline__ int warp_compact_fast(uint64_t* buf, int count, int R
   return kept;
 }
 
-template <bool kBF16, int kD>
+// kSample: the sample stage (block maxima only, no candidate lists; a.bmax != nullptr) is a
+// separate instantiation so the main stage's per-tile loop carries no mode checks.
+template <bool kBF16, int kD, bool kSample>
 __global__ void __launch_bounds__(kThreads, 1)
     k_score_topr(const __grid_constant__ CUtensorMap tmap_xlow, const ScoreArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -246,6 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc::mbar_init(a_full + 0, kEpiWarps);
     tc::mbar_init(a_full + 1, kEpiWarps);
+    for (int j = 0; j < 4; ++j) S.jc[j] = 0;
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmap_xlow);
   }
@@ -255,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr;
   const uint32_t acc_col0 = (uint32_t)d;          // A buffers occupy columns [0, d)
+  const uint32_t acc_full_u = tc::smem_u32(acc_full), acc_empty_u = tc::smem_u32(acc_empty);
 
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer (X_low tiles)
@@ -314,9 +319,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue: 16 warps
-    // warp -> (TMEM lane quarter, 32-column quarter of every tile); thread = one query x one
-    // column quarter, with its own candidate sub-list (4 per slot and query).
-    const int cq = warp >> 2;        // column quarter of each 128-column tile
+    // The four warps of a TMEM lane quarter take (tile, 32-column quarter) jobs from a shared
+    // counter in order, so a warp busy on the hit path does not hold back its column quarter;
+    // thread = one query of the quarter, with its own candidate sub-list (4 per slot and query).
+    // write_A keeps the static split: warp group cq writes K range cq of the A operand.
+    const int cq = warp >> 2;        // warp group in the lane quarter (A split, sub-list index)
     const int quarter = warp & 3;    // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
@@ -366,8 +373,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) tc::mbar_arrive(a_full + b);
     };
     if ((int)blockIdx.x < nunits) write_A(blockIdx.x, 0);
-    int acc = 0;
-    uint32_t acc_phase = 0;
+    const uint32_t tm_lane = tmem_base + lane_base + acc_col0;
+    int tiles_before = 0;   // tiles of this CTA's earlier units (global tile ordinal base)
+    int pending = -1;       // a job index already taken that belongs to a later unit
     int i = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
       if (u + (int)gridDim.x < nunits) write_A(u + gridDim.x, (i + 1) & 1);
@@ -379,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool qvalid = q < m_eff;
       // ---- unit start: claim a free candidate slot of query tile qt (units of one tile that run
       // concurrently on different CTAs use different slots; a slot's lists carry over)
-      const bool lists = a.bmax == nullptr;   // the sample stage keeps no candidate lists
+      constexpr bool lists = !kSample;   // the sample stage keeps no candidate lists
       if (lists && threadIdx.x == 0) {
         int32_t* busy = a.slot_busy + qt;
         long long spins = 0;
@@ -406,24 +414,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint64_t tk = lists ? a.tau[si] : 0ull;
       float ts = qvalid ? thr_score(tk) : FLT_MAX;   // padded queries never hit
       uint64_t* const bp = a.cand + si * (size_t)a.Cap;
-      const int tv_last = a.tile_valid[t_last] - cq * 32;   // valid columns of the chunk's last tile
+      const int n_t = (t1 - t0 + tstride - 1) / tstride;   // tiles of this unit
+      const int jend = (tiles_before + n_t) * 4;           // job index bound of this unit
 
-      for (int t = t0; t < t1; t += tstride) {
-        tc::mbar_wait_sleep(acc_full + acc, acc_phase);
+      for (;;) {
+        int J = pending;
+        if (J < 0) {
+          if (lane == 0) J = atomicAdd(&S.jc[quarter], 1);
+          J = __shfl_sync(0xffffffffu, J, 0);
+        }
+        if (J >= jend) {   // first job of a later unit: keep it for then
+          pending = J;
+          break;
+        }
+        pending = -1;
+        const int g = J >> 2, jq = J & 3;                  // global tile ordinal, column quarter
+        const int t = t0 + (g - tiles_before) * tstride;
+        const int accb = g % nacc;
+        tc::mbar_wait_sleep_u32(acc_full_u + 8u * (uint32_t)accb, (uint32_t)(g / nacc) & 1u);
         tc::tc_fence_after();
         float v[32];
-        tc::tmem_ld_32x32b_x32(tmem_base + lane_base + acc_col0 + (uint32_t)acc * kN + (uint32_t)cq * 32u, v);
+        tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kN + (uint32_t)jq * 32u, v);
         tc::tmem_wait_ld();
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(acc_empty + acc);
-        if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
+        if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
         if (skip_topr) continue;
-        const int base_pos = t * kN + cq * 32;
-        if (t == t_last && tv_last < 32) {
+        const int base_pos = t * kN + jq * 32;
+        if (t == t_last) {   // a cluster segment's last tile may be partial
+          const int tv = a.tile_valid[t_last] - jq * 32;
+          if (tv < 32) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j >= tv_last) v[j] = -FLT_MAX;
+            for (int j = 0; j < 32; ++j)
+              if (j >= tv) v[j] = -FLT_MAX;
+          }
         }
         if (a.raw != nullptr) {
 #pragma unroll
@@ -432,9 +456,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         float mx = v[0];
 #pragma unroll
         for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
-        if (a.bmax != nullptr) {
+        if (kSample) {
           // sample stage: record the block maximum (query q, 32 database rows); no top-R here
-          a.bmax[(size_t)((sbase + (t - t0) / tstride) * 4 + cq) * a.m_pad + q] = mx;
+          a.bmax[(size_t)((sbase + (t - t0) / tstride) * 4 + jq) * a.m_pad + q] = mx;
           continue;
         }
         const bool hit = mx >= ts && mx > -FLT_MAX;
@@ -484,15 +508,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         } while (hb != 0u);
         __syncwarp();
       }
+      tiles_before += n_t;
+      // unit end: every job of this unit has seen its tile committed, so the MMA is done with
+      // this unit's A buffer before any warp overwrites it (write_A of unit u + 2 at the next
+      // iteration); in the main stage the sub-list states go back to the slot, which is released
       if (lists) {
         if (qvalid) {
           a.cnt[si] = cnt;
           a.tau[si] = tk;
         }
         __threadfence();
-        tc::named_bar_sync(1, kEpiThreads);
-        if (threadIdx.x == 0) atomicAnd(a.slot_busy + qt, ~(1 << my_slot));   // release the slot
       }
+      tc::named_bar_sync(1, kEpiThreads);
+      if (lists && threadIdx.x == 0) atomicAnd(a.slot_busy + qt, ~(1 << my_slot));   // release the slot
     }
   }
   tc::tc_fence_before();
@@ -502,31 +530,33 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 size_t score_smem_bytes(int d, int stages) { return score_smem_layout(d, stages).total + 1024; }
 
-template <bool B, int D>
+template <bool B, int D, bool S>
 static cudaError_t launch_t(const CUtensorMap* tx, const ScoreArgs& a, int grid, size_t smem, cudaStream_t s) {
-  auto kern = k_score_topr<B, D>;
+  auto kern = k_score_topr<B, D, S>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, kThreads, smem, s>>>(*tx, a);
   return cudaGetLastError();
 }
 
-template <bool B>
+template <bool B, bool S>
 static cudaError_t launch_d(const CUtensorMap* tx, const ScoreArgs& a, int grid, size_t smem, cudaStream_t s) {
   switch (a.d) {
-    case 32: return launch_t<B, 32>(tx, a, grid, smem, s);
-    case 64: return launch_t<B, 64>(tx, a, grid, smem, s);
-    case 96: return launch_t<B, 96>(tx, a, grid, smem, s);
-    case 128: return launch_t<B, 128>(tx, a, grid, smem, s);
-    case 160: return launch_t<B, 160>(tx, a, grid, smem, s);
-    case 192: return launch_t<B, 192>(tx, a, grid, smem, s);
+    case 32: return launch_t<B, 32, S>(tx, a, grid, smem, s);
+    case 64: return launch_t<B, 64, S>(tx, a, grid, smem, s);
+    case 96: return launch_t<B, 96, S>(tx, a, grid, smem, s);
+    case 128: return launch_t<B, 128, S>(tx, a, grid, smem, s);
+    case 160: return launch_t<B, 160, S>(tx, a, grid, smem, s);
+    case 192: return launch_t<B, 192, S>(tx, a, grid, smem, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_score(const CUtensorMap* tmap_xlow, const ScoreArgs& a, bool bf16, int grid, size_t smem,
                          cudaStream_t s) {
-  return bf16 ? launch_d<true>(tmap_xlow, a, grid, smem, s) : launch_d<false>(tmap_xlow, a, grid, smem, s);
+  const bool sample = a.bmax != nullptr;
+  if (sample) return bf16 ? launch_d<true, true>(tmap_xlow, a, grid, smem, s) : launch_d<false, true>(tmap_xlow, a, grid, smem, s);
+  return bf16 ? launch_d<true, false>(tmap_xlow, a, grid, smem, s) : launch_d<false, false>(tmap_xlow, a, grid, smem, s);
 }
 
 int score_tile_rows(int d) { return score_tile_n(d); }

@@ -74,6 +74,25 @@ LV_TC_INL void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   }
 #endif
 }
+// Variants on a precomputed 32-bit shared address (no generic->shared conversion in hot loops).
+LV_TC_INL void mbar_arrive_u32(uint32_t bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(bar) : "memory");
+}
+LV_TC_INL void mbar_wait_sleep_u32(uint32_t bar, uint32_t parity) {
+  long long spins = 0;
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(1000000u)
+        : "memory");
+    if (ok) return;
+#ifndef LV_NO_HANG_TRAP
+    if (++spins > (1ll << 26)) __trap();
+#endif
+  }
+}
 // One lane of the warp (elect.sync); the other lanes get false.
 LV_TC_INL bool elect_one() {
   uint32_t e;
