@@ -31,6 +31,9 @@ constexpr int kTmaWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr int kThreads = 32 * (kEpiWarps + 2);
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kMaxKeysPerLane = 12;    // Cap <= 384
+constexpr int kJobCols = 64;           // score columns per epilogue job (one TMEM lane quarter)
+constexpr int kJV = kJobCols / 32;     // 32-column tcgen05.ld per job
+constexpr int kJobsPerTile = 128 / kJobCols;   // jobs per lane quarter and 128-column tile
 
 // Shared-memory epilogue state.
 struct EpiShared {
@@ -245,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < nacc; ++s) {
       tc::mbar_init(acc_full + s, 1);
-      tc::mbar_init(acc_empty + s, kEpiWarps);
+      tc::mbar_init(acc_empty + s, 4 * kJobsPerTile);   // one arrival per (lane quarter, job)
     }
     tc::mbar_init(a_full + 0, kEpiWarps);
     tc::mbar_init(a_full + 1, kEpiWarps);
@@ -415,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float ts = qvalid ? thr_score(tk) : FLT_MAX;   // padded queries never hit
       uint64_t* const bp = a.cand + si * (size_t)a.Cap;
       const int n_t = (t1 - t0 + tstride - 1) / tstride;   // tiles of this unit
-      const int jend = (tiles_before + n_t) * 4;           // job index bound of this unit
+      const int jend = (tiles_before + n_t) * kJobsPerTile;   // job index bound of this unit
 
       for (;;) {
         int J = pending;
@@ -428,85 +431,108 @@ __global__ void __launch_bounds__(kThreads, 1)
           break;
         }
         pending = -1;
-        const int g = J >> 2, jq = J & 3;                  // global tile ordinal, column quarter
+        const int g = J / kJobsPerTile, jh = J % kJobsPerTile;   // global tile ordinal, column block
         const int t = t0 + (g - tiles_before) * tstride;
+        const int base_pos = t * kN + jh * kJobCols;
+        // GleanVec: original ids of this lane's columns, loaded now so the loads overlap the
+        // accumulator wait and the max (they are only needed on the rare hit path)
+        int32_t my_id[kJV];
+#pragma unroll
+        for (int h = 0; h < kJV; ++h)
+          my_id[h] = (!kSample && a.perm) ? __ldg(a.perm + base_pos + 32 * h + lane) : base_pos + 32 * h + lane;
         const int accb = g % nacc;
         tc::mbar_wait_sleep_u32(acc_full_u + 8u * (uint32_t)accb, (uint32_t)(g / nacc) & 1u);
         tc::tc_fence_after();
-        float v[32];
-        tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kN + (uint32_t)jq * 32u, v);
+        float v[kJobCols];
+#pragma unroll
+        for (int h = 0; h < kJV; ++h)
+          tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kN + (uint32_t)(jh * kJobCols + 32 * h),
+                                 *reinterpret_cast<float(*)[32]>(&v[32 * h]));
         tc::tmem_wait_ld();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
         if (skip_topr) continue;
-        const int base_pos = t * kN + jq * 32;
         if (t == t_last) {   // a cluster segment's last tile may be partial
-          const int tv = a.tile_valid[t_last] - jq * 32;
-          if (tv < 32) {
+          const int tv = a.tile_valid[t_last] - jh * kJobCols;
+          if (tv < kJobCols) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
+            for (int j = 0; j < kJobCols; ++j)
               if (j >= tv) v[j] = -FLT_MAX;
           }
         }
         if (a.raw != nullptr) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + base_pos + j] = v[j];
+          for (int j = 0; j < kJobCols; ++j) a.raw[(size_t)q * a.n_pad + base_pos + j] = v[j];
         }
-        float mx = v[0];
+        float mxh[kJV];
 #pragma unroll
-        for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
+        for (int h = 0; h < kJV; ++h) {
+          float m_ = v[32 * h];
+#pragma unroll
+          for (int j = 1; j < 32; ++j) m_ = fmaxf(m_, v[32 * h + j]);
+          mxh[h] = m_;
+        }
         if (kSample) {
-          // sample stage: record the block maximum (query q, 32 database rows); no top-R here
-          a.bmax[(size_t)((sbase + (t - t0) / tstride) * 4 + jq) * a.m_pad + q] = mx;
+          // sample stage: record the block maxima (query q, 32 database rows each); no top-R here
+#pragma unroll
+          for (int h = 0; h < kJV; ++h)
+            a.bmax[(size_t)((sbase + (t - t0) / tstride) * 4 + jh * kJV + h) * a.m_pad + q] = mxh[h];
           continue;
         }
+        float mx = mxh[0];
+#pragma unroll
+        for (int h = 1; h < kJV; ++h) mx = fmaxf(mx, mxh[h]);
         const bool hit = mx >= ts && mx > -FLT_MAX;
-        uint32_t hb = __ballot_sync(0xffffffffu, hit);
-        if (hb == 0u) continue;
+        if (!__any_sync(0xffffffffu, hit)) continue;
         if (count_stats && lane == 0) atomicAdd(a.stats + 0, 1ull);
         if (fast_only) continue;
-        // hit path (divergence-free): each hitting lane's 32 scores are broadcast through shared
-        // memory, lane j tests column j, survivors are appended to the hitting lane's sub-list with
-        // coalesced stores
-        const int my_pos = base_pos + lane;
-        const int32_t my_id = a.perm ? __ldg(a.perm + my_pos) : my_pos;
-        if (hit) {
+        // hit path (divergence-free), per 32-column half: each hitting lane's 32 scores are
+        // broadcast through shared memory, lane j tests column j, survivors are appended to the
+        // hitting lane's sub-list with coalesced stores
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            reinterpret_cast<float4*>(srows[lane])[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-        }
-        __syncwarp();
-        do {
-          const int Lz = __ffs(hb) - 1;
-          hb &= hb - 1u;
-          const float f = srows[Lz][lane];
-          const float tsz = __shfl_sync(0xffffffffu, ts, Lz);
-          uint64_t tkz = __shfl_sync(0xffffffffu, tk, Lz);
-          int cz = __shfl_sync(0xffffffffu, cnt, Lz);
-          const uint64_t key = make_key(f, my_id);
-          bool keep = f >= tsz && f > -FLT_MAX && key > tkz;
-          uint32_t kb = __ballot_sync(0xffffffffu, keep);
-          if (kb == 0u) continue;
-          uint64_t* bz = reinterpret_cast<uint64_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(bp), Lz));
-          if (cz + __popc(kb) > a.Cap) {
-            // full sub-list: compact it to its top-R (raises its threshold), then re-filter
-            uint64_t nthr;
-            cz = warp_compact_fast(bz, cz, a.R, a.Cap, lane, hist, &nthr);
-            tkz = nthr;
-            if (lane == Lz) {
-              tk = nthr;
-              ts = thr_score(nthr);
-            }
-            if (count_stats && lane == 0) atomicAdd(a.stats + 2, 1ull);
-            keep = keep && key > tkz;
-            kb = __ballot_sync(0xffffffffu, keep);
+        for (int h = 0; h < kJV; ++h) {
+          const bool hh = mxh[h] >= ts && mxh[h] > -FLT_MAX;
+          uint32_t hb = __ballot_sync(0xffffffffu, hh);
+          if (hb == 0u) continue;
+          if (hh) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<float4*>(srows[lane])[j] =
+                  make_float4(v[32 * h + 4 * j], v[32 * h + 4 * j + 1], v[32 * h + 4 * j + 2], v[32 * h + 4 * j + 3]);
           }
-          if (keep) bz[cz + __popc(kb & lt)] = key;
-          if (lane == Lz) cnt = cz + __popc(kb);
-          if (count_stats && lane == 0) atomicAdd(a.stats + 1, (unsigned long long)__popc(kb));
-        } while (hb != 0u);
-        __syncwarp();
+          __syncwarp();
+          do {
+            const int Lz = __ffs(hb) - 1;
+            hb &= hb - 1u;
+            const float f = srows[Lz][lane];
+            const float tsz = __shfl_sync(0xffffffffu, ts, Lz);
+            uint64_t tkz = __shfl_sync(0xffffffffu, tk, Lz);
+            int cz = __shfl_sync(0xffffffffu, cnt, Lz);
+            const uint64_t key = make_key(f, my_id[h]);
+            bool keep = f >= tsz && f > -FLT_MAX && key > tkz;
+            uint32_t kb = __ballot_sync(0xffffffffu, keep);
+            if (kb == 0u) continue;
+            uint64_t* bz = reinterpret_cast<uint64_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(bp), Lz));
+            if (cz + __popc(kb) > a.Cap) {
+              // full sub-list: compact it to its top-R (raises its threshold), then re-filter
+              uint64_t nthr;
+              cz = warp_compact_fast(bz, cz, a.R, a.Cap, lane, hist, &nthr);
+              tkz = nthr;
+              if (lane == Lz) {
+                tk = nthr;
+                ts = thr_score(nthr);
+              }
+              if (count_stats && lane == 0) atomicAdd(a.stats + 2, 1ull);
+              keep = keep && key > tkz;
+              kb = __ballot_sync(0xffffffffu, keep);
+            }
+            if (keep) bz[cz + __popc(kb & lt)] = key;
+            if (lane == Lz) cnt = cz + __popc(kb);
+            if (count_stats && lane == 0) atomicAdd(a.stats + 1, (unsigned long long)__popc(kb));
+          } while (hb != 0u);
+          __syncwarp();
+        }
       }
       tiles_before += n_t;
       // unit end: every job of this unit has seen its tile committed, so the MMA is done with
