@@ -31,9 +31,7 @@ constexpr int kTmaWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr int kThreads = 32 * (kEpiWarps + 2);
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kMaxKeysPerLane = 12;    // Cap <= 384
-constexpr int kJobCols = 64;           // score columns per epilogue job (one TMEM lane quarter)
-constexpr int kJV = kJobCols / 32;     // 32-column tcgen05.ld per job
-constexpr int kJobsPerTile = 128 / kJobCols;   // jobs per lane quarter and 128-column tile
+
 
 // Shared-memory epilogue state.
 struct EpiShared {
@@ -58,6 +56,11 @@ __host__ __device__ constexpr int score_nacc(int d) {
   return (512 - d) / kTileN > kMaxAcc ? kMaxAcc : (512 - d) / kTileN;
 }
 __host__ __device__ constexpr int score_tile_n(int d) { return kTileN + 0 * d; }
+// Epilogue jobs: (128-column tile, column block) per TMEM lane quarter, taken in order by the
+// quarter's 4 warps.  A waiting warp checks the accumulator barrier by phase parity, which is
+// only unambiguous while the quarter's in-flight jobs (<= 4) span at most nacc tiles; hence
+// 64-column jobs (2 per tile, span <= 3 tiles) need nacc >= 3, else 32-column jobs (span <= 2).
+__host__ __device__ constexpr int job_cols(int d) { return score_nacc(d) >= 3 ? 64 : 32; }
 
 __host__ __device__ inline ScoreSmemLayout score_smem_layout(int d, int stages) {
   ScoreSmemLayout L;
@@ -221,6 +224,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int nch = d / kCH;
   constexpr uint32_t box_bytes = (uint32_t)kN * kCH * 2u;
   constexpr int nacc = score_nacc(kD);
+  constexpr int kJobCols = job_cols(kD);          // score columns per epilogue job
+  constexpr int kJV = kJobCols / 32;              // 32-column tcgen05.ld per job
+  constexpr int kJobsPerTile = 128 / kJobCols;    // jobs per lane quarter and tile
+  static_assert((3 + kJobsPerTile - 1) / kJobsPerTile + 1 <= nacc, "4 in-flight jobs must span <= nacc tiles");
   const ScoreSmemLayout L = score_smem_layout(d, a.stages);
   uint8_t* sB = smem + L.b_off;
   EpiShared& S = *reinterpret_cast<EpiShared*>(smem + L.epi_off);
@@ -438,70 +445,59 @@ __global__ void __launch_bounds__(kThreads, 1)
         // accumulator wait and the max (they are only needed on the rare hit path)
         int32_t my_id[kJV];
 #pragma unroll
-        for (int h = 0; h < kJV; ++h)
-          my_id[h] = (!kSample && a.perm) ? __ldg(a.perm + base_pos + 32 * h + lane) : base_pos + 32 * h + lane;
+        for (int h = 0; h < kJV; ++h) my_id[h] = (!kSample && a.perm) ? __ldg(a.perm + base_pos + 32 * h + lane) : 0;
         const int accb = g % nacc;
         tc::mbar_wait_sleep_u32(acc_full_u + 8u * (uint32_t)accb, (uint32_t)(g / nacc) & 1u);
         tc::tc_fence_after();
-        float v[kJobCols];
+        // the job's 32-column halves in turn: load, (mask), max, compare, rare hit path; the
+        // accumulator is released after the last half's load
 #pragma unroll
-        for (int h = 0; h < kJV; ++h)
-          tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kN + (uint32_t)(jh * kJobCols + 32 * h),
-                                 *reinterpret_cast<float(*)[32]>(&v[32 * h]));
-        tc::tmem_wait_ld();
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
-        if (skip_topr) continue;
-        if (t == t_last) {   // a cluster segment's last tile may be partial
-          const int tv = a.tile_valid[t_last] - jh * kJobCols;
-          if (tv < kJobCols) {
-#pragma unroll
-            for (int j = 0; j < kJobCols; ++j)
-              if (j >= tv) v[j] = -FLT_MAX;
+        for (int h = 0; h < kJV; ++h) {
+          float v[32];
+          tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kN + (uint32_t)(jh * kJobCols + 32 * h), v);
+          tc::tmem_wait_ld();
+          if (h + 1 == kJV) {
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
           }
-        }
-        if (a.raw != nullptr) {
+          if (skip_topr) continue;
+          const int hpos = base_pos + 32 * h;
+          if (t == t_last) {   // a cluster segment's last tile may be partial
+            const int tv = a.tile_valid[t_last] - (jh * kJobCols + 32 * h);
+            if (tv < 32) {
 #pragma unroll
-          for (int j = 0; j < kJobCols; ++j) a.raw[(size_t)q * a.n_pad + base_pos + j] = v[j];
-        }
-        float mxh[kJV];
+              for (int j = 0; j < 32; ++j)
+                if (j >= tv) v[j] = -FLT_MAX;
+            }
+          }
+          if (a.raw != nullptr) {
 #pragma unroll
-        for (int h = 0; h < kJV; ++h) {
-          float m_ = v[32 * h];
+            for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + hpos + j] = v[j];
+          }
+          float mx = v[0];
 #pragma unroll
-          for (int j = 1; j < 32; ++j) m_ = fmaxf(m_, v[32 * h + j]);
-          mxh[h] = m_;
-        }
-        if (kSample) {
-          // sample stage: record the block maxima (query q, 32 database rows each); no top-R here
-#pragma unroll
-          for (int h = 0; h < kJV; ++h)
-            a.bmax[(size_t)((sbase + (t - t0) / tstride) * 4 + jh * kJV + h) * a.m_pad + q] = mxh[h];
-          continue;
-        }
-        float mx = mxh[0];
-#pragma unroll
-        for (int h = 1; h < kJV; ++h) mx = fmaxf(mx, mxh[h]);
-        const bool hit = mx >= ts && mx > -FLT_MAX;
-        if (!__any_sync(0xffffffffu, hit)) continue;
-        if (count_stats && lane == 0) atomicAdd(a.stats + 0, 1ull);
-        if (fast_only) continue;
-        // hit path (divergence-free), per 32-column half: each hitting lane's 32 scores are
-        // broadcast through shared memory, lane j tests column j, survivors are appended to the
-        // hitting lane's sub-list with coalesced stores
-#pragma unroll
-        for (int h = 0; h < kJV; ++h) {
-          const bool hh = mxh[h] >= ts && mxh[h] > -FLT_MAX;
-          uint32_t hb = __ballot_sync(0xffffffffu, hh);
+          for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
+          if (kSample) {
+            // sample stage: record the block maximum (query q, 32 database rows); no top-R here
+            a.bmax[(size_t)((sbase + (t - t0) / tstride) * 4 + jh * kJV + h) * a.m_pad + q] = mx;
+            continue;
+          }
+          const bool hit = mx >= ts && mx > -FLT_MAX;
+          uint32_t hb = __ballot_sync(0xffffffffu, hit);
           if (hb == 0u) continue;
-          if (hh) {
+          if (count_stats && lane == 0) atomicAdd(a.stats + 0, 1ull);
+          if (fast_only) continue;
+          // hit path (divergence-free): each hitting lane's 32 scores are broadcast through shared
+          // memory, lane j tests column j, survivors are appended to the hitting lane's sub-list
+          // with coalesced stores
+          if (hit) {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-              reinterpret_cast<float4*>(srows[lane])[j] =
-                  make_float4(v[32 * h + 4 * j], v[32 * h + 4 * j + 1], v[32 * h + 4 * j + 2], v[32 * h + 4 * j + 3]);
+              reinterpret_cast<float4*>(srows[lane])[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
           __syncwarp();
+          const int32_t id_h = (a.perm ? my_id[h] : hpos + lane);
           do {
             const int Lz = __ffs(hb) - 1;
             hb &= hb - 1u;
@@ -509,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float tsz = __shfl_sync(0xffffffffu, ts, Lz);
             uint64_t tkz = __shfl_sync(0xffffffffu, tk, Lz);
             int cz = __shfl_sync(0xffffffffu, cnt, Lz);
-            const uint64_t key = make_key(f, my_id[h]);
+            const uint64_t key = make_key(f, id_h);
             bool keep = f >= tsz && f > -FLT_MAX && key > tkz;
             uint32_t kb = __ballot_sync(0xffffffffu, keep);
             if (kb == 0u) continue;
