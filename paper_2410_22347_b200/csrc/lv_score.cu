@@ -49,11 +49,16 @@ constexpr int kMaxAcc = 8;
 
 __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
-// TMEM: columns [0, d) hold the double-buffered A operand (one 128-query tile, d bf16 = d/2
-// columns per buffer); the rest holds NACC fp32 accumulator buffers of N = 128 columns.
+// TMEM: the A operand (one 128-query tile, d bf16 = d/2 columns) then NACC fp32 accumulator
+// buffers of N = 128 columns.  A is double-buffered across work units (the next unit's A is
+// written while the current one runs) unless that would leave fewer than 3 accumulators
+// (d > 128): then A is single-buffered and rewritten after each unit (one short bubble per
+// unit, units are long at those sizes).
 constexpr int kTileN = 128;
+__host__ __device__ constexpr bool score_single_a(int d) { return (512 - d) / kTileN < 3; }
+__host__ __device__ constexpr int score_a_cols(int d) { return score_single_a(d) ? d / 2 : d; }
 __host__ __device__ constexpr int score_nacc(int d) {
-  return (512 - d) / kTileN > kMaxAcc ? kMaxAcc : (512 - d) / kTileN;
+  return (512 - score_a_cols(d)) / kTileN > kMaxAcc ? kMaxAcc : (512 - score_a_cols(d)) / kTileN;
 }
 __host__ __device__ constexpr int score_tile_n(int d) { return kTileN + 0 * d; }
 // Epilogue jobs: (128-column tile, column block) per TMEM lane quarter, taken in order by the
@@ -268,7 +273,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr;
-  const uint32_t acc_col0 = (uint32_t)d;          // A buffers occupy columns [0, d)
+  constexpr bool kSingleA = score_single_a(kD);
+  const uint32_t acc_col0 = (uint32_t)score_a_cols(kD);   // A buffer(s) occupy columns [0, acc_col0)
   const uint32_t acc_full_u = tc::smem_u32(acc_full), acc_empty_u = tc::smem_u32(acc_empty);
 
   if (warp == kTmaWarp) {
@@ -303,9 +309,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int c = u / QT;
       const int* ci = a.chunk_info + kChunkInts * c;
       const int t0 = ci[0], t1 = ci[1], ts_ = ci[3];
-      tc::mbar_wait_sleep(a_full + (i & 1), (uint32_t)(i >> 1) & 1u);
+      if (kSingleA) tc::mbar_wait_sleep(a_full, (uint32_t)i & 1u);
+      else tc::mbar_wait_sleep(a_full + (i & 1), (uint32_t)(i >> 1) & 1u);
       tc::tc_fence_after();
-      const uint32_t at = tmem_base + (uint32_t)(i & 1) * (uint32_t)(d / 2);
+      const uint32_t at = tmem_base + (kSingleA ? 0u : (uint32_t)(i & 1) * (uint32_t)(d / 2));
       for (int t = t0; t < t1; t += ts_) {
         tc::mbar_wait_sleep(acc_empty + acc, acc_phase ^ 1);
         tc::mbar_wait_sleep(b_full + stage, phase);
@@ -388,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int pending = -1;       // a job index already taken that belongs to a later unit
     int i = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
-      if (u + (int)gridDim.x < nunits) write_A(u + gridDim.x, (i + 1) & 1);
+      if (!kSingleA && u + (int)gridDim.x < nunits) write_A(u + gridDim.x, (i + 1) & 1);
       const int c = u / QT, qt = u % QT;
       const int* ci = a.chunk_info + kChunkInts * c;
       const int t0 = ci[0], t1 = ci[1], tstride = ci[3], sbase = ci[4];
@@ -543,6 +550,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc::named_bar_sync(1, kEpiThreads);
       if (lists && threadIdx.x == 0) atomicAnd(a.slot_busy + qt, ~(1 << my_slot));   // release the slot
+      // single-buffered A: every job of this unit saw its tile committed, so the MMAs of this unit
+      // are complete and its A buffer can take the next unit's operand
+      if (kSingleA && u + (int)gridDim.x < nunits) write_A(u + gridDim.x, 0);
     }
   }
   tc::tc_fence_before();
