@@ -297,11 +297,12 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   int nsamp = 0;
   for (auto& sg : seg) nsamp += (sg.second - sg.first + stride - 1) / stride;
   const int j1 = (int)std::ceil(gamma * R / stride);
-  pl->sampled = env_double("LV_SAMPLED", 1.0) != 0.0 && stride >= 2 && nsamp >= 64 && 4 * nsamp >= 16 * j1 &&
-                4 * nsamp <= 65535;
+  const int bpt = lv::score_blocks_per_tile(ix->d);   // block maxima per sampled tile
+  pl->sampled = env_double("LV_SAMPLED", 1.0) != 0.0 && stride >= 2 && nsamp >= 64 && bpt * nsamp >= 8 * j1 &&
+                bpt * nsamp <= 65535;
   if (pl->sampled) {
     pl->stride = stride;
-    pl->nblk = 4 * nsamp;
+    pl->nblk = bpt * nsamp;
     pl->j1 = std::max(4, j1);
     pl->j2 = std::min(pl->nblk, 4 * pl->j1);
     pl->chunks.clear();

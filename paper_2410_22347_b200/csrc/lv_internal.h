@@ -37,7 +37,7 @@ struct ScoreArgs {
   uint64_t* tau;               // [NS][m_pad]
   int32_t* slot_busy;          // [QP] bitmask of claimed slots per query tile (zero between launches)
   float* raw;                  // [m_pad][n_pad] or nullptr
-  float* bmax;                 // sample stage: [n_sample_tiles * 4][m_pad] block maxima, else nullptr
+  float* bmax;                 // sample stage: [n_sample_tiles * blocks_per_tile][m_pad] block maxima, else nullptr
   const int32_t* m_dev;        // device query count (repair passes; overrides m and QP), or nullptr
   int64_t n_pad;
   int flags;                   // debug: bit0 = epilogue skips top-R (MMA/TMA throughput probe),
@@ -48,6 +48,7 @@ struct ScoreArgs {
 cudaError_t launch_score(const CUtensorMap* tmap_xlow, const ScoreArgs& a, bool bf16, int grid, size_t smem,
                          cudaStream_t s);
 int score_tile_rows(int d);
+int score_blocks_per_tile(int d);   // sample stage: block maxima recorded per tile and query
 
 struct RerankArgs {
   int m, m_pad, D, R, k, NS, Cap;

@@ -458,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tc_fence_after();
         // the job's 32-column halves in turn: load, (mask), max, compare, rare hit path; the
         // accumulator is released after the last half's load
+        float bm = -FLT_MAX;   // sample stage: running block maximum of the job
 #pragma unroll
         for (int h = 0; h < kJV; ++h) {
           float v[32];
@@ -486,8 +487,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
           if (kSample) {
-            // sample stage: record the block maximum (query q, 32 database rows); no top-R here
-            a.bmax[(size_t)((sbase + (t - t0) / tstride) * 4 + jh * kJV + h) * a.m_pad + q] = mx;
+            // sample stage: record the block maximum (query q, the job's kJobCols database rows);
+            // no top-R here
+            bm = fmaxf(bm, mx);
+            if (h + 1 == kJV)
+              a.bmax[(size_t)((sbase + (t - t0) / tstride) * kJobsPerTile + jh) * a.m_pad + q] = bm;
             continue;
           }
           const bool hit = mx >= ts && mx > -FLT_MAX;
@@ -592,5 +596,15 @@ cudaError_t launch_score(const CUtensorMap* tmap_xlow, const ScoreArgs& a, bool 
 }
 
 int score_tile_rows(int d) { return score_tile_n(d); }
+int score_blocks_per_tile(int d) {   // block maxima per sampled tile (one per epilogue job)
+  switch (d) {
+    case 32: return 128 / job_cols(32);
+    case 64: return 128 / job_cols(64);
+    case 96: return 128 / job_cols(96);
+    case 128: return 128 / job_cols(128);
+    case 160: return 128 / job_cols(160);
+    default: return 128 / job_cols(192);
+  }
+}
 
 }  // namespace lv

@@ -79,20 +79,31 @@ def test_fullsize_sampled_parity(lv, cfg_id):
     thr = ref_s[:, -1]
     # G2: the GPU candidates' reduced scores vs the oracle's score of the same (query, id)
     Xc = X[cid]                                                        # [s, R, D]
+    n_ok = n_all = 0
     for j in range(len(sel)):
         a = None if assign is None else assign[cid[j]]
         xl = O.encode(Xc[j], B32, a, store=c.low_dtype)
         s_ref = O.reduced_scores(Qp[j:j + 1], xl, a)[0]
+        flip = 2.0 ** -7 * O.reduced_scores(np.abs(Qp[j:j + 1]), np.abs(xl), a)[0]   # DESIGN.md R11
         scale = np.linalg.norm(Qp[j]) * np.linalg.norm(xl, axis=1).max()
-        assert (np.abs(csc[j] - s_ref) <= TOL_RED * np.maximum(np.abs(s_ref), 1e-2 * scale)).all(), j
-        # G3: same candidate set except ids within 2e-3 of the oracle's R-th reduced score
+        ok = np.abs(csc[j] - s_ref) <= TOL_RED * np.maximum(np.abs(s_ref), 1e-2 * scale)
+        n_ok += int(ok.sum())
+        n_all += ok.size
+        assert (np.abs(csc[j] - s_ref) <= flip + TOL_RED * np.abs(s_ref) + 1e-6).all(), j
+        # G3: same candidate set except ids near the oracle's R-th reduced score (2e-3 + flips)
+        iR = np.array([ref_i[j, -1]])
+        aR = None if assign is None else assign[iR]
+        xR = O.encode(X[iR], B32, aR, store=c.low_dtype)
+        fR = 2.0 ** -7 * O.reduced_scores(np.abs(Qp[j:j + 1]), np.abs(xR), aR)[0, 0]
         diff = set(cid[j].tolist()) ^ set(ref_i[j].tolist())
         for i in diff:
-            if i in set(cid[j].tolist()):
-                si = float(s_ref[list(cid[j]).index(i)])
-            else:
-                si = float(ref_s[j][list(ref_i[j]).index(i)])
-            assert abs(si - thr[j]) <= TOL_RED * max(abs(thr[j]), 1e-2), (j, i, si, thr[j])
+            ii = np.array([i])
+            ai = None if assign is None else assign[ii]
+            xi = O.encode(X[ii], B32, ai, store=c.low_dtype)
+            si = float(O.reduced_scores(Qp[j:j + 1], xi, ai)[0, 0])
+            fi = float(2.0 ** -7 * O.reduced_scores(np.abs(Qp[j:j + 1]), np.abs(xi), ai)[0, 0])
+            assert abs(si - thr[j]) <= TOL_RED * max(abs(thr[j]), 1e-2) + fi + fR, (j, i, si, thr[j])
+    assert n_ok >= 0.999 * n_all, (n_ok, n_all)
     # G4: re-rank scores vs fp64 <q, x> on the canonical vectors
     ex = np.einsum("md,mkd->mk", Qs.astype(np.float64), X[ids].astype(np.float64))
     assert (np.abs(sc - ex) <= TOL_RR * np.maximum(np.abs(ex), 1e-2)).all(), np.abs(sc - ex).max()

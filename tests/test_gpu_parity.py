@@ -155,19 +155,26 @@ def _check_search(lv, c, X, Q, A32, B32, assign, R, k, C, check_recall=True, tim
     csc = dbg["cand_scores"].cpu().numpy().astype(np.float64)
     ref = O.search(Q, X, A32, B32, assign if C > 1 else None, R, k, store=c.low_dtype)
     m = Q.shape[0]
-    # G2: candidate reduced scores vs oracle fp64 reduced scores of the same (q, id)
+    # G2: candidate reduced scores vs oracle fp64 reduced scores of the same (q, id).  A one-ulp
+    # storage flip of one operand element moves a score by <= 2^-8 |q'_e x_e| (R11):
+    # every score within the flip bound F = 2^-7 sum_e |q'_e x_e| + 2e-3 |s|, >= 99.9 % within 2e-3
     S = O.reduced_scores(ref["Qp"], ref["X_low"], assign if C > 1 else None)
+    F = 2.0 ** -7 * O.reduced_scores(np.abs(ref["Qp"]), np.abs(ref["X_low"]), assign if C > 1 else None)
     rows = np.arange(m)[:, None]
     got = csc
     exp = S[rows, cid]
     scale = np.abs(S).max()
-    assert _tol_ok(got, exp, TOL_RED, scale).all()
-    # G3: candidate sets equal except ids within 2e-3 (relative) of the oracle's R-th score
+    ok = _tol_ok(got, exp, TOL_RED, scale)
+    assert ok.mean() >= 0.999, (~ok).sum()
+    assert (np.abs(got - exp) <= F[rows, cid] + TOL_RED * np.abs(exp) + 1e-6).all()
+    # G3: candidate sets equal except ids near the oracle's R-th score (2e-3 plus both flip bounds)
     for j in range(m):
         a, b = set(cid[j].tolist()), set(ref["cand"][j].tolist())
         thr = ref["cand_scores"][j, -1]
+        iR = int(ref["cand"][j, -1])
         for i in a ^ b:
-            assert abs(S[j, i] - thr) <= TOL_RED * max(abs(thr), 1e-2), (j, i, S[j, i], thr)
+            band = TOL_RED * max(abs(thr), 1e-2) + F[j, i] + F[j, iR]
+            assert abs(S[j, i] - thr) <= band, (j, i, S[j, i], thr)
         # sorted order of the GPU list follows (score desc, id asc) on its own scores
         keys = list(zip(-csc[j], cid[j]))
         assert keys == sorted(keys)
@@ -180,10 +187,11 @@ def _check_search(lv, c, X, Q, A32, B32, assign, R, k, C, check_recall=True, tim
             a, b = set(ids[j].tolist()), set(ref["ids"][j].tolist())
             kth = ref["scores"][j, -1]
             thr = ref["cand_scores"][j, -1]
+            iR = int(ref["cand"][j, -1])
             for i in a ^ b:
                 rr = float(Q[j].astype(np.float64) @ X[i].astype(np.float64))
                 near_k = abs(rr - kth) <= TOL_RR * max(abs(kth), 1e-2)
-                near_r = abs(S[j, i] - thr) <= TOL_RED * max(abs(thr), 1e-2)
+                near_r = abs(S[j, i] - thr) <= TOL_RED * max(abs(thr), 1e-2) + F[j, i] + F[j, iR]
                 assert near_k or near_r, (j, i)
     # G6: recall against exact search
     if check_recall:
@@ -319,9 +327,9 @@ def test_deterministic(lv):
 
 
 def test_sampled_path_parity(lv):
-    """A database large enough (>= 64 sampled tiles) for the sampled-threshold path: sample stage
+    """A database large enough (>= 64 sampled tiles, >= 8 j1 block maxima) for the sampled-threshold path: sample stage
     of block maxima, per-query threshold, one thresholded main scan, exactness check."""
-    c, X, Q, A32, B32, assign, R, k = _case(1, n=150_000, m=300, d=64)
+    c, X, Q, A32, B32, assign, R, k = _case(1, n=200_000, m=300, d=64)
     dbg = _check_search(lv, c, X, Q, A32, B32, assign, R, k, 1, timing=True)
     assert dbg["path"] == 1
 
@@ -331,7 +339,7 @@ def test_sampled_path_repairs(lv, monkeypatch):
     every query fail the exactness check; round 1 repairs with the looser bound (about half fail
     again), round 2 without a threshold.  Results must still be the exact top-R / top-k."""
     monkeypatch.setenv("LV_SAMPLE_GAMMA", "0.05")
-    c, X, Q, A32, B32, assign, _, k = _case(1, n=150_000, m=200, d=32)
+    c, X, Q, A32, B32, assign, _, k = _case(1, n=200_000, m=200, d=32)
     dbg = _check_search(lv, c, X, Q, A32, B32, assign, 256, k, 1, check_recall=False, timing=True)
     assert dbg["path"] == 1 and dbg["failed"][0] == Q.shape[0] and dbg["failed"][1] > 0, dbg["failed"]
 
@@ -339,6 +347,6 @@ def test_sampled_path_repairs(lv, monkeypatch):
 def test_sampled_path_gleanvec(lv):
     """Sampled path on a cluster-sorted GleanVec index (C = 4): the sample is stratified per
     cluster segment, block maxima are indexed across segments."""
-    c, X, Q, A32, B32, assign, R, k = _case(3, n=150_000, m=200, d=96, C=4)
+    c, X, Q, A32, B32, assign, R, k = _case(3, n=200_000, m=200, d=96, C=4)
     dbg = _check_search(lv, c, X, Q, A32, B32, assign, R, k, 4, timing=True)
     assert dbg["path"] == 1
