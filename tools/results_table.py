@@ -1,0 +1,47 @@
+"""Markdown results table from the committed bench lines (profiles/<tag>_bench_cfg<N>*.json, newest
+per config), for DESIGN.md §11.
+
+  python tools/results_table.py [--tag r01]
+"""
+import argparse
+import glob
+import json
+import os
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def latest(tag, c):
+    fs = sorted(glob.glob(os.path.join(ROOT, "profiles", f"{tag}_bench_cfg{c}_v*.json")),
+                key=lambda p: int(p.rsplit("_v", 1)[1].split(".")[0]))
+    return fs[-1] if fs else None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tag", default="r01")
+    a = ap.parse_args()
+    print("| cfg | workload | queries/s | e2e q/s | ms/step | main scan ms | frac of bf16 peak (burst / sustained) "
+          "| K5 ms (frac of HBM, algorithmic) | K1 | sample+select | K4 | repairs | recall GPU / emulated oracle "
+          "| oracle q/s (cores) | SM MHz | file |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+    for c in range(1, 6):
+        f = latest(a.tag, c)
+        if not f:
+            continue
+        d = json.load(open(f))
+        k = d.get("kernel_ms", {})
+        r = d.get("roofline", {})
+        rr = d.get("roofline_rerank", {})
+        rec = d.get("recall_at_10", {})
+        cb = d.get("cpu_baseline", {})
+        print(f"| {c} | {d['config']['workload']} | {d['value']:,.0f} | {d['e2e']['value']:,.0f} | {d['ms_per_step']:.3f} "
+              f"| {k.get('main_scan', 0):.3f} | {r.get('frac', 0):.3f} / {r.get('frac_of_sustained', 0):.3f} "
+              f"| {k.get('rerank_K5', 0):.3f} ({rr.get('frac', 0):.2f}) | {k.get('project_K1', 0):.3f} "
+              f"| {k.get('sample_stage', 0) + k.get('threshold_select', 0):.3f} | {k.get('select_K4', 0):.3f} "
+              f"| {k.get('repairs', 0):.3f} | {rec.get('gpu', '-')} / {rec.get('oracle_emulated', '-')} "
+              f"| {cb.get('value', '-')} ({cb.get('cores', '-')}) | {d['clocks'].get('sm_mhz')} | {os.path.basename(f)} |")
+
+
+if __name__ == "__main__":
+    main()
