@@ -293,10 +293,19 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   // block maxima, a per-query threshold with >= j1 rows above it is selected, one main stage
   // scans everything with it; queries left with < R candidates are repaired exactly.
   const int stride = (int)env_double("LV_SAMPLE_STRIDE", 16.0);
-  const double gamma = env_double("LV_SAMPLE_GAMMA", 3.0);
   int nsamp = 0;
   for (auto& sg : seg) nsamp += (sg.second - sg.first + stride - 1) / stride;
-  const int j1 = (int)std::ceil(gamma * R / stride);
+  // j1: about j1 * stride database rows score above the j1-th largest sampled block maximum, with a
+  // relative spread ~ 1 / sqrt(j1); take the smallest j1 with j1 s - z sqrt(j1) s >= R (z = 2.9:
+  // ~0.2 % of queries need the repair pass), or gamma R / s if LV_SAMPLE_GAMMA is set
+  int j1 = 1;
+  const char* gam = getenv("LV_SAMPLE_GAMMA");
+  if (gam) {
+    j1 = (int)std::ceil(atof(gam) * R / stride);
+  } else {
+    const double z = env_double("LV_SAMPLE_Z", 2.9);
+    while ((double)j1 * stride - z * std::sqrt((double)j1) * stride < (double)R) ++j1;
+  }
   const int bpt = lv::score_blocks_per_tile(ix->d);   // block maxima per sampled tile
   pl->sampled = env_double("LV_SAMPLED", 1.0) != 0.0 && stride >= 2 && nsamp >= 64 && bpt * nsamp >= 8 * j1 &&
                 bpt * nsamp <= 65535;

@@ -1,2 +1,1 @@
-for c in 2 5; do CFG=$c REPS=2 FLAGS=2 timeout 900 python tools/prof_scan.py 2>&1 | grep "sampled"; CFG=$c REPS=2 timeout 900 python tools/prof_scan.py 2>&1 | grep -v "^\[bench\]"; done
-timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -q -x 2>&1 | tail -1
+for c in 3 2; do for f in 4 8 0; do echo "cfg $c flags $f"; CFG=$c REPS=3 FLAGS=$f timeout 900 python tools/prof_scan.py 2>&1 | grep -v "^\[bench\]"; done; done
