@@ -60,6 +60,10 @@ struct lv_index {
   int32_t Kp = 0;              // D rounded up to 64 (K1 operand planes)
   void* A_planes = nullptr;    // bf16 [3][C*d][Kp]: A split v = h + m + l (lv_proj.cu)
   CUtensorMap tmap_a;          // A planes, 128-row x 64-column boxes
+  void* B_planes = nullptr;    // bf16 [3][C*d][Kp]: B split, K6 operand
+  CUtensorMap tmap_b;          // B planes, d-row x 64-column boxes
+  float enc_ms[3] = {0, 0, 0}; // last encode: sort, K6, full copy (lv_encode_timing)
+  bool enc_timed = false;
   int64_t n = 0, n_pad = 0;
   void* X_low = nullptr;       // [n_pad, d] low dtype, cluster-sorted, 128-row padded segments
   int32_t* perm = nullptr;     // [n_pad] sorted position -> original id (-1 padding)
@@ -157,6 +161,12 @@ double env_double(const char* name, double dflt) {
 // K1 on tensor cores (lv_proj.cu) unless LV_K1=simt (fp32 CUDA-core GEMM)
 bool k1_tensor() {
   const char* v = getenv("LV_K1");
+  return !(v && v[0] == 's');
+}
+
+// K6 on tensor cores unless LV_K6=simt
+bool k6_tensor() {
+  const char* v = getenv("LV_K6");
   return !(v && v[0] == 's');
 }
 
@@ -498,6 +508,21 @@ lv_status lv_index_create(lv_index** out, int32_t D, int32_t d, int32_t C, lv_dt
     lv_index_destroy(ix);
     return st;
   }
+  // K6 operand: B split the same way
+  if (cudaMalloc(&ix->B_planes, (size_t)3 * Nc * ix->Kp * 2) != cudaSuccess) {
+    lv_index_destroy(ix);
+    return fail(LV_ENOMEM, "lv_index_create: cudaMalloc failed");
+  }
+  if (lv::launch_split3(ix->B, Nc, Nc, D, ix->Kp, ix->B_planes, 0) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
+    lv_index_destroy(ix);
+    return fail(LV_ECUDA, "lv_index_create: split failed");
+  }
+  st = make_tmap(&ix->tmap_b, ix->B_planes, 3 * Nc, ix->Kp, 64, true, d);
+  if (st) {
+    lv_index_destroy(ix);
+    return st;
+  }
   *out = ix;
   return LV_OK;
 }
@@ -525,6 +550,13 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
   free_db(ix);
   const int C = ix->C;
   std::vector<int64_t> hseg(2 * C + 1, 0);
+  struct Events {   // released on every return path
+    cudaEvent_t e[4] = {};
+    ~Events() { for (auto x : e) if (x) cudaEventDestroy(x); }
+  } evs;
+  cudaEvent_t* ev = evs.e;
+  for (int i = 0; i < 4; ++i) LV_CUDA(cudaEventCreate(&ev[i]));
+  LV_CUDA(cudaEventRecord(ev[0], s));
   int32_t* perm_tmp = nullptr;
   if (C > 1) {
     const int nb = (int)((n + lv::kSortBlock - 1) / lv::kSortBlock);
@@ -574,22 +606,47 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
   }
   int32_t* dwrow = nullptr;
   if (cudaMalloc(&ix->tile_valid, sizeof(int32_t) * nt) != cudaSuccess) return fail(LV_ENOMEM, "tile_valid");
-  LV_CUDA(cudaMallocAsync(&dwrow, sizeof(int32_t) * nt * 2, s));
+  LV_CUDA(cudaMallocAsync(&dwrow, sizeof(int32_t) * nt * 3, s));
   LV_CUDA(cudaMemcpyAsync(ix->tile_valid, tv.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, s));
   LV_CUDA(cudaMemcpyAsync(dwrow, wrow.data(), sizeof(int32_t) * nt * 2, cudaMemcpyHostToDevice, s));
+  // K6 tile order (C > 1): by the tile's first original row, so the CTAs in flight together read one
+  // contiguous window of X (all clusters' rows of it) instead of every C-th row of a wide span
+  int32_t* dorder = nullptr;
+  if (C > 1) {
+    std::vector<int32_t> first(nt), order(nt);
+    LV_CUDA(cudaMemcpy2DAsync(first.data(), sizeof(int32_t), ix->perm, 128 * sizeof(int32_t), sizeof(int32_t), nt,
+                              cudaMemcpyDeviceToHost, s));
+    LV_CUDA(cudaStreamSynchronize(s));
+    for (int64_t t = 0; t < nt; ++t) order[t] = (int32_t)t;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+      return (uint32_t)first[a] < (uint32_t)first[b];   // an all-padding tile (-1) goes last
+    });
+    dorder = dwrow + 2 * nt;
+    LV_CUDA(cudaMemcpyAsync(dorder, order.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, s));
+    LV_CUDA(cudaStreamSynchronize(s));   // `order` is pageable and leaves scope
+  }
   // X_low = RNE(B_c x) (K6)
   const size_t esz = 2;
   if (cudaMalloc(&ix->X_low, esz * ix->n_pad * ix->d) != cudaSuccess) return fail(LV_ENOMEM, "X_low");
-  LV_CUDA(lv::launch_rows_gemm(X, x_dtype == LV_F16, ix->D, ix->perm, n, ix->n_pad, ix->B, ix->D, dwrow, ix->d,
-                               ix->X_low, ix->low, ix->d, ix->n_pad, s));
+  LV_CUDA(cudaEventRecord(ev[1], s));
+  if (k6_tensor())
+    LV_CUDA(lv::launch_encode_tc(&ix->tmap_b, X, x_dtype == LV_F16, ix->D, ix->Kp, ix->d, ix->C * ix->d, ix->perm, dwrow,
+                                 dorder, nt, ix->X_low, ix->low == LV_BF16, s));
+  else
+    LV_CUDA(lv::launch_rows_gemm(X, x_dtype == LV_F16, ix->D, ix->perm, n, ix->n_pad, ix->B, ix->D, dwrow, ix->d,
+                                 ix->X_low, ix->low, ix->d, ix->n_pad, s));
   // full-precision copy for the re-rank
   const size_t fsz = ix->full == LV_F16 ? 2 : 4;
   if (cudaMalloc(&ix->X_full, fsz * n * ix->D) != cudaSuccess) return fail(LV_ENOMEM, "X_full");
+  LV_CUDA(cudaEventRecord(ev[2], s));
   LV_CUDA(lv::launch_convert(X, x_dtype == LV_F16, ix->X_full, ix->full == LV_F16, n * ix->D, s));
+  LV_CUDA(cudaEventRecord(ev[3], s));
   lv_status ts = make_tmap(&ix->tmap_xlow, ix->X_low, ix->n_pad, ix->d, (ix->d % 64 == 0) ? 64 : 32, ix->low == LV_BF16,
                            lv::score_tile_rows(ix->d));
   LV_CUDA(cudaStreamSynchronize(s));
   cudaFree(dwrow);
+  for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&ix->enc_ms[i], ev[i], ev[i + 1]);
+  ix->enc_timed = true;
   return ts;
 }
 
@@ -911,6 +968,13 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   return LV_OK;
 }
 
+lv_status lv_encode_timing(const lv_index* ix, float* ms) {
+  if (!ix || !ms) return fail(LV_EINVAL, "lv_encode_timing: bad arguments");
+  if (!ix->enc_timed) return fail(LV_EINVAL, "lv_encode_timing: no encode has run");
+  for (int i = 0; i < 3; ++i) ms[i] = ix->enc_ms[i];
+  return LV_OK;
+}
+
 lv_status lv_timing_collect(lv_index* ix, float* kernel_ms, int32_t* calls) {
   if (!ix || !kernel_ms) return fail(LV_EINVAL, "lv_timing_collect: bad arguments");
   double acc[8] = {0};
@@ -997,6 +1061,7 @@ void lv_index_destroy(lv_index* ix) {
   cudaFree(ix->A);
   cudaFree(ix->B);
   cudaFree(ix->A_planes);
+  cudaFree(ix->B_planes);
   for (auto& g : ix->ev_pending)
     for (auto e : g) cudaEventDestroy(e);
   for (auto e : ix->ev_pool) cudaEventDestroy(e);

@@ -196,4 +196,278 @@ cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a,
   return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// K6 encode on tcgen05 (Eq.(14) read with g; Eq.(5) g = B x):
+//   X_low[r, :] = RNE_low( B_{c(r)} X[perm[r], :] ) for the cluster-sorted rows r of one 128-row
+//   tile (the tile's cluster c(r) comes from the per-tile weight-row table).
+// Same precision contract as K1: X rows and B are split into three bf16 planes (24 significant
+// bits) and the six products above 2^-24 accumulate in fp32 TMEM (hh over up to three
+// accumulators).  X rows are gathered through perm, so TMA cannot load them: eight producer
+// warps (two per scheduler: one warp per SMSP could not issue the split fast enough) read each
+// row's 64-element K block with coalesced 16-byte loads, split it in registers and store the
+// planes in the SWIZZLE_128B K-major layout the MMA descriptor expects (16-byte chunk c of row r
+// at chunk c ^ (r & 7)); B planes come by TMA.  The same warps then round the accumulators and
+// store the tile.  One CTA per tile.
+constexpr int kEnPW = 8;                              // producer / epilogue warps
+constexpr int kEnRows = 128 / kEnPW;                  // tile rows per producer warp
+constexpr int kEnIt = kEnRows / 2;                    // two rows per warp-wide step
+constexpr int kEnThreads = 64 + 32 * kEnPW;
+
+__host__ __device__ constexpr int enc_hh(int d) { return (512 / d - 1) < 3 ? (512 / d - 1) : 3; }
+__host__ __device__ constexpr uint32_t enc_stage_bytes(int d) { return 3u * 128u * 128u + 3u * (uint32_t)d * 128u; }
+// two stages when they fit the 227 KB opt-in limit (d <= 160), else one
+__host__ __device__ constexpr int enc_stages(int d) { return 2 * enc_stage_bytes(d) + 1280 <= 232448 ? 2 : 1; }
+size_t encode_smem(int d) { return enc_stages(d) * enc_stage_bytes(d) + 1024 + 256; }
+
+template <bool kXF16, int kD, bool kOutBF16>
+__global__ void __launch_bounds__(kEnThreads, 1)
+    k_encode_tc(const __grid_constant__ CUtensorMap tmap_b, const void* __restrict__ X, int D, int Kp, int Nc, int vec,
+                const int32_t* __restrict__ perm, const int32_t* __restrict__ tile_wrow,
+                const int32_t* __restrict__ tile_order, void* __restrict__ out) {
+  constexpr int nH = enc_hh(kD);                    // hh accumulators (columns nH*d .. : cross terms)
+  constexpr uint32_t kXPlane = 128u * 128u;         // 128 rows x 64 bf16
+  constexpr uint32_t kBPlane = (uint32_t)kD * 128u; // d rows x 64 bf16
+  constexpr uint32_t kStage = enc_stage_bytes(kD);
+  constexpr int kEnStages = enc_stages(kD);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kEnStages * kStage);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kEnStages;
+  uint64_t* acc_full = bars + 2 * kEnStages;
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(acc_full + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = tile_order ? tile_order[blockIdx.x] : (int)blockIdx.x;
+  const int nkb = Kp / 64;
+  const int wrow = tile_wrow[2 * tile];             // c * d: first B row of the tile's cluster (per 64-row table)
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kEnStages; ++s) {
+      tc::mbar_init(full + s, 1 + kEnPW);           // TMA expect_tx arrive + the producer warps
+      tc::mbar_init(empty + s, 1);
+    }
+    tc::mbar_init(acc_full, 1);
+    tc::fence_barrier_init();
+    tc::tma_prefetch(&tmap_b);
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_ptr, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        tc::mbar_wait(empty + stage, phase ^ 1);
+        tc::mbar_arrive_expect_tx(full + stage, 3u * kBPlane);
+        uint8_t* st = smem + stage * kStage + 3u * kXPlane;
+        for (int p = 0; p < 3; ++p)
+          tc::tma_load_2d(st + p * kBPlane, &tmap_b, full + stage, kb * 64, p * Nc + wrow);
+        if (++stage == kEnStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = tc::make_idesc_f16(128, kD, true);
+    int stage = 0;
+    uint32_t phase = 0;
+    const bool issuer = tc::elect_one();
+    for (int kb = 0; kb < nkb; ++kb) {
+      tc::mbar_wait(full + stage, phase);
+      tc::tc_fence_after();
+      if (issuer) {
+        const uint32_t st = tc::smem_u32(smem + stage * kStage);
+        const uint32_t d_big = tmem + (uint32_t)(kb % nH) * (uint32_t)kD, d_small = tmem + (uint32_t)nH * (uint32_t)kD;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+#pragma unroll
+          for (int pr = 0; pr < 6; ++pr) {
+            const uint32_t xa = st + (uint32_t)kPjProd[pr][0] * kXPlane + (uint32_t)kk * 32u;
+            const uint32_t ba = st + 3u * kXPlane + (uint32_t)kPjProd[pr][1] * kBPlane + (uint32_t)kk * 32u;
+            if (pr == 0)
+              tc::mma_f16_ss(d_big, tc::make_sdesc(xa, 128), tc::make_sdesc(ba, 128), idesc, (kb >= nH || kk > 0) ? 1u : 0u);
+            else
+              tc::mma_f16_ss(d_small, tc::make_sdesc(xa, 128), tc::make_sdesc(ba, 128), idesc,
+                             (kb | kk | (pr - 1)) != 0 ? 1u : 0u);
+          }
+        }
+        tc::mma_commit(empty + stage);
+        if (kb + 1 == nkb) tc::mma_commit(acc_full);
+      }
+      __syncwarp();
+      if (++stage == kEnStages) { stage = 0; phase ^= 1; }
+    }
+  } else {
+    // producers: warp w (2..9) owns tile rows kEnRows*(w-2) ..; two rows per step (lanes 0-15 and
+    // 16-31), 4 consecutive elements per lane.  The loads of K block kb+1 are issued before the
+    // stage wait and the plane stores of block kb (register double buffer), so two blocks of row
+    // reads are in flight per warp and they overlap the MMAs.
+    const int pw = warp - 2;
+    const int half = lane >> 4, l16 = lane & 15;
+    int srcs[kEnIt];
+    {
+      const int my_src = perm[(size_t)tile * 128 + pw * kEnRows + (lane % kEnRows)];
+#pragma unroll
+      for (int it = 0; it < kEnIt; ++it) srcs[it] = __shfl_sync(0xffffffffu, my_src, 2 * it + half);
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    auto load_block = [&](float (&x)[kEnIt][4], int kb) {
+      const int k0 = kb * 64 + l16 * 4;
+#pragma unroll
+      for (int it = 0; it < kEnIt; ++it) {
+        const int src = srcs[it];
+        x[it][0] = x[it][1] = x[it][2] = x[it][3] = 0.f;
+        if (src >= 0) {
+          if (kXF16) {
+            const __half* row = reinterpret_cast<const __half*>(X) + (size_t)src * D;
+            if (vec && k0 + 3 < D) {
+              const uint2 u = __ldcs(reinterpret_cast<const uint2*>(row + k0));
+              const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+              const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+              x[it][0] = a.x; x[it][1] = a.y; x[it][2] = b.x; x[it][3] = b.y;
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (k0 + e < D) x[it][e] = __half2float(row[k0 + e]);
+            }
+          } else {
+            const float* row = reinterpret_cast<const float*>(X) + (size_t)src * D;
+            if (vec && k0 + 3 < D) {
+              const float4 f = __ldcs(reinterpret_cast<const float4*>(row + k0));
+              x[it][0] = f.x; x[it][1] = f.y; x[it][2] = f.z; x[it][3] = f.w;
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (k0 + e < D) x[it][e] = row[k0 + e];
+            }
+          }
+        }
+      }
+    };
+    auto store_block = [&](const float (&x)[kEnIt][4]) {
+      tc::mbar_wait(empty + stage, phase ^ 1);
+      uint8_t* st = smem + stage * kStage;
+#pragma unroll
+      for (int it = 0; it < kEnIt; ++it) {
+        const int r = pw * kEnRows + 2 * it + half;      // row in the tile
+        uint32_t hp[2], mp[2], lp[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float v0 = x[it][2 * e], v1 = x[it][2 * e + 1];
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(v0, v1);
+          const float2 hf = __bfloat1622float2(h2);
+          const float r0 = v0 - hf.x, r1 = v1 - hf.y;      // exact in fp32
+          const __nv_bfloat162 m2 = __floats2bfloat162_rn(r0, r1);
+          const float2 mf = __bfloat1622float2(m2);
+          const __nv_bfloat162 l2 = __floats2bfloat162_rn(r0 - mf.x, r1 - mf.y);
+          hp[e] = *reinterpret_cast<const uint32_t*>(&h2);
+          mp[e] = *reinterpret_cast<const uint32_t*>(&m2);
+          lp[e] = *reinterpret_cast<const uint32_t*>(&l2);
+        }
+        // SWIZZLE_128B: 16-byte chunk (l16 >> 1) of row r lands at chunk (l16 >> 1) ^ (r & 7)
+        const uint32_t off = (uint32_t)r * 128u + ((uint32_t)((l16 >> 1) ^ (r & 7)) << 4) + (uint32_t)(l16 & 1) * 8u;
+        *reinterpret_cast<uint2*>(st + off) = make_uint2(hp[0], hp[1]);
+        *reinterpret_cast<uint2*>(st + kXPlane + off) = make_uint2(mp[0], mp[1]);
+        *reinterpret_cast<uint2*>(st + 2u * kXPlane + off) = make_uint2(lp[0], lp[1]);
+      }
+      tc::fence_proxy_async();   // generic-proxy smem writes -> visible to the tensor core
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(full + stage);
+      if (++stage == kEnStages) { stage = 0; phase ^= 1; }
+    };
+    // two register buffers with fixed roles (unrolled by 2: no register copies of in-flight loads)
+    float xa[kEnIt][4], xb[kEnIt][4];
+    load_block(xa, 0);
+    for (int kb = 0; kb < nkb; kb += 2) {
+      if (kb + 1 < nkb) load_block(xb, kb + 1);
+      store_block(xa);
+      if (kb + 1 >= nkb) break;
+      if (kb + 2 < nkb) load_block(xa, kb + 2);
+      store_block(xb);
+    }
+    // epilogue: rows of TMEM lane quarter (warp % 4; the hardware ties warp w to lanes
+    // 32*(w%4)..), 32-column blocks split between the two warps of a quarter
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    constexpr int kCB = kD / 32, kCBh = (kCB + 1) / 2;
+    const int cb0 = pw < 4 ? 0 : kCBh, cb1 = pw < 4 ? kCBh : kCB;
+    tc::mbar_wait(acc_full, 0);
+    tc::tc_fence_after();
+    const int nbig = nkb < nH ? nkb : nH;
+#pragma unroll 1
+    for (int cb = cb0; cb < cb1; ++cb) {
+      float v[32], t[32];
+      const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb * 32u;
+      tc::tmem_ld_32x32b_x32(ta, v);
+      tc::tmem_wait_ld();
+      for (int b = 1; b < nbig; ++b) {
+        tc::tmem_ld_32x32b_x32(ta + (uint32_t)b * (uint32_t)kD, t);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += t[j];
+      }
+      tc::tmem_ld_32x32b_x32(ta + (uint32_t)nH * (uint32_t)kD, t);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] += t[j];
+      uint32_t w[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (kOutBF16) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+          w[j] = *reinterpret_cast<const uint32_t*>(&h2);
+        } else {
+          const __half2 h2 = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
+          w[j] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+      }
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(out) + ((size_t)tile * 128 + row) * kD + cb * 32);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+template <bool F, int D, bool O>
+static cudaError_t launch_enc_t(const CUtensorMap* tb, const void* X, int Dx, int Kp, int Nc, const int32_t* perm,
+                                const int32_t* tile_wrow, const int32_t* order, int64_t ntiles, void* out, cudaStream_t s) {
+  auto kern = k_encode_tc<F, D, O>;
+  const size_t smem = encode_smem(D);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int vec = ((Dx & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) ? 1 : 0;
+  kern<<<(unsigned)ntiles, kEnThreads, smem, s>>>(*tb, X, Dx, Kp, Nc, vec, perm, tile_wrow, order, out);
+  return cudaGetLastError();
+}
+
+template <bool F, bool O>
+static cudaError_t launch_enc_d(int d, const CUtensorMap* tb, const void* X, int Dx, int Kp, int Nc, const int32_t* perm,
+                                const int32_t* tile_wrow, const int32_t* order, int64_t ntiles, void* out, cudaStream_t s) {
+  switch (d) {
+    case 32: return launch_enc_t<F, 32, O>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    case 64: return launch_enc_t<F, 64, O>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    case 96: return launch_enc_t<F, 96, O>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    case 128: return launch_enc_t<F, 128, O>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    case 160: return launch_enc_t<F, 160, O>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    case 192: return launch_enc_t<F, 192, O>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_encode_tc(const CUtensorMap* tmap_b, const void* X, bool x_f16, int D, int Kp, int d, int Nc,
+                             const int32_t* perm, const int32_t* tile_wrow, const int32_t* order, int64_t ntiles,
+                             void* out, bool out_bf16, cudaStream_t s) {
+  if (x_f16) return out_bf16 ? launch_enc_d<true, true>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
+                             : launch_enc_d<true, false>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+  return out_bf16 ? launch_enc_d<false, true>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
+                  : launch_enc_d<false, false>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+}
+
 }  // namespace lv

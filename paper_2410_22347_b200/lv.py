@@ -20,7 +20,7 @@ _DT = {"fp32": LV_F32, "f32": LV_F32, "fp16": LV_F16, "f16": LV_F16, "bf16": LV_
 _TORCH_DT = {LV_F32: torch.float32, LV_F16: torch.float16, LV_BF16: torch.bfloat16}
 
 EXPORTS = ["lv_last_error", "lv_version", "lv_fit_stats", "lv_index_create", "lv_encode_database",
-           "lv_project_queries", "lv_search", "lv_search_host", "lv_timing_collect", "lv_assign_tags",
+           "lv_project_queries", "lv_search", "lv_search_host", "lv_timing_collect", "lv_encode_timing", "lv_assign_tags",
            "lv_index_info", "lv_index_export", "lv_index_destroy"]
 
 
@@ -59,6 +59,7 @@ def lib():
             "lv_search": [vp, vp, i64, i32, i32, vp, vp, ctypes.POINTER(SearchDebug), vp],
             "lv_search_host": [vp, vp, i64, i32, i32, vp, vp, vp],
             "lv_timing_collect": [vp, vp, ctypes.POINTER(i32)],
+            "lv_encode_timing": [vp, vp],
             "lv_assign_tags": [vp, i32, i64, i32, vp, i32, vp, vp],
             "lv_index_info": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32),
                               ctypes.POINTER(i32), ctypes.POINTER(i32)],
@@ -205,6 +206,13 @@ def lv_timing_collect(index: Index):
     calls = ctypes.c_int32()
     _check(lib().lv_timing_collect(index.h, ms, ctypes.byref(calls)), "lv_timing_collect")
     return dict(zip(KERNEL_PHASES, list(ms))), calls.value
+
+
+def lv_encode_timing(index: Index):
+    """Kernel times (ms) of the last lv_encode_database: sort (C > 1), K6 encode, full copy."""
+    ms = (ctypes.c_float * 3)()
+    _check(lib().lv_encode_timing(index.h, ms), "lv_encode_timing")
+    return dict(zip(["sort", "encode_K6", "full_copy"], list(ms)))
 
 
 def lv_search_host(index: Index, Q_host: torch.Tensor, k: int, R: int, ids_host=None, scores_host=None):

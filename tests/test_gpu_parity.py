@@ -121,6 +121,39 @@ def test_g1_encode_project_and_raw_scores(lv, d):
     assert (np.abs(raw - ref) <= flip).all()
 
 
+@pytest.mark.parametrize("D,d,C,xdt,low", [(200, 64, 1, "f32", "fp16"), (132, 32, 1, "f32", "bf16"),
+                                           (96, 96, 3, "f16", "bf16"), (768, 160, 2, "f32", "bf16"),
+                                           (512, 128, 1, "f16", "fp16"), (256, 192, 1, "f32", "bf16")])
+def test_g1_encode_shapes(lv, D, d, C, xdt, low):
+    """K6 (tensor-core encode) G1 across the shapes its layout depends on: ragged D (a partial last
+    64-wide K block), fp16 input rows, several clusters (per-tile B
+    rows, padded tiles), every d tile width.  x_low within 1 storage ulp + the fp32
+    accumulation bound of the oracle's fp64 B_c x, flips < 0.5 %."""
+    rng = np.random.default_rng(D * 7 + d)
+    n = 3000
+    X = rng.standard_normal((n, D)).astype(np.float32)
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    if xdt == "f16":
+        X = X.astype(np.float16)
+    B = (rng.standard_normal((C, d, D)) / np.sqrt(D)).astype(np.float32)
+    A = (rng.standard_normal((C, d, D)) / np.sqrt(D)).astype(np.float32)
+    assign = rng.integers(0, C, n).astype(np.int32)
+    ix = lv.lv_index_create(D, d, C, low, "fp32", torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    lv.lv_encode_database(ix, torch.from_numpy(X).cuda(), torch.from_numpy(assign).cuda() if C > 1 else None)
+    X_low, perm, offs = lv.lv_index_export(ix)
+    perm = perm.cpu().numpy()
+    valid = perm >= 0
+    X64 = X.astype(np.float64)
+    a = assign if C > 1 else None
+    B1 = B if C > 1 else B[0]
+    xl_ref = O.encode(X64, B1, a, store=low)[perm[valid]]
+    absdot = O.encode(np.abs(X64), np.abs(B1), a)[perm[valid]]
+    got = X_low.float().cpu().numpy().astype(np.float64)
+    ok, flips = _g1_ok(got[valid], xl_ref, absdot, low, D)
+    assert ok and flips < 5e-3, flips
+    assert np.all(got[~valid] == 0)            # padded rows of a cluster's last tile encode to 0
+
+
 @pytest.mark.parametrize("d,low", [(32, "bf16"), (64, "bf16"), (96, "bf16"), (128, "fp16"), (160, "bf16"),
                                    (64, "fp16")])
 def test_mma_exact_operands(lv, d, low):
