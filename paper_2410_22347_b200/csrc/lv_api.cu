@@ -23,6 +23,7 @@ struct Plan {
   int m_pad, QP, NS, Cap, grid, stages;
   size_t smem;
   bool sampled = false;       // sampled-threshold path (else: staged path)
+  bool fine_blocks = false;   // sample stage records 32-row (not 64-row) block maxima
   int stride = 1, nblk = 0, j1 = 0, j2 = 0;
   std::vector<std::vector<int32_t>> chunks;   // staged: one list per stage; sampled: {sample, main}
   std::vector<int32_t> repair_chunks;         // sampled: full database, planned for one query tile
@@ -316,11 +317,16 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
     const double z = env_double("LV_SAMPLE_Z", 2.9);
     while ((double)j1 * stride - z * std::sqrt((double)j1) * stride < (double)R) ++j1;
   }
-  const int bpt = lv::score_blocks_per_tile(ix->d);   // block maxima per sampled tile
+  // 32-row sample blocks while the block-maximum array stays small (<= 8192 blocks); coarser
+  // 64-row blocks at the 10M-row sizes, where the array's HBM traffic would cost more than the
+  // tighter threshold saves
+  const bool fine = (int64_t)lv::score_blocks_per_tile(ix->d, true) * nsamp <= 8192;
+  const int bpt = lv::score_blocks_per_tile(ix->d, fine);   // block maxima per sampled tile
   pl->sampled = env_double("LV_SAMPLED", 1.0) != 0.0 && stride >= 2 && nsamp >= 64 && bpt * nsamp >= 8 * j1 &&
                 bpt * nsamp <= 65535;
   if (pl->sampled) {
     pl->stride = stride;
+    pl->fine_blocks = fine;
     pl->nblk = bpt * nsamp;
     pl->j1 = std::max(4, j1);
     pl->j2 = std::min(pl->nblk, 4 * pl->j1);
@@ -888,8 +894,11 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     // above it; (3) one main stage with that threshold; (4) exactness check in the re-rank;
     // (5) repair of the failed queries with the looser j2 threshold, then with none
     sa.bmax = pc.bmax;
+    const int flags0 = sa.flags;
+    if (pl.fine_blocks) sa.flags |= 8;
     st = scan(chunk_info[0], pl.chunks[0], pl.QP, "sample");
     if (st) return st;
+    sa.flags = flags0;
     sa.bmax = nullptr;
     if ((st = mark(2))) return st;
     LV_CUDA(lv::launch_bmax_select(pc.bmax, pl.nblk, (int)m, pl.m_pad, pl.j1, pl.j2, pc.tau, pc.cnt, NS2, pc.tau2, s));

@@ -48,7 +48,7 @@ struct ScoreArgs {
 cudaError_t launch_score(const CUtensorMap* tmap_xlow, const ScoreArgs& a, bool bf16, int grid, size_t smem,
                          cudaStream_t s);
 int score_tile_rows(int d);
-int score_blocks_per_tile(int d);   // sample stage: block maxima recorded per tile and query
+int score_blocks_per_tile(int d, bool fine);   // sample stage: block maxima per tile and query (fine: 32-row blocks)
 
 struct RerankArgs {
   int m, m_pad, D, R, k, NS, Cap;

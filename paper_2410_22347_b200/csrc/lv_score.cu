@@ -252,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool skip_topr = (a.flags & 1) != 0;
   const bool count_stats = (a.flags & 2) != 0 && a.stats != nullptr;
   const bool fast_only = (a.flags & 4) != 0;   // debug: detect hits but drop them (fast-path cost probe)
+  const bool fine_blocks = (a.flags & 8) != 0;  // sample stage: 32-row block maxima
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
@@ -487,11 +488,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
           if (kSample) {
-            // sample stage: record the block maximum (query q, the job's kJobCols database rows);
-            // no top-R here
-            bm = fmaxf(bm, mx);
-            if (h + 1 == kJV)
-              a.bmax[(size_t)((sbase + (t - t0) / tstride) * kJobsPerTile + jh) * a.m_pad + q] = bm;
+            // sample stage: record block maxima (query q; blocks of 32 database rows when
+            // a.flags & 8, else of the job's 64: fine blocks keep the threshold estimate of
+            // DESIGN.md §5 tight when top rows cluster); no top-R here
+            const int sblk = (sbase + (t - t0) / tstride) * kJobsPerTile + jh;
+            if (fine_blocks) {
+              a.bmax[(size_t)(sblk * kJV + h) * a.m_pad + q] = mx;
+            } else {
+              bm = fmaxf(bm, mx);
+              if (h + 1 == kJV) a.bmax[(size_t)sblk * a.m_pad + q] = bm;
+            }
             continue;
           }
           const bool hit = mx >= ts && mx > -FLT_MAX;
@@ -596,15 +602,8 @@ cudaError_t launch_score(const CUtensorMap* tmap_xlow, const ScoreArgs& a, bool 
 }
 
 int score_tile_rows(int d) { return score_tile_n(d); }
-int score_blocks_per_tile(int d) {   // block maxima per sampled tile (one per epilogue job)
-  switch (d) {
-    case 32: return 128 / job_cols(32);
-    case 64: return 128 / job_cols(64);
-    case 96: return 128 / job_cols(96);
-    case 128: return 128 / job_cols(128);
-    case 160: return 128 / job_cols(160);
-    default: return 128 / job_cols(192);
-  }
+int score_blocks_per_tile(int d, bool fine) {   // block maxima per sampled tile
+  return fine ? kTileN / 32 : kTileN / job_cols(d);
 }
 
 }  // namespace lv

@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblv.so")
+LIB_PATH = os.environ.get("LV_LIB") or os.path.join(HERE, "liblv.so")   # LV_LIB: experiment builds
 
 LV_F32, LV_F16, LV_BF16 = 0, 1, 2
 _DT = {"fp32": LV_F32, "f32": LV_F32, "fp16": LV_F16, "f16": LV_F16, "bf16": LV_BF16}
