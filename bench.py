@@ -100,7 +100,7 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_index(cfg, rank=0, world=1, log=print):
+def build_index(cfg, rank=0, world=1, log=print, family=None):
     """Generate the config's data, fit with the product path (lv_fit_stats + host eig, GPU k-means
     for GleanVec), encode.  Returns dict with index, device Q, host Q, data."""
     import torch
@@ -109,8 +109,8 @@ def build_index(cfg, rank=0, world=1, log=print):
     t0 = time.time()
     X = lvgen.database(cfg)
     lo, hi = shard_queries(cfg.m_test, rank, world)
-    Q = lvgen.queries(cfg, "test", m=hi)[lo:hi]
-    Ql = lvgen.queries(cfg, "learn")
+    Q = lvgen.queries(cfg, "test", family=family, m=hi)[lo:hi]
+    Ql = lvgen.queries(cfg, "learn", family=family)
     lr = lvgen.learn_rows(cfg)
     log(f"[bench] generated n={cfg.n} D={cfg.D} in {time.time() - t0:.1f}s")
     t0 = time.time()
@@ -176,18 +176,19 @@ def roofline_rerank(cfg, ms, m):
             "dram_frac": round(traffic / (ms * 1e-3) / 1e9 / pk["hbm"], 4) if traffic else None}
 
 
-def roofline_encode(cfg, k6_ms, n_pad):
+def roofline_encode(cfg, k6_ms, n_pad, x_bytes):
     """K6 encode X_low = RNE(B_c x) over the whole database (index build, outside the search step):
-    every fp32 row read once, every d-wide storage row written once, the permutation read once.
+    every database row read once (fp32, cfg 5 fp16), every d-wide storage row written once, the
+    permutation read once.
     Tensor work 6 plane products x 2 n d D flop (three-plane bf16 split, lv_proj.cu)."""
     pk = _peaks()
-    byts = cfg.n * cfg.D * 4 + n_pad * cfg.d * 2 + n_pad * 4
+    byts = cfg.n * cfg.D * x_bytes + n_pad * cfg.d * 2 + n_pad * 4
     ach = byts / (k6_ms * 1e-3) / 1e9
     tf = 6 * 2.0 * cfg.n * cfg.d * cfg.D / (k6_ms * 1e-3) / 1e12
     return {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s", "frac": round(ach / pk["hbm"], 4),
             "tensor_tflops": round(tf, 1), "tensor_frac": round(tf / pk["bf16"], 4),
             "kernel": "k_encode_tc (K6, one launch)", "launch_ms": round(k6_ms, 4),
-            "algorithmic": f"{byts:.3e} B per launch (n D 4 + n_pad d 2 + n_pad 4)"}
+            "algorithmic": f"{byts:.3e} B per launch (n D {x_bytes} + n_pad d 2 + n_pad 4)"}
 
 
 def _ncu_traffic(cfg_id):
@@ -253,6 +254,7 @@ def main():
     ap.add_argument("--impl", default="lv", choices=["lv", "reference"])
     ap.add_argument("--oracle-queries", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--family", default=None, help="query family (cfg 4: ood (default) or id; one fit + encode each)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -263,7 +265,8 @@ def main():
 
     import lvgen
     cfg = lvgen.get_config(args.config)
-    workload = f"cfg{cfg.cfg_id} {cfg.name}"
+    family = args.family or cfg.families[-1]
+    workload = f"cfg{cfg.cfg_id} {cfg.name}" + (f" [{family} queries]" if len(cfg.families) > 1 else "")
     conf = {"workload": workload, "n": cfg.n, "D": cfg.D, "d": cfg.d, "C": cfg.C, "m": cfg.m_test, "R": cfg.R,
             "k": cfg.k, "low_dtype": cfg.low_dtype, "full_dtype": cfg.full_dtype,
             "l2": "no flush: X_low and X exceed the 126 MB L2 and are streamed every step"}
@@ -273,8 +276,8 @@ def main():
             return
         import oracle as O
         X = lvgen.database(cfg)
-        Q = lvgen.queries(cfg, "test")
-        Ql = lvgen.queries(cfg, "learn")
+        Q = lvgen.queries(cfg, "test", family=family)
+        Ql = lvgen.queries(cfg, "learn", family=family)
         Xl = X[lvgen.learn_rows(cfg)]
         if cfg.C == 1:
             f = O.sphering_fit(Ql, Xl, cfg.d)
@@ -319,7 +322,7 @@ def main():
         dist.init_process_group("nccl")
     from paper_2410_22347_b200 import lv
 
-    data = build_index(cfg, rank=rank, world=world, log=log)
+    data = build_index(cfg, rank=rank, world=world, log=log, family=family)
     ix, Qd = data["ix"], data["Qd"]
     m = Qd.shape[0]
     ids = torch.empty((m, cfg.k), dtype=torch.int32, device="cuda")
@@ -386,7 +389,7 @@ def main():
            "clocks": clk.summary(),
            "index_build": {"fit_s": round(data["fit_s"], 2), "encode_ms": round(data["encode_ms"], 2),
                            "encode_kernels_ms": {k: round(v, 4) for k, v in data["encode_kernels"].items()},
-                           "roofline_encode": roofline_encode(cfg, data["encode_kernels"]["encode_K6"], data["n_pad"])}}
+                           "roofline_encode": roofline_encode(cfg, data["encode_kernels"]["encode_K6"], data["n_pad"], data["X"].dtype.itemsize)}}
     if world == 1 and not args.no_cpu_baseline:
         import oracle as O
         nq = min(args.oracle_queries, m)

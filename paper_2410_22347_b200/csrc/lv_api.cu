@@ -348,7 +348,7 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   pl->NS = ns;
   pl->grid = (int)std::min<int64_t>(G, (int64_t)pmax * pl->QP);
   const size_t budget = 227 * 1024 - 1024 - 256;
-  int st = 8;
+  int st = std::max(2, std::min(8, (int)env_double("LV_STAGES", 8.0)));   // LV_STAGES: probe knob
   while (st >= 2 && lv::score_smem_bytes(ix->d, st) > budget) --st;
   if (st < 2) return fail(LV_EUNSUPPORTED, "d=%d leaves no room for a 2-stage pipeline", ix->d);
   pl->stages = st;
@@ -637,7 +637,7 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
   LV_CUDA(cudaEventRecord(ev[1], s));
   if (k6_tensor())
     LV_CUDA(lv::launch_encode_tc(&ix->tmap_b, X, x_dtype == LV_F16, ix->D, ix->Kp, ix->d, ix->C * ix->d, ix->perm, dwrow,
-                                 dorder, nt, ix->X_low, ix->low == LV_BF16, s));
+                                 dorder, nt, ix->X_low, ix->low == LV_BF16, env_double("LV_K6_PLANES", 3.0) >= 3.0, s));
   else
     LV_CUDA(lv::launch_rows_gemm(X, x_dtype == LV_F16, ix->D, ix->perm, n, ix->n_pad, ix->B, ix->D, dwrow, ix->d,
                                  ix->X_low, ix->low, ix->d, ix->n_pad, s));

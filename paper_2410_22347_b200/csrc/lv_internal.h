@@ -90,10 +90,11 @@ cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a,
                            int64_t ld_out, int rows_store, bool out_bf16, cudaStream_t s);
 // K6 on tensor cores: out[r, :] = RNE(B_{c(r)} X[perm[r], :]) for 128-row tiles (tile_wrow[2t] = c*d),
 // CTA i encodes tile order[i] (nullptr: tile i)
-size_t encode_smem(int d);
+// (three bf16 planes; two for bf16 storage when !planes3)
+size_t encode_smem(int d, int np);
 cudaError_t launch_encode_tc(const CUtensorMap* tmap_b, const void* X, bool x_f16, int D, int Kp, int d, int Nc,
                              const int32_t* perm, const int32_t* tile_wrow, const int32_t* order, int64_t ntiles,
-                             void* out, bool out_bf16, cudaStream_t s);
+                             void* out, bool out_bf16, bool planes3, cudaStream_t s);
 cudaError_t launch_iota_perm(int32_t* perm, int64_t n, int64_t n_pad, cudaStream_t s);
 
 cudaError_t launch_stats(const void* in, int in_f16, int64_t ld, const int32_t* rowidx, int nchunks,

@@ -201,26 +201,35 @@ cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a,
 // K6 encode on tcgen05 (Eq.(14) read with g; Eq.(5) g = B x):
 //   X_low[r, :] = RNE_low( B_{c(r)} X[perm[r], :] ) for the cluster-sorted rows r of one 128-row
 //   tile (the tile's cluster c(r) comes from the per-tile weight-row table).
-// Same precision contract as K1: X rows and B are split into three bf16 planes (24 significant
-// bits) and the six products above 2^-24 accumulate in fp32 TMEM (hh over up to three
-// accumulators).  X rows are gathered through perm, so TMA cannot load them: eight producer
-// warps (two per scheduler: one warp per SMSP could not issue the split fast enough) read each
-// row's 64-element K block with coalesced 16-byte loads, split it in registers and store the
-// planes in the SWIZZLE_128B K-major layout the MMA descriptor expects (16-byte chunk c of row r
-// at chunk c ^ (r & 7)); B planes come by TMA.  The same warps then round the accumulators and
-// store the tile.  One CTA per tile.
+// Precision contract (R18): for fp16 storage as K1 (X rows and B split into three bf16
+// planes, 24 significant bits, the six products above 2^-24 in fp32 TMEM, hh over up to three
+// accumulators); an opt-in two-plane variant for bf16 storage halves the tensor work.
+// X rows are gathered through perm, so TMA cannot load them: eight producer warps (two per
+// scheduler: one warp per SMSP could not issue the split fast enough) read each row's 64-element
+// K block with coalesced 16-byte loads, split it in registers and store the planes in the
+// SWIZZLE_128B K-major layout the MMA descriptor expects (16-byte chunk c of row r at chunk
+// c ^ (r & 7)); B planes come by TMA.  The same warps then round the accumulators and store the
+// tile.  One CTA per tile.
 constexpr int kEnPW = 8;                              // producer / epilogue warps
 constexpr int kEnRows = 128 / kEnPW;                  // tile rows per producer warp
 constexpr int kEnIt = kEnRows / 2;                    // two rows per warp-wide step
 constexpr int kEnThreads = 64 + 32 * kEnPW;
 
 __host__ __device__ constexpr int enc_hh(int d) { return (512 / d - 1) < 3 ? (512 / d - 1) : 3; }
-__host__ __device__ constexpr uint32_t enc_stage_bytes(int d) { return 3u * 128u * 128u + 3u * (uint32_t)d * 128u; }
-// two stages when they fit the 227 KB opt-in limit (d <= 160), else one
-__host__ __device__ constexpr int enc_stages(int d) { return 2 * enc_stage_bytes(d) + 1280 <= 232448 ? 2 : 1; }
-size_t encode_smem(int d) { return enc_stages(d) * enc_stage_bytes(d) + 1024 + 256; }
+// np planes of the X tile and of the B block per stage
+__host__ __device__ constexpr uint32_t enc_stage_bytes(int d, int np) {
+  return (uint32_t)np * (128u * 128u + (uint32_t)d * 128u);
+}
+// as many stages (<= 3) as fit the 227 KB opt-in limit
+__host__ __device__ constexpr int enc_stages(int d, int np) {
+  return 3 * enc_stage_bytes(d, np) + 1280 <= 232448 ? 3 : (2 * enc_stage_bytes(d, np) + 1280 <= 232448 ? 2 : 1);
+}
+size_t encode_smem(int d, int np) { return enc_stages(d, np) * enc_stage_bytes(d, np) + 1024 + 256; }
 
-template <bool kXF16, int kD, bool kOutBF16>
+// kNP = 3: v = h + m + l, six products (the default); kNP = 2: v = h + m (16 significant bits),
+// products hh, hm, mh, bf16 storage only, opt-in (LV_K6_PLANES=2): the dropped terms are
+// <= 2^-18 sum|b x| and flip 0.34 % of the bf16 outputs (three planes: 0.015 %; R18).
+template <bool kXF16, int kD, bool kOutBF16, int kNP>
 __global__ void __launch_bounds__(kEnThreads, 1)
     k_encode_tc(const __grid_constant__ CUtensorMap tmap_b, const void* __restrict__ X, int D, int Kp, int Nc, int vec,
                 const int32_t* __restrict__ perm, const int32_t* __restrict__ tile_wrow,
@@ -228,8 +237,9 @@ __global__ void __launch_bounds__(kEnThreads, 1)
   constexpr int nH = enc_hh(kD);                    // hh accumulators (columns nH*d .. : cross terms)
   constexpr uint32_t kXPlane = 128u * 128u;         // 128 rows x 64 bf16
   constexpr uint32_t kBPlane = (uint32_t)kD * 128u; // d rows x 64 bf16
-  constexpr uint32_t kStage = enc_stage_bytes(kD);
-  constexpr int kEnStages = enc_stages(kD);
+  constexpr uint32_t kStage = enc_stage_bytes(kD, kNP);
+  constexpr int kEnStages = enc_stages(kD, kNP);
+  constexpr int kProds = kNP == 3 ? 6 : 3;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kEnStages * kStage);
@@ -263,9 +273,9 @@ __global__ void __launch_bounds__(kEnThreads, 1)
       uint32_t phase = 0;
       for (int kb = 0; kb < nkb; ++kb) {
         tc::mbar_wait(empty + stage, phase ^ 1);
-        tc::mbar_arrive_expect_tx(full + stage, 3u * kBPlane);
-        uint8_t* st = smem + stage * kStage + 3u * kXPlane;
-        for (int p = 0; p < 3; ++p)
+        tc::mbar_arrive_expect_tx(full + stage, (uint32_t)kNP * kBPlane);
+        uint8_t* st = smem + stage * kStage + (uint32_t)kNP * kXPlane;
+        for (int p = 0; p < kNP; ++p)
           tc::tma_load_2d(st + p * kBPlane, &tmap_b, full + stage, kb * 64, p * Nc + wrow);
         if (++stage == kEnStages) { stage = 0; phase ^= 1; }
       }
@@ -284,9 +294,9 @@ __global__ void __launch_bounds__(kEnThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
 #pragma unroll
-          for (int pr = 0; pr < 6; ++pr) {
+          for (int pr = 0; pr < kProds; ++pr) {
             const uint32_t xa = st + (uint32_t)kPjProd[pr][0] * kXPlane + (uint32_t)kk * 32u;
-            const uint32_t ba = st + 3u * kXPlane + (uint32_t)kPjProd[pr][1] * kBPlane + (uint32_t)kk * 32u;
+            const uint32_t ba = st + (uint32_t)kNP * kXPlane + (uint32_t)kPjProd[pr][1] * kBPlane + (uint32_t)kk * 32u;
             if (pr == 0)
               tc::mma_f16_ss(d_big, tc::make_sdesc(xa, 128), tc::make_sdesc(ba, 128), idesc, (kb >= nH || kk > 0) ? 1u : 0u);
             else
@@ -372,7 +382,7 @@ __global__ void __launch_bounds__(kEnThreads, 1)
         const uint32_t off = (uint32_t)r * 128u + ((uint32_t)((l16 >> 1) ^ (r & 7)) << 4) + (uint32_t)(l16 & 1) * 8u;
         *reinterpret_cast<uint2*>(st + off) = make_uint2(hp[0], hp[1]);
         *reinterpret_cast<uint2*>(st + kXPlane + off) = make_uint2(mp[0], mp[1]);
-        *reinterpret_cast<uint2*>(st + 2u * kXPlane + off) = make_uint2(lp[0], lp[1]);
+        if (kNP == 3) *reinterpret_cast<uint2*>(st + 2u * kXPlane + off) = make_uint2(lp[0], lp[1]);
       }
       tc::fence_proxy_async();   // generic-proxy smem writes -> visible to the tensor core
       __syncwarp();
@@ -435,11 +445,11 @@ __global__ void __launch_bounds__(kEnThreads, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-template <bool F, int D, bool O>
+template <bool F, int D, bool O, int NP>
 static cudaError_t launch_enc_t(const CUtensorMap* tb, const void* X, int Dx, int Kp, int Nc, const int32_t* perm,
                                 const int32_t* tile_wrow, const int32_t* order, int64_t ntiles, void* out, cudaStream_t s) {
-  auto kern = k_encode_tc<F, D, O>;
-  const size_t smem = encode_smem(D);
+  auto kern = k_encode_tc<F, D, O, NP>;
+  const size_t smem = encode_smem(D, NP);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int vec = ((Dx & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) ? 1 : 0;
@@ -447,27 +457,32 @@ static cudaError_t launch_enc_t(const CUtensorMap* tb, const void* X, int Dx, in
   return cudaGetLastError();
 }
 
-template <bool F, bool O>
+template <bool F, bool O, int NP>
 static cudaError_t launch_enc_d(int d, const CUtensorMap* tb, const void* X, int Dx, int Kp, int Nc, const int32_t* perm,
                                 const int32_t* tile_wrow, const int32_t* order, int64_t ntiles, void* out, cudaStream_t s) {
   switch (d) {
-    case 32: return launch_enc_t<F, 32, O>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
-    case 64: return launch_enc_t<F, 64, O>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
-    case 96: return launch_enc_t<F, 96, O>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
-    case 128: return launch_enc_t<F, 128, O>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
-    case 160: return launch_enc_t<F, 160, O>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
-    case 192: return launch_enc_t<F, 192, O>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    case 32: return launch_enc_t<F, 32, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    case 64: return launch_enc_t<F, 64, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    case 96: return launch_enc_t<F, 96, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    case 128: return launch_enc_t<F, 128, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    case 160: return launch_enc_t<F, 160, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    case 192: return launch_enc_t<F, 192, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
+// three planes (six products); two planes (three products) for bf16 storage when !planes3
 cudaError_t launch_encode_tc(const CUtensorMap* tmap_b, const void* X, bool x_f16, int D, int Kp, int d, int Nc,
                              const int32_t* perm, const int32_t* tile_wrow, const int32_t* order, int64_t ntiles,
-                             void* out, bool out_bf16, cudaStream_t s) {
-  if (x_f16) return out_bf16 ? launch_enc_d<true, true>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
-                             : launch_enc_d<true, false>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
-  return out_bf16 ? launch_enc_d<false, true>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
-                  : launch_enc_d<false, false>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+                             void* out, bool out_bf16, bool planes3, cudaStream_t s) {
+  if (!out_bf16)
+    return x_f16 ? launch_enc_d<true, false, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
+                 : launch_enc_d<false, false, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+  if (planes3)
+    return x_f16 ? launch_enc_d<true, true, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
+                 : launch_enc_d<false, true, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+  return x_f16 ? launch_enc_d<true, true, 2>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
+               : launch_enc_d<false, true, 2>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
 }
 
 }  // namespace lv

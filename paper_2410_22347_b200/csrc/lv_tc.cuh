@@ -251,70 +251,6 @@ LV_TC_INL void tmem_ld_32x32b_x16(uint32_t taddr, float (&v)[16]) {
 LV_TC_INL void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 
-// ------------------------------------------------------------------ CTA pair (cta_group::2)
-LV_TC_INL uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-// shared::cluster address of the variable at local shared address `a` in CTA `rank` of the cluster
-LV_TC_INL uint32_t mapa_shared(uint32_t a, uint32_t rank) {
-  uint32_t d;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(rank));
-  return d;
-}
-LV_TC_INL void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// arrive on an mbarrier of another CTA of the cluster (shared::cluster address)
-LV_TC_INL void mbar_arrive_remote_relaxed(uint32_t cl_addr) {
-  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
-}
-LV_TC_INL void mbar_arrive_remote_release(uint32_t cl_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
-}
-LV_TC_INL void tmem_alloc_pair(uint32_t* smem_result, uint32_t ncols) {
-  // executed by one full warp in each CTA of the pair
-  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_result)),
-               "r"(ncols)
-               : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-}
-LV_TC_INL void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
-  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
-}
-// 2D TMA load into this CTA's smem whose completion is counted on the pair leader's mbarrier
-// (cl_bar: shared::cluster address)
-LV_TC_INL void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map, uint32_t cl_bar, int32_t c0, int32_t c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(cl_bar), "r"(c0), "r"(c1)
-      : "memory");
-}
-// D[tmem] (+)= A[tmem] * B[smem]^T with the CTA pair: M = 256 (128 rows per CTA, A and D in each
-// CTA's TMEM at the same address), B split by N between the two CTAs' smem (same offset).
-// Whole-warp variant, one elected lane issues.
-LV_TC_INL void mma_f16_ts_pair_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
-                                     uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t.reg .b32 rl;\n\t"
-      "elect.sync rl|e, 0xffffffff;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// commit: arrive once on the mbarrier at this smem offset in every CTA of ctaMask
-LV_TC_INL void mma_commit_pair_elect(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t.reg .b32 rl;\n\telect.sync rl|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-
 LV_TC_INL void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -124,11 +124,12 @@ def test_g1_encode_project_and_raw_scores(lv, d):
 @pytest.mark.parametrize("D,d,C,xdt,low", [(200, 64, 1, "f32", "fp16"), (132, 32, 1, "f32", "bf16"),
                                            (96, 96, 3, "f16", "bf16"), (768, 160, 2, "f32", "bf16"),
                                            (512, 128, 1, "f16", "fp16"), (256, 192, 1, "f32", "bf16")])
-def test_g1_encode_shapes(lv, D, d, C, xdt, low):
+def test_g1_encode_shapes(lv, D, d, C, xdt, low, monkeypatch, planes="3"):
     """K6 (tensor-core encode) G1 across the shapes its layout depends on: ragged D (a partial last
     64-wide K block), fp16 input rows, several clusters (per-tile B
     rows, padded tiles), every d tile width.  x_low within 1 storage ulp + the fp32
     accumulation bound of the oracle's fp64 B_c x, flips < 0.5 %."""
+    monkeypatch.setenv("LV_K6_PLANES", planes)   # "2": the opt-in two-plane split (bf16 storage, R18)
     rng = np.random.default_rng(D * 7 + d)
     n = 3000
     X = rng.standard_normal((n, D)).astype(np.float32)
@@ -149,9 +150,21 @@ def test_g1_encode_shapes(lv, D, d, C, xdt, low):
     xl_ref = O.encode(X64, B1, a, store=low)[perm[valid]]
     absdot = O.encode(np.abs(X64), np.abs(B1), a)[perm[valid]]
     got = X_low.float().cpu().numpy().astype(np.float64)
-    ok, flips = _g1_ok(got[valid], xl_ref, absdot, low, D)
-    assert ok and flips < 5e-3, flips
+    if planes == "3":
+        ok, flips = _g1_ok(got[valid], xl_ref, absdot, low, D)
+        assert ok and flips < 5e-3, flips
+    else:
+        # two planes: 16 significant bits per operand, dropped terms <= 3 * 2^-18 sum|b x| (R18), on
+        # top of the fp32 accumulation bound D 2^-24 sum|b x| of _g1_ok
+        ok, flips = _g1_ok(got[valid], xl_ref, absdot * (1.0 + 3 * 2.0 ** -18 / 2.0 ** -24 / D), low, D)
+        assert ok and flips < 1e-2, flips
     assert np.all(got[~valid] == 0)            # padded rows of a cluster's last tile encode to 0
+
+
+@pytest.mark.parametrize("D,d,C", [(768, 160, 2), (200, 64, 1), (512, 128, 1)])
+def test_g1_encode_two_planes_bf16(lv, D, d, C, monkeypatch):
+    """The opt-in two-plane encode (LV_K6_PLANES=2, bf16 storage) within its own bound (R18)."""
+    test_g1_encode_shapes(lv, D, d, C, "f32", "bf16", monkeypatch, planes="2")
 
 
 @pytest.mark.parametrize("d,low", [(32, "bf16"), (64, "bf16"), (96, "bf16"), (128, "fp16"), (160, "bf16"),

@@ -93,11 +93,13 @@ def main():
     ap.add_argument("--rep")
     ap.add_argument("--launches")
     ap.add_argument("--tag", default="r01")
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles"), help="output directory (on a GPU box: under gpurun_out/)")
     a = ap.parse_args()
-    prof = os.path.join(ROOT, "profiles")
+    prof = a.out
     os.makedirs(prof, exist_ok=True)
     traffic_path = os.path.join(prof, "ncu_traffic.json")
-    traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    seed = traffic_path if os.path.exists(traffic_path) else os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    traffic = json.load(open(seed)) if os.path.exists(seed) else {}
     t = traffic.setdefault(f"cfg{a.cfg}", {})
     if a.rep:
         ks = summarize_rep(a.rep)

@@ -20,9 +20,12 @@ def main():
     ap.add_argument("--C", type=int, default=1)
     ap.add_argument("--low", default="bf16")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--xf16", action="store_true", help="fp16 database rows (cfg 5's canonical type)")
     a = ap.parse_args()
     g = torch.Generator(device="cuda").manual_seed(0)
     X = torch.randn(a.n, a.D, device="cuda", generator=g)
+    if a.xf16:
+        X = X.half()
     A = torch.randn(a.C, a.d, a.D, device="cuda", generator=g) / a.D ** 0.5
     B = torch.randn(a.C, a.d, a.D, device="cuda", generator=g) / a.D ** 0.5
     assign = torch.randint(0, a.C, (a.n,), device="cuda", dtype=torch.int32, generator=g) if a.C > 1 else None
@@ -31,7 +34,7 @@ def main():
         lv.lv_encode_database(ix, X, assign)
         t = lv.lv_encode_timing(ix)
         n_pad = ix.info()["n_pad"]
-        gbs = (a.n * a.D * 4 + n_pad * a.d * 2 + n_pad * 4) / (t["encode_K6"] * 1e-3) / 1e9
+        gbs = (a.n * a.D * X.element_size() + n_pad * a.d * 2 + n_pad * 4) / (t["encode_K6"] * 1e-3) / 1e9
         print(f"rep {r}: {t}  K6 {gbs:.0f} GB/s algorithmic", flush=True)
 
 

@@ -23,9 +23,9 @@ def main():
     a = ap.parse_args()
     print("| cfg | workload | queries/s | e2e q/s | ms/step | main scan ms | frac of bf16 peak (burst / sustained) "
           "| K5 ms (frac of HBM, algorithmic) | K1 | sample+select | K4 | repairs | recall GPU / emulated oracle "
-          "| oracle q/s (cores) | SM MHz | file |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
-    for c in range(1, 6):
+          "| oracle q/s (cores) | SM MHz | K6 encode ms (frac of HBM) | file |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+    for c in ["1", "2", "3", "4", "4id", "5"]:
         f = latest(a.tag, c)
         if not f:
             continue
@@ -35,12 +35,14 @@ def main():
         rr = d.get("roofline_rerank", {})
         rec = d.get("recall_at_10", {})
         cb = d.get("cpu_baseline", {})
+        re_ = d.get("index_build", {}).get("roofline_encode")
+        enc = f"{re_['launch_ms']:.2f} ({re_['frac']:.2f})" if re_ else "-"
         print(f"| {c} | {d['config']['workload']} | {d['value']:,.0f} | {d['e2e']['value']:,.0f} | {d['ms_per_step']:.3f} "
               f"| {k.get('main_scan', 0):.3f} | {r.get('frac', 0):.3f} / {r.get('frac_of_sustained', 0):.3f} "
               f"| {k.get('rerank_K5', 0):.3f} ({rr.get('frac', 0):.2f}) | {k.get('project_K1', 0):.3f} "
               f"| {k.get('sample_stage', 0) + k.get('threshold_select', 0):.3f} | {k.get('select_K4', 0):.3f} "
               f"| {k.get('repairs', 0):.3f} | {rec.get('gpu', '-')} / {rec.get('oracle_emulated', '-')} "
-              f"| {cb.get('value', '-')} ({cb.get('cores', '-')}) | {d['clocks'].get('sm_mhz')} | {os.path.basename(f)} |")
+              f"| {cb.get('value', '-')} ({cb.get('cores', '-')}) | {d['clocks'].get('sm_mhz')} | {enc} | {os.path.basename(f)} |")
 
 
 if __name__ == "__main__":
