@@ -212,7 +212,6 @@ cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a,
 // tile.  One CTA per tile.
 constexpr int kEnPW = 8;                              // producer / epilogue warps
 constexpr int kEnRows = 128 / kEnPW;                  // tile rows per producer warp
-constexpr int kEnIt = kEnRows / 2;                    // two rows per warp-wide step
 constexpr int kEnThreads = 64 + 32 * kEnPW;
 
 __host__ __device__ constexpr int enc_hh(int d) { return (512 / d - 1) < 3 ? (512 / d - 1) : 3; }
@@ -311,62 +310,72 @@ __global__ void __launch_bounds__(kEnThreads, 1)
       if (++stage == kEnStages) { stage = 0; phase ^= 1; }
     }
   } else {
-    // producers: warp w (2..9) owns tile rows kEnRows*(w-2) ..; two rows per step (lanes 0-15 and
-    // 16-31), 4 consecutive elements per lane.  The loads of K block kb+1 are issued before the
-    // stage wait and the plane stores of block kb (register double buffer), so two blocks of row
-    // reads are in flight per warp and they overlap the MMAs.
+    // producers: warp w (2..9) owns tile rows kEnRows*(w-2) ..; each lane loads 16 bytes of one
+    // row per step (4 fp32 or 8 fp16 elements: 16 or 8 lanes per 64-element row, 2 or 4 rows per
+    // step).  The loads of K block kb+1 are issued before the stage wait and the plane stores of
+    // block kb (register double buffer), so two blocks of row reads are in flight per warp and
+    // they overlap the MMAs.
+    constexpr int kEPL = kXF16 ? 8 : 4;          // elements per lane and step
+    constexpr int kLPR = 64 / kEPL;              // lanes per row
+    constexpr int kRPS = 32 / kLPR;              // rows per step
+    constexpr int kIt = kEnRows / kRPS;          // steps per K block
     const int pw = warp - 2;
-    const int half = lane >> 4, l16 = lane & 15;
-    int srcs[kEnIt];
+    const int rsub = lane / kLPR, lc = lane % kLPR;
+    int srcs[kIt];
     {
       const int my_src = perm[(size_t)tile * 128 + pw * kEnRows + (lane % kEnRows)];
 #pragma unroll
-      for (int it = 0; it < kEnIt; ++it) srcs[it] = __shfl_sync(0xffffffffu, my_src, 2 * it + half);
+      for (int it = 0; it < kIt; ++it) srcs[it] = __shfl_sync(0xffffffffu, my_src, kRPS * it + rsub);
     }
     int stage = 0;
     uint32_t phase = 0;
-    auto load_block = [&](float (&x)[kEnIt][4], int kb) {
-      const int k0 = kb * 64 + l16 * 4;
+    auto load_block = [&](float (&x)[kIt][kEPL], int kb) {
+      const int k0 = kb * 64 + lc * kEPL;
 #pragma unroll
-      for (int it = 0; it < kEnIt; ++it) {
+      for (int it = 0; it < kIt; ++it) {
         const int src = srcs[it];
-        x[it][0] = x[it][1] = x[it][2] = x[it][3] = 0.f;
+#pragma unroll
+        for (int e = 0; e < kEPL; ++e) x[it][e] = 0.f;
         if (src >= 0) {
           if (kXF16) {
             const __half* row = reinterpret_cast<const __half*>(X) + (size_t)src * D;
-            if (vec && k0 + 3 < D) {
-              const uint2 u = __ldcs(reinterpret_cast<const uint2*>(row + k0));
-              const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
-              const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
-              x[it][0] = a.x; x[it][1] = a.y; x[it][2] = b.x; x[it][3] = b.y;
+            if (vec && k0 + kEPL - 1 < D) {
+              const uint4 u = __ldcs(reinterpret_cast<const uint4*>(row + k0));
+              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[e]));
+                x[it][2 * e] = f.x;
+                x[it][2 * e + 1] = f.y;
+              }
             } else {
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
+              for (int e = 0; e < kEPL; ++e)
                 if (k0 + e < D) x[it][e] = __half2float(row[k0 + e]);
             }
           } else {
             const float* row = reinterpret_cast<const float*>(X) + (size_t)src * D;
-            if (vec && k0 + 3 < D) {
+            if (vec && k0 + kEPL - 1 < D) {
               const float4 f = __ldcs(reinterpret_cast<const float4*>(row + k0));
               x[it][0] = f.x; x[it][1] = f.y; x[it][2] = f.z; x[it][3] = f.w;
             } else {
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
+              for (int e = 0; e < kEPL; ++e)
                 if (k0 + e < D) x[it][e] = row[k0 + e];
             }
           }
         }
       }
     };
-    auto store_block = [&](const float (&x)[kEnIt][4]) {
+    auto store_block = [&](const float (&x)[kIt][kEPL]) {
       tc::mbar_wait(empty + stage, phase ^ 1);
       uint8_t* st = smem + stage * kStage;
 #pragma unroll
-      for (int it = 0; it < kEnIt; ++it) {
-        const int r = pw * kEnRows + 2 * it + half;      // row in the tile
-        uint32_t hp[2], mp[2], lp[2];
+      for (int it = 0; it < kIt; ++it) {
+        const int r = pw * kEnRows + kRPS * it + rsub;   // row in the tile
+        uint32_t hp[kEPL / 2], mp[kEPL / 2], lp[kEPL / 2];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
+        for (int e = 0; e < kEPL / 2; ++e) {
           const float v0 = x[it][2 * e], v1 = x[it][2 * e + 1];
           const __nv_bfloat162 h2 = __floats2bfloat162_rn(v0, v1);
           const float2 hf = __bfloat1622float2(h2);
@@ -378,11 +387,18 @@ __global__ void __launch_bounds__(kEnThreads, 1)
           mp[e] = *reinterpret_cast<const uint32_t*>(&m2);
           lp[e] = *reinterpret_cast<const uint32_t*>(&l2);
         }
-        // SWIZZLE_128B: 16-byte chunk (l16 >> 1) of row r lands at chunk (l16 >> 1) ^ (r & 7)
-        const uint32_t off = (uint32_t)r * 128u + ((uint32_t)((l16 >> 1) ^ (r & 7)) << 4) + (uint32_t)(l16 & 1) * 8u;
-        *reinterpret_cast<uint2*>(st + off) = make_uint2(hp[0], hp[1]);
-        *reinterpret_cast<uint2*>(st + kXPlane + off) = make_uint2(mp[0], mp[1]);
-        if (kNP == 3) *reinterpret_cast<uint2*>(st + 2u * kXPlane + off) = make_uint2(lp[0], lp[1]);
+        // SWIZZLE_128B: the 16-byte chunk c of row r lands at chunk c ^ (r & 7)
+        if constexpr (kEPL == 8) {   // one whole chunk per lane
+          const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(lc ^ (r & 7)) << 4);
+          *reinterpret_cast<uint4*>(st + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+          *reinterpret_cast<uint4*>(st + kXPlane + off) = make_uint4(mp[0], mp[1], mp[2], mp[3]);
+          if (kNP == 3) *reinterpret_cast<uint4*>(st + 2u * kXPlane + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+        } else {                     // half a chunk per lane
+          const uint32_t off = (uint32_t)r * 128u + ((uint32_t)((lc >> 1) ^ (r & 7)) << 4) + (uint32_t)(lc & 1) * 8u;
+          *reinterpret_cast<uint2*>(st + off) = make_uint2(hp[0], hp[1]);
+          *reinterpret_cast<uint2*>(st + kXPlane + off) = make_uint2(mp[0], mp[1]);
+          if (kNP == 3) *reinterpret_cast<uint2*>(st + 2u * kXPlane + off) = make_uint2(lp[0], lp[1]);
+        }
       }
       tc::fence_proxy_async();   // generic-proxy smem writes -> visible to the tensor core
       __syncwarp();
@@ -390,7 +406,7 @@ __global__ void __launch_bounds__(kEnThreads, 1)
       if (++stage == kEnStages) { stage = 0; phase ^= 1; }
     };
     // two register buffers with fixed roles (unrolled by 2: no register copies of in-flight loads)
-    float xa[kEnIt][4], xb[kEnIt][4];
+    float xa[kIt][kEPL], xb[kIt][kEPL];
     load_block(xa, 0);
     for (int kb = 0; kb < nkb; kb += 2) {
       if (kb + 1 < nkb) load_block(xb, kb + 1);
