@@ -17,6 +17,7 @@
 // (tcgen05.ld 32 columns at a time, RNE to bf16 / fp16, 16-byte stores).
 #include <algorithm>
 #include <cfloat>
+#include <type_traits>
 
 #include "lv_common.cuh"
 #include "lv_internal.h"
@@ -329,54 +330,52 @@ __global__ void __launch_bounds__(kEnThreads, 1)
     }
     int stage = 0;
     uint32_t phase = 0;
-    auto load_block = [&](float (&x)[kIt][kEPL], int kb) {
+    // raw 16-byte words in registers (converted at store time), so an fp16 block costs the same
+    // registers as an fp32 one and kRing blocks of loads can be in flight: 2 for fp32 (128 B per
+    // lane and block), 4 for fp16 (64 B per lane and block)
+    constexpr int kRing = kXF16 ? 4 : 2;
+    auto load_block = [&](uint4 (&x)[kIt], int kb) {
       const int k0 = kb * 64 + lc * kEPL;
 #pragma unroll
       for (int it = 0; it < kIt; ++it) {
         const int src = srcs[it];
-#pragma unroll
-        for (int e = 0; e < kEPL; ++e) x[it][e] = 0.f;
+        x[it] = make_uint4(0u, 0u, 0u, 0u);
         if (src >= 0) {
-          if (kXF16) {
-            const __half* row = reinterpret_cast<const __half*>(X) + (size_t)src * D;
-            if (vec && k0 + kEPL - 1 < D) {
-              const uint4 u = __ldcs(reinterpret_cast<const uint4*>(row + k0));
-              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[e]));
-                x[it][2 * e] = f.x;
-                x[it][2 * e + 1] = f.y;
-              }
-            } else {
-#pragma unroll
-              for (int e = 0; e < kEPL; ++e)
-                if (k0 + e < D) x[it][e] = __half2float(row[k0 + e]);
-            }
+          using T = typename std::conditional<kXF16, __half, float>::type;
+          const T* row = reinterpret_cast<const T*>(X) + (size_t)src * D;
+          if (vec && k0 + kEPL - 1 < D) {
+            x[it] = __ldcs(reinterpret_cast<const uint4*>(row + k0));
           } else {
-            const float* row = reinterpret_cast<const float*>(X) + (size_t)src * D;
-            if (vec && k0 + kEPL - 1 < D) {
-              const float4 f = __ldcs(reinterpret_cast<const float4*>(row + k0));
-              x[it][0] = f.x; x[it][1] = f.y; x[it][2] = f.z; x[it][3] = f.w;
-            } else {
+            alignas(16) T tmp[kEPL];
 #pragma unroll
-              for (int e = 0; e < kEPL; ++e)
-                if (k0 + e < D) x[it][e] = row[k0 + e];
-            }
+            for (int e = 0; e < kEPL; ++e) tmp[e] = (k0 + e < D) ? row[k0 + e] : T(0.f);
+            x[it] = *reinterpret_cast<const uint4*>(tmp);
           }
         }
       }
     };
-    auto store_block = [&](const float (&x)[kIt][kEPL]) {
+    auto store_block = [&](const uint4 (&x)[kIt]) {
       tc::mbar_wait(empty + stage, phase ^ 1);
       uint8_t* st = smem + stage * kStage;
 #pragma unroll
       for (int it = 0; it < kIt; ++it) {
         const int r = pw * kEnRows + kRPS * it + rsub;   // row in the tile
+        float xv[kEPL];
+        const uint32_t w4[4] = {x[it].x, x[it].y, x[it].z, x[it].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if constexpr (kXF16) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[e]));
+            xv[2 * e] = f.x;
+            xv[2 * e + 1] = f.y;
+          } else {
+            xv[e] = __uint_as_float(w4[e]);
+          }
+        }
         uint32_t hp[kEPL / 2], mp[kEPL / 2], lp[kEPL / 2];
 #pragma unroll
         for (int e = 0; e < kEPL / 2; ++e) {
-          const float v0 = x[it][2 * e], v1 = x[it][2 * e + 1];
+          const float v0 = xv[2 * e], v1 = xv[2 * e + 1];
           const __nv_bfloat162 h2 = __floats2bfloat162_rn(v0, v1);
           const float2 hf = __bfloat1622float2(h2);
           const float r0 = v0 - hf.x, r1 = v1 - hf.y;      // exact in fp32
@@ -405,15 +404,20 @@ __global__ void __launch_bounds__(kEnThreads, 1)
       if (lane == 0) tc::mbar_arrive(full + stage);
       if (++stage == kEnStages) { stage = 0; phase ^= 1; }
     };
-    // two register buffers with fixed roles (unrolled by 2: no register copies of in-flight loads)
-    float xa[kIt][kEPL], xb[kIt][kEPL];
-    load_block(xa, 0);
-    for (int kb = 0; kb < nkb; kb += 2) {
-      if (kb + 1 < nkb) load_block(xb, kb + 1);
-      store_block(xa);
-      if (kb + 1 >= nkb) break;
-      if (kb + 2 < nkb) load_block(xa, kb + 2);
-      store_block(xb);
+    // kRing register buffers with fixed roles (the loop is unrolled by kRing, so no register
+    // copies of in-flight loads): block kb + kRing - 1 is requested before block kb is stored
+    uint4 xr[kRing][kIt];
+#pragma unroll
+    for (int r = 0; r < kRing - 1; ++r)
+      if (r < nkb) load_block(xr[r], r);
+    for (int kb0 = 0; kb0 < nkb; kb0 += kRing) {
+#pragma unroll
+      for (int r = 0; r < kRing; ++r) {
+        const int kb = kb0 + r;
+        if (kb >= nkb) break;
+        if (kb + kRing - 1 < nkb) load_block(xr[(r + kRing - 1) % kRing], kb + kRing - 1);
+        store_block(xr[r]);
+      }
     }
     // epilogue: rows of TMEM lane quarter (warp % 4; the hardware ties warp w to lanes
     // 32*(w%4)..), 32-column blocks split between the two warps of a quarter
@@ -468,7 +472,8 @@ static cudaError_t launch_enc_t(const CUtensorMap* tb, const void* X, int Dx, in
   const size_t smem = encode_smem(D, NP);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int vec = ((Dx & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) ? 1 : 0;
+  // 16-byte row loads need 16-byte aligned rows: D % 4 == 0 (fp32), D % 8 == 0 (fp16)
+  const int vec = ((Dx & (F ? 7 : 3)) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) ? 1 : 0;
   kern<<<(unsigned)ntiles, kEnThreads, smem, s>>>(*tb, X, Dx, Kp, Nc, vec, perm, tile_wrow, order, out);
   return cudaGetLastError();
 }

@@ -122,13 +122,14 @@ def test_g1_encode_project_and_raw_scores(lv, d):
 
 
 @pytest.mark.parametrize("D,d,C,xdt,low", [(200, 64, 1, "f32", "fp16"), (132, 32, 1, "f32", "bf16"),
+                                           (132, 32, 2, "f16", "bf16"),
                                            (96, 96, 3, "f16", "bf16"), (768, 160, 2, "f32", "bf16"),
                                            (512, 128, 1, "f16", "fp16"), (256, 192, 1, "f32", "bf16")])
 def test_g1_encode_shapes(lv, D, d, C, xdt, low, monkeypatch, planes="3"):
     """K6 (tensor-core encode) G1 across the shapes its layout depends on: ragged D (a partial last
-    64-wide K block), fp16 input rows, several clusters (per-tile B
-    rows, padded tiles), every d tile width.  x_low within 1 storage ulp + the fp32
-    accumulation bound of the oracle's fp64 B_c x, flips < 0.5 %."""
+    64-wide K block), fp16 input rows (D % 8 != 0: the scalar loads), several clusters (per-tile B
+    rows, padded tiles), every d tile width.  x_low within 1 storage ulp + the fp32 accumulation
+    bound of the oracle's fp64 B_c x, flips < 0.5 %."""
     monkeypatch.setenv("LV_K6_PLANES", planes)   # "2": the opt-in two-plane split (bf16 storage, R18)
     rng = np.random.default_rng(D * 7 + d)
     n = 3000
