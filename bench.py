@@ -7,11 +7,14 @@ resident in HBM; X_low (256 MB) and X (2 GB) exceed the 126 MB L2, so the scan s
 HBM every step (no explicit flush).  Default workload: configs[1] (cfg 2, LeanVec-Sphering
 1M x 512, d=128, R=100, k=10).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl lv|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--family ood|id]
+                  [--impl lv|reference] [--oracle-queries Q] [--no-cpu-baseline]
 
 N > 1 (torchrun): query-sharded replicas — each rank holds the full index and searches its own
-m-query batch (weak scaling, no data-path collective; DESIGN.md §7).  `--impl reference` times
-the CPU oracle (the only reference this paper has) on a bounded query sample per step.
+m-query batch (weak scaling, no data-path collective; DESIGN.md §8).  `--impl reference` times
+the CPU oracle (the only reference this paper has) on a bounded query sample per step.  The
+index build (fit, K6 encode with its HBM roofline) is reported under `index_build`, outside
+the timed step; config 4 has two query families (`--family`), each with its own fit and encode.
 """
 from __future__ import annotations
 
@@ -205,7 +208,7 @@ def _ncu_traffic(cfg_id):
 
 def shard_queries(m, rank, world):
     """Query rows [rank * m, (rank + 1) * m) of the config's test stream: each rank searches its own
-    batch of the same size (weak scaling, no data-path collective; DESIGN.md §7)."""
+    batch of the same size (weak scaling, no data-path collective; DESIGN.md §8)."""
     return rank * m, (rank + 1) * m
 
 

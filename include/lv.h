@@ -183,6 +183,20 @@ lv_status lv_search_host(lv_index* index, const float* Q_host, int64_t m, int32_
 lv_status lv_assign_tags(const void* X, lv_dtype x_dtype, int64_t n, int32_t D,
                          const float* centres, int32_t C, int32_t* assign, void* stream);
 
+/*
+ * lv_index_set_search_dim — flexible target dimensionality (§3.1, Eq.(10): "select the
+ * value of d during search by considering the first d dimensions of x' and of P'W^-1 q").  With
+ * LeanVec-Sphering the rows of P (hence of A and B) are ordered by decreasing singular value, so
+ * the first d_search coordinates of every stored x_low and of every projected q' are exactly the
+ * reduction to d_search.  Subsequent lv_search / lv_project_queries calls score only those: the
+ * scan reads the first d_search columns of X_low (row pitch d stays), K1 uses the first d_search
+ * rows of A.  d_search in {32, 64, ..., 192}, <= the stored d; <= 0 restores d.  C > 1 (GleanVec,
+ * one P per cluster) keeps d: LV_EINVAL.  The index's other state is unchanged; no device work.
+ * lv_index_get_search_dim reads the current value (HOST out).
+ */
+lv_status lv_index_set_search_dim(lv_index* index, int32_t d_search);
+lv_status lv_index_get_search_dim(const lv_index* index, int32_t* d_search);
+
 /* Sizes of the encoded index (HOST out pointers, any may be NULL). */
 lv_status lv_index_info(const lv_index* index, int64_t* n, int64_t* n_pad, int32_t* D,
                         int32_t* d, int32_t* C);

@@ -55,6 +55,7 @@ struct PlanCache {
 
 struct lv_index {
   int32_t D = 0, d = 0, C = 0;
+  int32_t ds = 0;              // search dimension <= d (§3.1 flexible d: the first ds reduced coordinates)
   lv_dtype low = LV_BF16, full = LV_F32;
   float* A = nullptr;          // [C*d, D]
   float* B = nullptr;          // [C*d, D]
@@ -71,7 +72,8 @@ struct lv_index {
   int32_t* tile_valid = nullptr;  // [n_pad/128]
   std::vector<int64_t> offsets;   // host [C+1] padded segment starts
   void* X_full = nullptr;      // [n, D] full dtype, original order
-  CUtensorMap tmap_xlow;
+  CUtensorMap tmap_xlow;      // X_low, d columns
+  CUtensorMap tmap_xlow_s;    // X_low's first ds columns (row pitch d): the scan's B operand
   // search workspace
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -138,12 +140,14 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 2D row-major [rows, cols] of 16-bit elements; box [box_rows, ch cols]; swizzle = ch*2 bytes.
-lv_status make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int ch, bool bf16, int box_rows) {
+// 2D row-major [rows, cols] of 16-bit elements (row pitch ld >= cols elements, default cols);
+// box [box_rows, ch cols]; swizzle = ch*2 bytes.
+lv_status make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int ch, bool bf16, int box_rows,
+                    int64_t ld = 0) {
   auto enc = get_encode();
   if (!enc) return fail(LV_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t gstride[1] = {(cuuint64_t)cols * 2};
+  cuuint64_t gstride[1] = {(cuuint64_t)(ld > 0 ? ld : cols) * 2};
   cuuint32_t box[2] = {(cuuint32_t)ch, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
@@ -152,6 +156,12 @@ lv_status make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t co
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(LV_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return LV_OK;
+}
+
+// The scan's view of X_low: its first ds columns (boxes of the width the scan kernel for ds uses).
+lv_status make_search_tmap(lv_index* ix) {
+  return make_tmap(&ix->tmap_xlow_s, ix->X_low, ix->n_pad, ix->ds, (ix->ds % 64 == 0) ? 64 : 32, ix->low == LV_BF16,
+                   lv::score_tile_rows(ix->ds), ix->d);
 }
 
 double env_double(const char* name, double dflt) {
@@ -320,8 +330,8 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   // 32-row sample blocks while the block-maximum array stays small (<= 8192 blocks); coarser
   // 64-row blocks at the 10M-row sizes, where the array's HBM traffic would cost more than the
   // tighter threshold saves
-  const bool fine = (int64_t)lv::score_blocks_per_tile(ix->d, true) * nsamp <= 8192;
-  const int bpt = lv::score_blocks_per_tile(ix->d, fine);   // block maxima per sampled tile
+  const bool fine = (int64_t)lv::score_blocks_per_tile(ix->ds, true) * nsamp <= 8192;
+  const int bpt = lv::score_blocks_per_tile(ix->ds, fine);   // block maxima per sampled tile
   pl->sampled = env_double("LV_SAMPLED", 1.0) != 0.0 && stride >= 2 && nsamp >= 64 && bpt * nsamp >= 8 * j1 &&
                 bpt * nsamp <= 65535;
   if (pl->sampled) {
@@ -349,10 +359,10 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   pl->grid = (int)std::min<int64_t>(G, (int64_t)pmax * pl->QP);
   const size_t budget = 227 * 1024 - 1024 - 256;
   int st = std::max(2, std::min(8, (int)env_double("LV_STAGES", 8.0)));   // LV_STAGES: probe knob
-  while (st >= 2 && lv::score_smem_bytes(ix->d, st) > budget) --st;
-  if (st < 2) return fail(LV_EUNSUPPORTED, "d=%d leaves no room for a 2-stage pipeline", ix->d);
+  while (st >= 2 && lv::score_smem_bytes(ix->ds, st) > budget) --st;
+  if (st < 2) return fail(LV_EUNSUPPORTED, "d=%d leaves no room for a 2-stage pipeline", ix->ds);
   pl->stages = st;
-  pl->smem = lv::score_smem_bytes(ix->d, st);
+  pl->smem = lv::score_smem_bytes(ix->ds, st);
   return LV_OK;
 }
 
@@ -484,6 +494,7 @@ lv_status lv_index_create(lv_index** out, int32_t D, int32_t d, int32_t C, lv_dt
   lv_index* ix = new lv_index();
   ix->D = D;
   ix->d = d;
+  ix->ds = d;
   ix->C = C;
   ix->low = low_dtype;
   ix->full = full_dtype;
@@ -634,6 +645,10 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
   // X_low = RNE(B_c x) (K6)
   const size_t esz = 2;
   if (cudaMalloc(&ix->X_low, esz * ix->n_pad * ix->d) != cudaSuccess) return fail(LV_ENOMEM, "X_low");
+  // full-precision copy for the re-rank (allocated before the timed kernels: a host-side
+  // cudaMalloc between two event records would count as kernel time)
+  const size_t fsz = ix->full == LV_F16 ? 2 : 4;
+  if (cudaMalloc(&ix->X_full, fsz * n * ix->D) != cudaSuccess) return fail(LV_ENOMEM, "X_full");
   LV_CUDA(cudaEventRecord(ev[1], s));
   if (k6_tensor())
     LV_CUDA(lv::launch_encode_tc(&ix->tmap_b, X, x_dtype == LV_F16, ix->D, ix->Kp, ix->d, ix->C * ix->d, ix->perm, dwrow,
@@ -641,14 +656,12 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
   else
     LV_CUDA(lv::launch_rows_gemm(X, x_dtype == LV_F16, ix->D, ix->perm, n, ix->n_pad, ix->B, ix->D, dwrow, ix->d,
                                  ix->X_low, ix->low, ix->d, ix->n_pad, s));
-  // full-precision copy for the re-rank
-  const size_t fsz = ix->full == LV_F16 ? 2 : 4;
-  if (cudaMalloc(&ix->X_full, fsz * n * ix->D) != cudaSuccess) return fail(LV_ENOMEM, "X_full");
   LV_CUDA(cudaEventRecord(ev[2], s));
   LV_CUDA(lv::launch_convert(X, x_dtype == LV_F16, ix->X_full, ix->full == LV_F16, n * ix->D, s));
   LV_CUDA(cudaEventRecord(ev[3], s));
   lv_status ts = make_tmap(&ix->tmap_xlow, ix->X_low, ix->n_pad, ix->d, (ix->d % 64 == 0) ? 64 : 32, ix->low == LV_BF16,
                            lv::score_tile_rows(ix->d));
+  if (!ts) ts = make_search_tmap(ix);
   LV_CUDA(cudaStreamSynchronize(s));
   cudaFree(dwrow);
   for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&ix->enc_ms[i], ev[i], ev[i + 1]);
@@ -662,9 +675,9 @@ lv_status lv_project_queries(const lv_index* ix, const float* Q, int64_t m, void
   if (!ix || !Q || !Qp || m <= 0) return fail(LV_EINVAL, "lv_project_queries: bad arguments");
   if (m > (1 << 24)) return fail(LV_EINVAL, "lv_project_queries: m too large");
   cudaStream_t s = (cudaStream_t)stream;
+  const int Cd = ix->C * ix->ds;   // search width (C = 1 when ds < d: the first ds rows of A)
   if (!k1_tensor()) {
-    LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, m, ix->A, ix->D, nullptr, ix->C * ix->d, Qp, ix->low,
-                                 (int64_t)ix->C * ix->d, m, s));
+    LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, m, ix->A, ix->D, nullptr, Cd, Qp, ix->low, Cd, m, s));
     return LV_OK;
   }
   const int64_t m_pad = (m + 127) / 128 * 128;
@@ -677,7 +690,7 @@ lv_status lv_project_queries(const lv_index* ix, const float* Q, int64_t m, void
     return st;
   }
   LV_CUDA(lv::launch_split3(Q, m, m_pad, ix->D, ix->Kp, planes, s));
-  LV_CUDA(lv::launch_proj_tc(&tq, &ix->tmap_a, (int)m_pad, ix->C * ix->d, ix->Kp, Qp, (int64_t)ix->C * ix->d, (int)m,
+  LV_CUDA(lv::launch_proj_tc(&tq, &ix->tmap_a, (int)m_pad, Cd, ix->C * ix->d, ix->Kp, Qp, Cd, (int)m,
                              ix->low == LV_BF16, s));
   LV_CUDA(cudaFreeAsync(planes, s));
   return LV_OK;
@@ -693,7 +706,7 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   if (k < 1 || k > R || R > 256 || R > ix->n) return fail(LV_EINVAL, "lv_search: need 1 <= k <= R <= min(n, 256)");
   if (m > (1 << 24)) return fail(LV_EINVAL, "lv_search: m too large");
   cudaStream_t s = (cudaStream_t)stream;
-  const int Cd = ix->C * ix->d;
+  const int Cd = ix->C * ix->ds;   // search width (lv_index_set_search_dim)
   PlanCache& pc = ix->plan;
   if (!(pc.valid && pc.m == m && pc.R == R && pc.nsm == nsm)) {
     // new search shape: plan the scan, (re)size the workspace, upload the chunk tables once
@@ -785,7 +798,8 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   // K1 projection (rows >= m are zero)
   if (k1_tensor()) {
     LV_CUDA(lv::launch_split3(Q, m, pl.m_pad, ix->D, ix->Kp, pc.Qplanes, s));
-    LV_CUDA(lv::launch_proj_tc(&pc.tmap_q, &ix->tmap_a, pl.m_pad, Cd, ix->Kp, Qp, Cd, pl.m_pad, ix->low == LV_BF16, s));
+    LV_CUDA(lv::launch_proj_tc(&pc.tmap_q, &ix->tmap_a, pl.m_pad, Cd, ix->C * ix->d, ix->Kp, Qp, Cd, pl.m_pad,
+                               ix->low == LV_BF16, s));
     launches += 2;
   } else {
     LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, pl.m_pad, ix->A, ix->D, nullptr, Cd, Qp, ix->low, Cd,
@@ -799,7 +813,7 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   sa.m = (int)m;
   sa.m_pad = pl.m_pad;
   sa.QP = pl.QP;
-  sa.d = ix->d;
+  sa.d = ix->ds;
   sa.R = R;
   sa.NS = pl.NS;
   sa.Cap = pl.Cap;
@@ -830,7 +844,7 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     const int grid = (int)std::min<int64_t>(nsm, (int64_t)sa.P * qtiles);
     if (grid <= 0) return LV_OK;
     if (sa.stats) LV_CUDA(cudaMemsetAsync(sa.stats, 0, 8 * sizeof(unsigned long long), s));
-    LV_CUDA(lv::launch_score(&ix->tmap_xlow, sa, ix->low == LV_BF16, grid, pl.smem, s));
+    LV_CUDA(lv::launch_score(&ix->tmap_xlow_s, sa, ix->low == LV_BF16, grid, pl.smem, s));
     ++launches;
     if (sa.stats) {
       unsigned long long h[8];
@@ -1040,6 +1054,26 @@ lv_status lv_assign_tags(const void* X, lv_dtype x_dtype, int64_t n, int32_t D, 
   if (!X || !centres || !assign || n <= 0 || D <= 0 || C < 1) return fail(LV_EINVAL, "lv_assign_tags: bad arguments");
   if (x_dtype != LV_F32 && x_dtype != LV_F16) return fail(LV_EINVAL, "lv_assign_tags: x_dtype must be F32/F16");
   LV_CUDA(lv::launch_assign(X, x_dtype == LV_F16, n, D, centres, C, assign, (cudaStream_t)stream));
+  return LV_OK;
+}
+
+lv_status lv_index_set_search_dim(lv_index* ix, int32_t d_search) {
+  if (!ix) return fail(LV_EINVAL, "lv_index_set_search_dim: bad arguments");
+  if (d_search <= 0) d_search = ix->d;
+  if (d_search > ix->d) return fail(LV_EINVAL, "lv_index_set_search_dim: d_search=%d > stored d=%d", d_search, ix->d);
+  if (d_search != ix->d && ix->C != 1)
+    return fail(LV_EINVAL, "lv_index_set_search_dim: a prefix search needs C = 1 (LeanVec-Sphering, §3.1)");
+  if (d_search % 32 != 0 || d_search > 192)
+    return fail(LV_EINVAL, "lv_index_set_search_dim: d_search=%d not in {32, 64, ..., 192}", d_search);
+  if (d_search == ix->ds) return LV_OK;
+  ix->ds = d_search;
+  ix->plan.valid = false;   // the scan plan depends on the width
+  return ix->X_low ? make_search_tmap(ix) : LV_OK;
+}
+
+lv_status lv_index_get_search_dim(const lv_index* ix, int32_t* d_search) {
+  if (!ix || !d_search) return fail(LV_EINVAL, "lv_index_get_search_dim: bad arguments");
+  *d_search = ix->ds;
   return LV_OK;
 }
 

@@ -86,8 +86,9 @@ cudaError_t launch_rows_gemm(const void* in, int in_f16, int64_t ld_in, const in
 // K1 on tensor cores (lv_proj.cu): three-plane bf16 split and the six-product GEMM.
 cudaError_t launch_split3(const float* in, int64_t rows_valid, int64_t rows_pad, int D, int Kp, void* out,
                           cudaStream_t s);
-cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a, int m_pad, int Nc, int Kp, void* out,
-                           int64_t ld_out, int rows_store, bool out_bf16, cudaStream_t s);
+// Q' [m_pad rows, Nc columns] = the first Nc rows of the A stack (a_rows rows per plane) times Q
+cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a, int m_pad, int Nc, int a_rows, int Kp,
+                           void* out, int64_t ld_out, int rows_store, bool out_bf16, cudaStream_t s);
 // K6 on tensor cores: out[r, :] = RNE(B_{c(r)} X[perm[r], :]) for 128-row tiles (tile_wrow[2t] = c*d),
 // CTA i encodes tile order[i] (nullptr: tile i)
 // (three bf16 planes; two for bf16 storage when !planes3)

@@ -56,7 +56,7 @@ __global__ void k_split3(const float* __restrict__ in, int64_t rows_valid, int64
 template <bool kOutBF16>
 __global__ void __launch_bounds__(kPjThreads, 1)
     k_proj_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_a, int m_pad,
-              int Nc, int Kp, void* __restrict__ out, int64_t ld_out, int rows_store) {
+              int Nc, int a_rows, int Kp, void* __restrict__ out, int64_t ld_out, int rows_store) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kPjStages * kPjStageBytes);
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kPjThreads, 1)
         uint8_t* st = smem + stage * kPjStageBytes;
         for (int p = 0; p < 3; ++p) {
           tc::tma_load_2d(st + p * kPjPlaneBytes, &tmap_q, full + stage, kb * 64, p * m_pad + m0);
-          tc::tma_load_2d(st + (3 + p) * kPjPlaneBytes, &tmap_a, full + stage, kb * 64, p * Nc + n0);
+          tc::tma_load_2d(st + (3 + p) * kPjPlaneBytes, &tmap_a, full + stage, kb * 64, p * a_rows + n0);
         }
         if (++stage == kPjStages) { stage = 0; phase ^= 1; }
       }
@@ -187,13 +187,13 @@ cudaError_t launch_split3(const float* in, int64_t rows_valid, int64_t rows_pad,
   return cudaGetLastError();
 }
 
-cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a, int m_pad, int Nc, int Kp, void* out,
-                           int64_t ld_out, int rows_store, bool out_bf16, cudaStream_t s) {
+cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a, int m_pad, int Nc, int a_rows, int Kp,
+                           void* out, int64_t ld_out, int rows_store, bool out_bf16, cudaStream_t s) {
   auto kern = out_bf16 ? k_proj_tc<true> : k_proj_tc<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPjSmem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((Nc + 127) / 128), (unsigned)(m_pad / 128));
-  kern<<<grid, kPjThreads, kPjSmem, s>>>(*tmap_q, *tmap_a, m_pad, Nc, Kp, out, ld_out, rows_store);
+  kern<<<grid, kPjThreads, kPjSmem, s>>>(*tmap_q, *tmap_a, m_pad, Nc, a_rows, Kp, out, ld_out, rows_store);
   return cudaGetLastError();
 }
 

@@ -21,7 +21,8 @@ _TORCH_DT = {LV_F32: torch.float32, LV_F16: torch.float16, LV_BF16: torch.bfloat
 
 EXPORTS = ["lv_last_error", "lv_version", "lv_fit_stats", "lv_index_create", "lv_encode_database",
            "lv_project_queries", "lv_search", "lv_search_host", "lv_timing_collect", "lv_encode_timing", "lv_assign_tags",
-           "lv_index_info", "lv_index_export", "lv_index_destroy"]
+           "lv_index_info", "lv_index_export", "lv_index_destroy", "lv_index_set_search_dim",
+           "lv_index_get_search_dim"]
 
 
 class LVError(RuntimeError):
@@ -60,6 +61,8 @@ def lib():
             "lv_search_host": [vp, vp, i64, i32, i32, vp, vp, vp],
             "lv_timing_collect": [vp, vp, ctypes.POINTER(i32)],
             "lv_encode_timing": [vp, vp],
+            "lv_index_set_search_dim": [vp, i32],
+            "lv_index_get_search_dim": [vp, ctypes.POINTER(i32)],
             "lv_assign_tags": [vp, i32, i64, i32, vp, i32, vp, vp],
             "lv_index_info": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32),
                               ctypes.POINTER(i32), ctypes.POINTER(i32)],
@@ -162,9 +165,22 @@ def lv_encode_database(index: Index, X: torch.Tensor, assign: torch.Tensor | Non
            "lv_encode_database")
 
 
+def lv_index_set_search_dim(index: Index, d_search: int):
+    """§3.1 flexible d: search on the first d_search reduced coordinates (<= 0: the stored d)."""
+    _check(lib().lv_index_set_search_dim(index.h, int(d_search)), "lv_index_set_search_dim")
+
+
+def lv_index_get_search_dim(index: Index) -> int:
+    ds = ctypes.c_int32()
+    _check(lib().lv_index_get_search_dim(index.h, ctypes.byref(ds)), "lv_index_get_search_dim")
+    return ds.value
+
+
 def lv_project_queries(index: Index, Q: torch.Tensor) -> torch.Tensor:
+    """Q' [m, C * d_search] (d_search = the stored d unless lv_index_set_search_dim changed it)."""
     Q = _dev(Q, torch.float32)
-    Qp = torch.empty((Q.shape[0], index.C * index.d), dtype=_TORCH_DT[_DT[index.low]], device=Q.device)
+    Qp = torch.empty((Q.shape[0], index.C * lv_index_get_search_dim(index)), dtype=_TORCH_DT[_DT[index.low]],
+                     device=Q.device)
     _check(lib().lv_project_queries(index.h, _ptr(Q), Q.shape[0], _ptr(Qp), _stream()), "lv_project_queries")
     return Qp
 

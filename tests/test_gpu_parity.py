@@ -397,3 +397,46 @@ def test_sampled_path_gleanvec(lv):
     c, X, Q, A32, B32, assign, R, k = _case(3, n=200_000, m=200, d=96, C=4)
     dbg = _check_search(lv, c, X, Q, A32, B32, assign, R, k, 4, timing=True)
     assert dbg["path"] == 1
+
+
+@pytest.mark.parametrize("d_store,d_search,n", [(128, 64, 20_000), (128, 96, 200_000), (128, 128, 5000),
+                                                (96, 32, 6000), (192, 96, 6000), (160, 32, 200_000)])
+def test_flexible_search_dim(lv, d_store, d_search, n):
+    """§3.1 flexible d: an index encoded at d_store and searched on its first d_search
+    coordinates (lv_index_set_search_dim) returns exactly what an index built from the first
+    d_search rows of the same A/B returns (the stored prefix and the projected prefix are the same
+    numbers: K6 splits its accumulation the same way for both widths when d_store <= 128), on the
+    staged and the sampled path; every case also passes the oracle gates on the prefix stacks."""
+    c, X, Q, A32, B32, assign, R, k = _case(2, n=n, m=300, d=d_store)
+    ix = _gpu_index(lv, c, X, A32, B32, assign, 1)
+    lv.lv_index_set_search_dim(ix, d_search)
+    assert lv.lv_index_get_search_dim(ix) == d_search
+    ids, sc, dbg = lv.lv_search(ix, torch.from_numpy(Q).cuda(), k, R, cand=True)
+    cp = c.replace(d=d_search)
+    ix2 = _gpu_index(lv, cp, X, np.ascontiguousarray(A32[:, :d_search]), np.ascontiguousarray(B32[:, :d_search]),
+                     assign, 1)
+    ids2, sc2, dbg2 = lv.lv_search(ix2, torch.from_numpy(Q).cuda(), k, R, cand=True)
+    assert dbg["path"] == dbg2["path"]
+    Qp = lv.lv_project_queries(ix, torch.from_numpy(Q).cuda())
+    assert Qp.shape[1] == d_search and torch.equal(Qp, lv.lv_project_queries(ix2, torch.from_numpy(Q).cuda()))
+    if d_store <= 128:
+        assert torch.equal(lv.lv_index_export(ix)[0][:, :d_search], lv.lv_index_export(ix2)[0])
+        assert torch.equal(ids, ids2) and torch.equal(sc, sc2)
+        assert torch.equal(dbg["cand_ids"], dbg2["cand_ids"])
+    # and against the oracle on the prefix stacks (G3-G6 gates)
+    _check_search(lv, cp, X, Q, np.ascontiguousarray(A32[:, :d_search]), np.ascontiguousarray(B32[:, :d_search]),
+                  assign, R, k, 1)
+    lv.lv_index_set_search_dim(ix, 0)   # back to the stored d
+    assert lv.lv_index_get_search_dim(ix) == d_store
+
+
+def test_flexible_search_dim_rejects(lv):
+    c, X, Q, A32, B32, assign, R, k = _case(3, n=3000, m=50, d=96, C=2)
+    ix = _gpu_index(lv, c, X, A32, B32, assign, 2)
+    with pytest.raises(lv.LVError):
+        lv.lv_index_set_search_dim(ix, 64)     # GleanVec: one P per cluster, no shared prefix
+    c1, X1, Q1, A1, B1, a1, _, _ = _case(1, n=2000, m=20, d=64)
+    ix1 = _gpu_index(lv, c1, X1, A1, B1, a1, 1)
+    for bad in (96, 48):                       # > stored d; not a multiple of 32
+        with pytest.raises(lv.LVError):
+            lv.lv_index_set_search_dim(ix1, bad)

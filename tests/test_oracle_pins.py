@@ -164,6 +164,26 @@ def test_loss_closed_form_optimum_and_orderings():
     assert losses[-1] <= 1e-9 * losses[0]
 
 
+def test_flexible_d_prefix_is_the_smaller_fit():
+    """§3.1: P' holds the singular vectors in decreasing order, so searching on the
+    first d2 coordinates of x' = P'Wx and of P'W^-1 q IS the d2 reduction: its loss is the
+    Eckart-Young optimum m * sum_{j>d2} lambda_j(W K_X W) (a closed form, not the oracle's fit
+    route), and the prefix scores equal <A_d2 q, B_d2 x>."""
+    Q, X = _ood_pair(_rng(11))
+    m, D = Q.shape
+    full = O.sphering_fit(Q, X, D)                       # P' = D x D (Eq. 10's storage)
+    lam = np.sort(np.linalg.eigvalsh(full["W"] @ (X.T @ X) @ full["W"]))[::-1]
+    q = Q[:9]
+    for d2 in (2, 5, 9):
+        A2, B2 = full["A"][:d2], full["B"][:d2]          # first d2 rows = first d2 coordinates
+        L = O.leanvec_loss(A2, B2, Q, X)
+        closed = m * lam[d2:].sum()
+        assert abs(L - closed) <= 1e-9 * closed
+        s_pre = O.reduced_scores(O.project(q, full["A"])[:, :, :d2], O.encode(X, full["B"])[:, :d2])
+        s_d2 = O.reduced_scores(O.project(q, A2), O.encode(X, B2))
+        assert np.allclose(s_pre, s_d2, rtol=0, atol=1e-12)
+
+
 def test_scale_invariance_of_AtB():
     """Q -> cQ leaves A^T B unchanged."""
     Q, X = _ood_pair(_rng(8))
