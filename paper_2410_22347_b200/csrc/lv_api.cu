@@ -193,6 +193,8 @@ T* carve(uint8_t*& p, size_t count) {
 // Chunks of the given segments (tile ranges) so that units = P * QP spread evenly over the grid.
 // With stride > 1 only every stride-th tile of a segment is scanned (sample stage); the scanned
 // tiles are numbered consecutively from *sample_base (block-maximum rows, lv_score.cu).
+constexpr double kUnitCostTiles = 4.0;
+
 void make_chunks(const std::vector<std::pair<int, int>>& segs, const std::vector<int>& segc, int QP, int G,
                  int maxChunks, std::vector<int32_t>* out, int stride = 1, int* sample_base = nullptr) {
   std::vector<int> cnts(segs.size());
@@ -213,8 +215,10 @@ void make_chunks(const std::vector<std::pair<int, int>>& segs, const std::vector
     if (P > maxChunks) continue;
     const int64_t units = (int64_t)P * QP;
     const int g = (int)std::min<int64_t>(G, units);
-    // time ~ max units on one CTA x tiles per unit; efficiency vs perfect spread
-    const double per_cta = (double)((units + g - 1) / g) * len;
+    // time ~ max units on one CTA x (tiles per unit + the unit boundary's cost, ~4 tiles: slot
+    // claim/release, list-state flush and the epilogue's barrier; measured: 2.54 -> 2.36 ms on
+    // cfg 2 going from 103 to ~30 chunks); efficiency vs perfect spread
+    const double per_cta = (double)((units + g - 1) / g) * (len + kUnitCostTiles);
     const double ideal = (double)ntiles * QP / G;
     double eff = ideal / per_cta - 1e-4 * (double)P / (double)ntiles;   // prefer fewer chunks on ties
     if (eff > best_eff + 1e-9) {
@@ -258,7 +262,7 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   const int ns_smem = (int)((200 * 1024 - (size_t)ix->D * 4) / ((size_t)pl->Cap * 8)) / 2;
   const int ns = std::min((int)env_double("LV_SLOTS", 8.0), ns_smem);
   if (ns < 1) return fail(LV_EUNSUPPORTED, "R=%d too large for the merge", R);
-  const int max_chunks = 1 << 30;
+  const int max_chunks = (int)env_double("LV_MAX_CHUNKS", 1e9);   // probe knob (units per chunk sweep)
   const int ns_target = ns;
   // segment tile ranges
   std::vector<std::pair<int, int>> seg;

@@ -590,15 +590,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       // unit end: every job of this unit has seen its tile committed, so the MMA is done with
       // this unit's A buffer before any warp overwrites it (write_A of unit u + 2 at the next
       // iteration); in the main stage the sub-list states go back to the slot, which is released
-      if (lists) {
-        if (qvalid) {
-          a.cnt[si] = cnt;
-          a.tau[si] = tk;
-        }
-        __threadfence();
+      if (lists && qvalid) {
+        a.cnt[si] = cnt;
+        a.tau[si] = tk;
       }
       tc::named_bar_sync(1, kEpiThreads);
-      if (lists && threadIdx.x == 0) atomicAnd(a.slot_busy + qt, ~(1 << my_slot));   // release the slot
+      if (lists && threadIdx.x == 0) {
+        // the barrier orders every epilogue thread's list-state stores before this thread's
+        // (cumulative) fence, which orders them before the release the next owner acquires
+        __threadfence();
+        atomicAnd(a.slot_busy + qt, ~(1 << my_slot));   // release the slot
+      }
       // single-buffered A: every job of this unit saw its tile committed, so the MMAs of this unit
       // are complete and its A buffer can take the next unit's operand
       if (kSingleA && u + (int)gridDim.x < nunits) write_A(u + gridDim.x, 0);
