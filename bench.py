@@ -339,6 +339,11 @@ def main():
         lv.lv_search(ix, Qd, cfg.k, cfg.R, out=(ids, sc))
     torch.cuda.synchronize()
     launches_per_step = lv.lv_search(ix, Qd, cfg.k, cfg.R, out=(ids, sc))[2]["launches"]
+    # one untimed pass of the timed loop's shape: the library's event pool then holds the
+    # 8 * steps events the timed loop records (no event creation inside the timed region)
+    for _ in range(args.steps):
+        lv.lv_search(ix, Qd, cfg.k, cfg.R, out=(ids, sc), timing=2)
+    torch.cuda.synchronize()
     lv.lv_timing_collect(ix)   # drop anything recorded before the timed region
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

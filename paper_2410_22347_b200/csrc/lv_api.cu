@@ -74,6 +74,7 @@ struct lv_index {
   void* X_full = nullptr;      // [n, D] full dtype, original order
   CUtensorMap tmap_xlow;      // X_low, d columns
   CUtensorMap tmap_xlow_s;    // X_low's first ds columns (row pitch d): the scan's B operand
+  unsigned long long* dbg_stats = nullptr;   // [8] scan event counters (debug flag 2)
   // search workspace
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -836,7 +837,7 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     const char* f = getenv("LV_DEBUG_SCAN_FLAGS");
     sa.flags = f ? atoi(f) : 0;
   }
-  static unsigned long long* dstats = nullptr;
+  unsigned long long*& dstats = ix->dbg_stats;   // debug counters (LV_DEBUG_SCAN_FLAGS & 2), owned by the index
   sa.stats = nullptr;
   if (sa.flags & 2) {
     if (!dstats) LV_CUDA(cudaMalloc(&dstats, 8 * sizeof(unsigned long long)));
@@ -1107,6 +1108,7 @@ void lv_index_destroy(lv_index* ix) {
   free_db(ix);
   cudaFree(ix->A);
   cudaFree(ix->B);
+  cudaFree(ix->dbg_stats);
   cudaFree(ix->A_planes);
   cudaFree(ix->B_planes);
   for (auto& g : ix->ev_pending)
