@@ -34,11 +34,8 @@ constexpr int kMaxKeysPerLane = 12;    // Cap <= 384
 
 
 // Shared-memory epilogue state.
-#ifndef LV_ROWS
-#define LV_ROWS 32                     // staged hitting rows per warp (fewer: more smem for the B ring)
-#endif
 struct EpiShared {
-  float rows[kEpiWarps][LV_ROWS][32];  // hitting lanes' 32 scores, read column-wise
+  float rows[kEpiWarps][32][32];       // hitting lanes' 32 scores (row = lane), read column-wise
   int hist[kEpiWarps][256];            // radix scratch of the compaction
   int slot;                            // candidate slot of the current unit
   int jc[4];                           // per TMEM lane quarter: next (tile, column-quarter) job
@@ -255,9 +252,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool skip_topr = (a.flags & 1) != 0;
   const bool count_stats = (a.flags & 2) != 0 && a.stats != nullptr;
   const bool fast_only = (a.flags & 4) != 0;   // debug: detect hits but drop them (fast-path cost probe)
-#ifdef LV_PROBE_NOLD
-  const bool no_ld = (a.flags & 16) != 0;       // debug: release accumulators unread (MMA-pipeline probe)
-#endif
   const bool fine_blocks = (a.flags & 8) != 0;  // sample stage: 32-row block maxima
 
   if (threadIdx.x == 0) {
@@ -468,15 +462,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         float bm = -FLT_MAX;   // sample stage: running block maximum of the job
 #pragma unroll
         for (int h = 0; h < kJV; ++h) {
-#ifdef LV_PROBE_NOLD
-          if (no_ld) {   // debug probe (experiment builds): release without reading the accumulator
-            if (h + 1 == kJV) {
-              __syncwarp();
-              if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
-            }
-            continue;
-          }
-#endif
           float v[32];
           tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kN + (uint32_t)(jh * kJobCols + 32 * h), v);
           tc::tmem_wait_ld();
@@ -524,37 +509,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           // memory, lane j tests column j, survivors are appended to the hitting lane's sub-list
           // with coalesced stores
           const int32_t id_h = (a.perm ? my_id[h] : hpos + lane);
-#if LV_ROWS < 32
-          // staged in rounds of at most LV_ROWS hitting lanes (the i-th hitting lane of a round
-          // takes row i)
-          uint32_t rem = hb;
-          while (rem != 0u) {
-          hb = __popc(rem) <= LV_ROWS ? rem : rem & (uint32_t)((2ull << __fns(rem, 0, LV_ROWS)) - 1ull);
-          rem &= ~hb;
-          if (hb & (1u << lane)) {
-            float* row = srows[__popc(hb & lt)];
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              reinterpret_cast<float4*>(row)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          }
-          __syncwarp();
-          int row_i = 0;
-#else
           if (hit) {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               reinterpret_cast<float4*>(srows[lane])[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
           __syncwarp();
-#endif
           do {
             const int Lz = __ffs(hb) - 1;
             hb &= hb - 1u;
-#if LV_ROWS < 32
-            const float f = srows[row_i++][lane];
-#else
             const float f = srows[Lz][lane];
-#endif
             const float tsz = __shfl_sync(0xffffffffu, ts, Lz);
             uint64_t tkz = __shfl_sync(0xffffffffu, tk, Lz);
             int cz = __shfl_sync(0xffffffffu, cnt, Lz);
@@ -581,9 +545,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (count_stats && lane == 0) atomicAdd(a.stats + 1, (unsigned long long)__popc(kb));
           } while (hb != 0u);
           __syncwarp();
-#if LV_ROWS < 32
-          }
-#endif
         }
       }
       tiles_before += n_t;
