@@ -194,7 +194,7 @@ T* carve(uint8_t*& p, size_t count) {
 // Chunks of the given segments (tile ranges) so that units = P * QP spread evenly over the grid.
 // With stride > 1 only every stride-th tile of a segment is scanned (sample stage); the scanned
 // tiles are numbered consecutively from *sample_base (block-maximum rows, lv_score.cu).
-constexpr double kUnitCostTiles = 4.0;
+constexpr double kUnitCostTiles = 16.0;   // tools/gpu_unitcost.sh: flat from 4 to 16 at 1M rows, 16 best at 10M
 
 void make_chunks(const std::vector<std::pair<int, int>>& segs, const std::vector<int>& segc, int QP, int G,
                  int maxChunks, std::vector<int32_t>* out, int stride = 1, int* sample_base = nullptr) {
@@ -208,6 +208,7 @@ void make_chunks(const std::vector<std::pair<int, int>>& segs, const std::vector
   if (ntiles == 0) return;
   double best_eff = -1;
   int best_len = ntiles;
+  const double unit_cost = env_double("LV_UNIT_COST", kUnitCostTiles);   // probe knob
   const int maxP = std::min(ntiles, 4096);
   for (int target = 1; target <= maxP; ++target) {
     const int len = (ntiles + target - 1) / target;
@@ -216,10 +217,10 @@ void make_chunks(const std::vector<std::pair<int, int>>& segs, const std::vector
     if (P > maxChunks) continue;
     const int64_t units = (int64_t)P * QP;
     const int g = (int)std::min<int64_t>(G, units);
-    // time ~ max units on one CTA x (tiles per unit + the unit boundary's cost, ~4 tiles: slot
+    // time ~ max units on one CTA x (tiles per unit + the unit boundary's cost: slot
     // claim/release, list-state flush and the epilogue's barrier; measured: 2.54 -> 2.36 ms on
     // cfg 2 going from 103 to ~30 chunks); efficiency vs perfect spread
-    const double per_cta = (double)((units + g - 1) / g) * (len + kUnitCostTiles);
+    const double per_cta = (double)((units + g - 1) / g) * (len + unit_cost);
     const double ideal = (double)ntiles * QP / G;
     double eff = ideal / per_cta - 1e-4 * (double)P / (double)ntiles;   // prefer fewer chunks on ties
     if (eff > best_eff + 1e-9) {
