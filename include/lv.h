@@ -136,7 +136,10 @@ lv_status lv_index_create(lv_index** out, int32_t D, int32_t d, int32_t C,
  * Layout: rows are stably sorted by cluster (counting sort), each
  * cluster segment is padded to a multiple of 128 rows, so every 128-row tile of X_low
  * belongs to one cluster; perm maps sorted position -> original id (-1 = padding).
- * x_low = RNE(fp32 FMA product) to low_dtype.  X is converted to full_dtype.
+ * x_low = RNE(fp32-faithful product) to low_dtype: K6 on tcgen05, X rows and B split into three
+ * bf16 planes (24 significant bits), six plane products accumulated in fp32 TMEM (DESIGN.md
+ * R18; LV_K6_PLANES=2 opts into a two-plane split for bf16 storage, LV_K6=simt into an fp32
+ * CUDA-core GEMM).  X is converted to full_dtype.  lv_encode_timing reports the kernel times.
  * The caller may free X after the call returns (the call synchronises `stream`).
  * Replaces any previous contents.  Errors: LV_EINVAL, LV_EDATA, LV_ENOMEM, LV_ECUDA.
  */
