@@ -44,6 +44,7 @@ struct PlanCache {
   uint64_t* tau2 = nullptr;    // sampled: per-query repair threshold
   float* bmax = nullptr;       // sampled: block maxima of the sample stage
   int32_t* fail = nullptr;     // [4]: fail counts of the two checks, repair row counts
+  int32_t* unit_ctr = nullptr; // [kMaxScans]: zeroed work-unit counter per scan launch (dynamic unit order)
   int32_t* fail_list = nullptr;   // [2][m_pad]
   int32_t* slot_busy = nullptr;
   int32_t* sel_ids = nullptr;  // [m_pad][R]
@@ -194,6 +195,7 @@ T* carve(uint8_t*& p, size_t count) {
 // Chunks of the given segments (tile ranges) so that units = P * QP spread evenly over the grid.
 // With stride > 1 only every stride-th tile of a segment is scanned (sample stage); the scanned
 // tiles are numbered consecutively from *sample_base (block-maximum rows, lv_score.cu).
+constexpr int kMaxScans = 64;   // scan launches per lv_search with their own unit counter
 constexpr double kUnitCostTiles = 16.0;   // tools/gpu_unitcost.sh: flat from 4 to 16 at 1M rows, 16 best at 10M
 
 void make_chunks(const std::vector<std::pair<int, int>>& segs, const std::vector<int>& segc, int QP, int G,
@@ -726,7 +728,7 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     const size_t mp = pl.m_pad;
     size_t need = (mp * Cd * 2 + 256) + ((size_t)3 * mp * ix->Kp * 2 + 256) + ((size_t)NS2 * mp * pl.Cap * 8 + 256) +
                   ((size_t)NS2 * mp * 4 + 256) +
-                  ((size_t)NS2 * mp * 8 + 256) + ((size_t)pl.QP * 4 + 256) + (16 * 4 + 256) +
+                  ((size_t)NS2 * mp * 8 + 256) + ((size_t)pl.QP * 4 + 256) + (16 * 4 + 256) + (kMaxScans * 4 + 256) +
                   (mp * (size_t)R * 4 + 256) + (mp * 4 + 256) +
                   (nchunk_ints * 4 + 256 * (pl.chunks.size() + 2));
     if (pl.sampled)
@@ -752,6 +754,7 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     pc.sel_ids = carve<int32_t>(p, mp * (size_t)R);
     pc.sel_n = carve<int32_t>(p, mp);
     pc.fail = carve<int32_t>(p, 16);
+    pc.unit_ctr = carve<int32_t>(p, kMaxScans);
     pc.zero_hi = p;
     if (pl.sampled) {
       pc.Qr = carve<uint16_t>(p, mp * Cd);
@@ -844,11 +847,16 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
     if (!dstats) LV_CUDA(cudaMalloc(&dstats, 8 * sizeof(unsigned long long)));
     sa.stats = dstats;
   }
+  int nscan = 0;
+  const bool dyn_units = env_double("LV_DYN_UNITS", 1.0) != 0.0;
   auto scan = [&](const int32_t* info, const std::vector<int32_t>& host_chunks, int qtiles, const char* what) -> lv_status {
     sa.P = (int)(host_chunks.size() / lv::kChunkInts);
     sa.chunk_info = info;
     const int grid = (int)std::min<int64_t>(nsm, (int64_t)sa.P * qtiles);
     if (grid <= 0) return LV_OK;
+    // dynamic unit order (LV_DYN_UNITS, default on): a fresh zeroed counter per launch
+    sa.unit_ctr = (dyn_units && nscan < kMaxScans) ? pc.unit_ctr + nscan : nullptr;
+    ++nscan;
     if (sa.stats) LV_CUDA(cudaMemsetAsync(sa.stats, 0, 8 * sizeof(unsigned long long), s));
     LV_CUDA(lv::launch_score(&ix->tmap_xlow_s, sa, ix->low == LV_BF16, grid, pl.smem, s));
     ++launches;

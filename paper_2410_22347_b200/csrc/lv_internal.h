@@ -43,6 +43,7 @@ struct ScoreArgs {
   int flags;                   // debug: bit0 = epilogue skips top-R (MMA/TMA throughput probe),
                                //        bit1 = count events into stats, bit2 = detect hits but drop them
   unsigned long long* stats;   // debug counters [8] or nullptr: hit warp-tiles, appends, compactions, wait spins
+  int32_t* unit_ctr;           // zeroed work-unit counter of this launch (dynamic unit order), or nullptr (static)
 };
 
 cudaError_t launch_score(const CUtensorMap* tmap_xlow, const ScoreArgs& a, bool bf16, int grid, size_t smem,

@@ -46,6 +46,7 @@ struct ScoreSmemLayout {
   uint32_t b_off, epi_off, bar_off, total;
 };
 constexpr int kMaxAcc = 8;
+constexpr int kUQ = 4;                 // work-unit queue depth (dynamic unit order)
 
 __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
@@ -73,7 +74,8 @@ __host__ __device__ inline ScoreSmemLayout score_smem_layout(int d, int stages) 
   L.epi_off = align_up((uint32_t)stages * (uint32_t)kTileN * (uint32_t)d * 2u, 1024);
   L.bar_off = align_up(L.epi_off + (uint32_t)sizeof(EpiShared), 16);
   // barriers: b_full[stages], b_empty[stages], acc_full[kMaxAcc], acc_empty[kMaxAcc], a_full[2], tmem ptr
-  L.total = L.bar_off + 8u * (2 * stages + 2 * kMaxAcc + 2) + 16;
+  // + the unit queue: uq_full[kUQ], uq_empty[kUQ] and kUQ unit ids
+  L.total = L.bar_off + 8u * (2 * stages + 2 * kMaxAcc + 2 + 2 * kUQ) + 16 + 4u * kUQ;
   return L;
 }
 
@@ -242,7 +244,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = bars + 2 * a.stages;
   uint64_t* acc_empty = acc_full + kMaxAcc;
   uint64_t* a_full = acc_empty + kMaxAcc;
-  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(a_full + 2);
+  uint64_t* uq_full = a_full + 2;      // unit queue (a.unit_ctr): slot s holds the CTA's i-th unit, i % kUQ = s
+  uint64_t* uq_empty = uq_full + kUQ;
+  int32_t* uq = reinterpret_cast<int32_t*>(uq_empty + kUQ);
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(uq + kUQ);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -265,6 +270,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc::mbar_init(a_full + 0, kEpiWarps);
     tc::mbar_init(a_full + 1, kEpiWarps);
+    for (int j = 0; j < kUQ; ++j) {
+      tc::mbar_init(uq_full + j, 1);
+      tc::mbar_init(uq_empty + j, 1 + kEpiWarps);   // the MMA warp and every epilogue warp read each slot
+    }
     for (int j = 0; j < 4; ++j) S.jc[j] = 0;
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmap_xlow);
@@ -277,13 +286,53 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr bool kSingleA = score_single_a(kD);
   const uint32_t acc_col0 = (uint32_t)score_a_cols(kD);   // A buffer(s) occupy columns [0, acc_col0)
   const uint32_t acc_full_u = tc::smem_u32(acc_full), acc_empty_u = tc::smem_u32(acc_empty);
+  // Work units of this CTA in order: static (blockIdx.x + i * gridDim.x) or, with a.unit_ctr,
+  // dynamic: the TMA thread takes units from the launch's global counter as it needs them (CTAs
+  // that drew slow units take fewer) and publishes them through a kUQ-slot queue; an id >= nunits
+  // ends the sequence.  unit_at(i) is the CTA's i-th unit; unit_release(i) frees its slot (once
+  // per consumer warp, after its last read).
+  const bool dyn = a.unit_ctr != nullptr;
+  auto unit_at = [&](int i) -> int {
+    if (!dyn) return (int)blockIdx.x + i * (int)gridDim.x;
+    tc::mbar_wait_sleep(uq_full + i % kUQ, (uint32_t)(i / kUQ) & 1u);
+    return *reinterpret_cast<volatile int32_t*>(uq + i % kUQ);
+  };
+  auto unit_release = [&](int i) {
+    if (dyn) {
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(uq_empty + i % kUQ);
+    }
+  };
 
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer (X_low tiles)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      int pushed = 0;   // dynamic order: units published so far
+      auto push = [&]() -> int {
+        const int sl = pushed % kUQ;
+        if (pushed >= kUQ) tc::mbar_wait_sleep(uq_empty + sl, (uint32_t)(pushed / kUQ - 1) & 1u);
+        int u = atomicAdd(a.unit_ctr, 1);
+        if (u > nunits) u = nunits;
+        *reinterpret_cast<volatile int32_t*>(uq + sl) = u;
+        tc::mbar_arrive(uq_full + sl);   // release: the id is visible to the waiting consumers
+        ++pushed;
+        return u;
+      };
+      // keep two units published ahead of the one being loaded: the epilogue writes unit i+1's A
+      // operand while it works on unit i
+      int u_cur = dyn ? push() : (int)blockIdx.x;
+      int u_nxt = dyn ? (u_cur < nunits ? push() : nunits) : u_cur + (int)gridDim.x;
+      for (int u = u_cur; u < nunits; u = u_cur) {
+        if (dyn) {
+          const int u_nn = u_nxt < nunits ? push() : nunits;
+          u_cur = u_nxt;
+          u_nxt = u_nn;
+        } else {
+          u_cur = u_nxt;
+          u_nxt += (int)gridDim.x;
+        }
         const int c = u / QT;
         const int* ci = a.chunk_info + kChunkInts * c;
         const int t0 = ci[0], t1 = ci[1], ts_ = ci[3];
@@ -306,7 +355,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     int i = 0;
     const bool issuer = tc::elect_one();   // the single lane that issues tcgen05.mma / commit
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
+    for (;; ++i) {
+      const int u = unit_at(i);
+      unit_release(i);
+      if (u >= nunits) break;
       const int c = u / QT;
       const int* ci = a.chunk_info + kChunkInts * c;
       const int t0 = ci[0], t1 = ci[1], ts_ = ci[3];
@@ -390,13 +442,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(a_full + b);
     };
-    if ((int)blockIdx.x < nunits) write_A(blockIdx.x, 0);
+    int u_next = unit_at(0);   // the unit after the current one (its A operand goes in early)
+    if (u_next < nunits) write_A(u_next, 0);
     const uint32_t tm_lane = tmem_base + lane_base + acc_col0;
     int tiles_before = 0;   // tiles of this CTA's earlier units (global tile ordinal base)
     int pending = -1;       // a job index already taken that belongs to a later unit
     int i = 0;
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
-      if (!kSingleA && u + (int)gridDim.x < nunits) write_A(u + gridDim.x, (i + 1) & 1);
+    for (;; ++i) {
+      const int u = u_next;
+      unit_release(i);
+      if (u >= nunits) break;
+      u_next = unit_at(i + 1);
+      if (!kSingleA && u_next < nunits) write_A(u_next, (i + 1) & 1);
       const int c = u / QT, qt = u % QT;
       const int* ci = a.chunk_info + kChunkInts * c;
       const int t0 = ci[0], t1 = ci[1], tstride = ci[3], sbase = ci[4];
@@ -564,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // single-buffered A: every job of this unit saw its tile committed, so the MMAs of this unit
       // are complete and its A buffer can take the next unit's operand
-      if (kSingleA && u + (int)gridDim.x < nunits) write_A(u + gridDim.x, 0);
+      if (kSingleA && u_next < nunits) write_A(u_next, 0);
     }
   }
   tc::tc_fence_before();
