@@ -103,6 +103,23 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def bind_to_gpu_numa(local_rank, log=print):
+    """Pin this process to the CPU cores NVML reports as closest to its GPU, before any pinned host
+    buffer is allocated, so the e2e host<->device copies run from the GPU's NUMA node."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(local_rank)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * w + b for w, word in enumerate(words) for b in range(64) if (word >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            log(f"[bench] bound to {len(cpus)} CPUs near GPU {local_rank}")
+    except Exception as e:   # no NVML / no permission: keep the default placement
+        log(f"[bench] NUMA binding skipped: {e}")
+
+
 def build_index(cfg, rank=0, world=1, log=print, family=None):
     """Generate the config's data, fit with the product path (lv_fit_stats + host eig, GPU k-means
     for GleanVec), encode.  Returns dict with index, device Q, host Q, data."""
@@ -319,6 +336,7 @@ def main():
         return
 
     import torch
+    bind_to_gpu_numa(local, log)
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
