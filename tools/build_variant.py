@@ -1,7 +1,9 @@
-"""Experiment builds: liblv with extra -D defines on lv_score.cu (the other objects are the main
-build's), written to paper_2410_22347_b200/variants/liblv_<name>.so; select with LV_LIB=<path>.
+"""Experiment builds: liblv with extra -D defines on one source (default lv_score.cu; VARIANT_SRC
+picks another; the other objects are the main build's), written to
+paper_2410_22347_b200/variants/liblv_<name>.so; select with LV_LIB=<path>.
 
   python tools/build_variant.py spin_mma -DLV_MMA_SPIN
+  VARIANT_SRC=lv_rerank.cu python tools/build_variant.py k5g4 -DLV_K5_G4
 """
 import os
 import subprocess
@@ -16,12 +18,13 @@ def main():
     B.build()
     out_dir = os.path.join(B.HERE, "variants")
     os.makedirs(out_dir, exist_ok=True)
-    obj = os.path.join(out_dir, f"lv_score_{name}.o")
-    r = subprocess.run([B.NVCC, *B.FLAGS, *defs, "-c", os.path.join(B.CSRC, "lv_score.cu"), "-o", obj],
+    src = os.environ.get("VARIANT_SRC", "lv_score.cu")
+    obj = os.path.join(out_dir, f"{src[:-3]}_{name}.o")
+    r = subprocess.run([B.NVCC, *B.FLAGS, *defs, "-c", os.path.join(B.CSRC, src), "-o", obj],
                        capture_output=True, text=True)
     if r.returncode:
         sys.exit(r.stderr)
-    objs = [obj] + [os.path.join(B.CSRC, s.replace(".cu", ".o")) for s in B.SOURCES if s != "lv_score.cu"]
+    objs = [obj] + [os.path.join(B.CSRC, s.replace(".cu", ".o")) for s in B.SOURCES if s != src]
     lib = os.path.join(out_dir, f"liblv_{name}.so")
     r = subprocess.run([B.NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", lib],
                        capture_output=True, text=True)
