@@ -267,7 +267,8 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   // 16 slots: the main scan never needs more than ~5 concurrent CTAs per query tile, but a repair
   // scan (one query tile) runs on as many CTAs as there are slots (cfg 2: a one-query repair
   // 0.56 -> 0.35 ms against 8 slots; no change when nothing is repaired)
-  const int ns = std::min((int)env_double("LV_SLOTS", 16.0), ns_smem);
+  // (small databases take the staged path, where 8 slots keep the merges and K4 cheaper)
+  const int ns = std::min((int)env_double("LV_SLOTS", ntiles >= 1024 ? 16.0 : 8.0), ns_smem);
   if (ns < 1) return fail(LV_EUNSUPPORTED, "R=%d too large for the merge", R);
   const int max_chunks = (int)env_double("LV_MAX_CHUNKS", 1e9);   // probe knob (units per chunk sweep)
   const int ns_target = ns;
