@@ -27,6 +27,9 @@
  *    Asynchronous kernel faults surface at the caller's next synchronisation.
  *  - There is no CPU fallback: if the device is not an sm_100 GPU every compute
  *    call returns LV_EUNSUPPORTED.
+ *  - An index is not thread-safe: its search workspace, plan cache and staging buffers are
+ *    shared by every call on it.  Use one index from one host thread and one stream at a time;
+ *    when the stream changes, make the new stream wait on the old one (an event) first.
  */
 #ifndef LV_H_
 #define LV_H_
@@ -121,8 +124,9 @@ lv_status lv_fit_stats(const float* Q_learn, int64_t m_learn,
  *                     B_c (database side, g_c(x) = B_c x); copied.
  *   low_dtype         LV_BF16 or LV_F16: storage of x_low and q' (P:129 reduced footprint)
  *   full_dtype        LV_F32 or LV_F16: storage of the full vectors used by the re-rank
- * Constraints: 1 <= d <= D, d % 32 == 0, d <= 256, D % 4 == 0 (LV_F32) / D % 8 == 0 (LV_F16),
+ * Constraints: 32 <= d <= min(D, 192), d % 32 == 0, D % 4 == 0 (LV_F32) / D % 8 == 0 (LV_F16),
  *              1 <= C <= 1024.  Errors: LV_EINVAL, LV_ENOMEM, LV_EUNSUPPORTED.
+ * Synchronises the device (the operand planes are prepared before the call returns).
  */
 lv_status lv_index_create(lv_index** out, int32_t D, int32_t d, int32_t C,
                           lv_dtype low_dtype, lv_dtype full_dtype,
@@ -148,8 +152,9 @@ lv_status lv_encode_database(lv_index* index, const void* X, lv_dtype x_dtype, i
 
 /*
  * lv_project_queries — Alg. 1 line 1 / Alg. 4 preprocess:
- *   Qp[j, c*d:(c+1)*d] = RNE(A_c q_j) to low_dtype, fp32 FMA accumulation.
- *   Q   device fp32 [m, D];  Qp device low_dtype [m, C*d]
+ *   Qp[j, c*d:(c+1)*d] = RNE(A_c q_j) to low_dtype, an fp32-faithful product on tcgen05 (K1: Q and
+ *   A split into three bf16 planes, six plane products accumulated in fp32 TMEM, R18).
+ *   Q   device fp32 [m, D];  Qp device low_dtype [m, C*d_search]  (d_search: lv_index_set_search_dim)
  */
 lv_status lv_project_queries(const lv_index* index, const float* Q, int64_t m, void* Qp,
                              void* stream);
@@ -165,7 +170,14 @@ lv_status lv_project_queries(const lv_index* index, const float* Q, int64_t m, v
  *   Q       device fp32 [m, D]
  *   ids     device int32 [m, k] out (original database ids);  scores device fp32 [m, k] out (r_ji)
  *   dbg     NULL or lv_search_debug* (HOST struct; its pointers are device pointers)
- * Constraints: 1 <= k <= R <= n, R <= 256, m >= 1.  The index must be encoded.
+ * Constraints: 1 <= k <= R <= n, R <= 256, 1 <= m <= 2^24.  The index must be encoded.
+ * Batches: m is processed in query batches of at most LV_MAX_BATCH (env, default 32768) queries,
+ *   which bounds the workspace (~64 x Cap x 8 bytes per query, Cap = min(384, R + 160)); results
+ *   do not depend on the batching.  dbg->raw_scores requires m <= LV_MAX_BATCH.
+ * Synchronisation: none in the steady state.  The first call with a new (batch size, R) plans the
+ *   scan, (re)allocates the workspace and uploads the chunk tables, and synchronises `stream`
+ *   once for that; later calls with the same shape reuse the plan.  dbg->timing = 1 also
+ *   synchronises.
  * Not thread-safe per index (shared workspace).  Errors: LV_EINVAL, LV_ENOMEM, LV_ECUDA.
  */
 lv_status lv_search(lv_index* index, const float* Q, int64_t m, int32_t k, int32_t R,
@@ -174,7 +186,10 @@ lv_status lv_search(lv_index* index, const float* Q, int64_t m, int32_t k, int32
 /*
  * lv_search_host — lv_search with HOST buffers: copies Q_host (fp32 [m, D]) to the device,
  * runs lv_search, copies ids/scores back into HOST arrays [m, k].  Synchronises `stream`.
- * Pinned host memory gives full PCIe bandwidth; pageable memory works.
+ * For m >= 4096 the batch is searched as two query batches: the second batch's upload (on an
+ * internal copy stream) overlaps the first batch's search, the first batch's download the
+ * second's search.  Arguments are checked before any copy is enqueued.
+ * Pinned host memory gives full PCIe bandwidth and the copy/compute overlap; pageable works.
  */
 lv_status lv_search_host(lv_index* index, const float* Q_host, int64_t m, int32_t k, int32_t R,
                          int32_t* ids_host, float* scores_host, void* stream);
@@ -185,6 +200,27 @@ lv_status lv_search_host(lv_index* index, const float* Q_host, int64_t m, int32_
  */
 lv_status lv_assign_tags(const void* X, lv_dtype x_dtype, int64_t n, int32_t D,
                          const float* centres, int32_t C, int32_t* assign, void* stream);
+
+/*
+ * Spherical k-means of GleanVec's index build (Alg. 5 lines 1-2; App. A).
+ *
+ * lv_normalize_rows — x~_i = x_i / ||x_i||, fp32 sum of squares.  X device [n, D]
+ *   (F32/F16), Xn device fp32 [n, D] out (zero rows stay zero).
+ * lv_kmeans_assign — the E-step and the k-means++ distance: for every row i,
+ *   assign[i] = argmax_c <x_i, mu_c> (lowest c on ties; NULL to skip) and best[i] = max_c <x_i, mu_c>
+ *   (NULL to skip), or with accumulate != 0, best[i] = max(best[i], max_c <x_i, mu_c>) (k-means++
+ *   adds one centre at a time; D^2(x) = 2 - 2 best).  fp32 dot products.  centres device fp32 [C, D].
+ * lv_kmeans_centre_sums — the M-step sums: sums[c, :] = sum_{assign[i] = c} x_i and
+ *   counts[c] = #{i : assign[i] = c}; fp32 over 2048-row chunks in row order, chunks summed in
+ *   fp64 in order (deterministic).  sums HOST fp64 [C, D] out, counts HOST int64 [C] out.
+ *   C <= 384.  Synchronises `stream`.  mu_c = sums[c] / ||sums[c]|| is the caller's (C x D) step.
+ */
+lv_status lv_normalize_rows(const void* X, lv_dtype x_dtype, int64_t n, int32_t D, float* Xn, void* stream);
+lv_status lv_kmeans_assign(const void* X, lv_dtype x_dtype, int64_t n, int32_t D, const float* centres,
+                           int32_t C, int32_t* assign, float* best, int32_t accumulate, void* stream);
+lv_status lv_kmeans_centre_sums(const void* X, lv_dtype x_dtype, int64_t n, int32_t D,
+                                const int32_t* assign, int32_t C, double* sums, int64_t* counts,
+                                void* stream);
 
 /*
  * lv_index_set_search_dim — flexible target dimensionality (§3.1, Eq.(10): "select the

@@ -83,9 +83,11 @@ struct lv_index {
   // per-kernel timing (lv_search timing = 2): event groups of 8 marks, pending until collected
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::vector<cudaEvent_t>> ev_pending;
-  // host-buffer staging for lv_search_host
+  // host-buffer staging for lv_search_host: device buffers, a copy stream, its events
   void* hs = nullptr;
   size_t hs_bytes = 0;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t hev[4] = {};
 };
 
 namespace {
@@ -171,20 +173,6 @@ double env_double(const char* name, double dflt) {
   return v ? atof(v) : dflt;
 }
 
-// K1 on tensor cores (lv_proj.cu) unless LV_K1=simt (fp32 CUDA-core GEMM)
-bool k1_tensor() {
-  const char* v = getenv("LV_K1");
-  return !(v && v[0] == 's');
-}
-
-// K6 on tensor cores unless LV_K6=simt
-bool k6_tensor() {
-  const char* v = getenv("LV_K6");
-  return !(v && v[0] == 's');
-}
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
 template <typename T>
 T* carve(uint8_t*& p, size_t count) {
   T* r = reinterpret_cast<T*>(p);
@@ -254,6 +242,8 @@ void make_chunks(const std::vector<std::pair<int, int>>& segs, const std::vector
 // seen so far as its threshold.  Stage sizes are chosen so that a slot's expected appends within
 // a stage (g * R / NS) stay well below its capacity: thresholds are tight from the second stage
 // on and slot compactions are rare.
+constexpr int kMaxSlots = 16;   // 4 sub-lists per slot; K4 / k_tau_merge hold <= 64 sub-lists per query
+
 lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   pl->QP = (int)((m + 127) / 128);   // 128-query tiles (units pair a tile with a database chunk)
   pl->m_pad = pl->QP * 128;
@@ -261,17 +251,7 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   if (pl->Cap < R + 96) return fail(LV_EUNSUPPORTED, "R=%d too large (R <= 256)", R);
   const int ntiles = (int)(ix->n_pad / 128);
   const int G = nsm;
-  // every slot is split in two sub-lists (one per epilogue column half): 2*NS lists per query;
-  // a query tile's concurrently running units claim distinct slots (lv_score.cu)
-  const int ns_smem = (int)((200 * 1024 - (size_t)ix->D * 4) / ((size_t)pl->Cap * 8)) / 2;
-  // 16 slots: the main scan never needs more than ~5 concurrent CTAs per query tile, but a repair
-  // scan (one query tile) runs on as many CTAs as there are slots (cfg 2: a one-query repair
-  // 0.56 -> 0.35 ms against 8 slots; no change when nothing is repaired)
-  // (small databases take the staged path, where 8 slots keep the merges and K4 cheaper)
-  const int ns = std::min((int)env_double("LV_SLOTS", ntiles >= 1024 ? 16.0 : 8.0), ns_smem);
-  if (ns < 1) return fail(LV_EUNSUPPORTED, "R=%d too large for the merge", R);
   const int max_chunks = (int)env_double("LV_MAX_CHUNKS", 1e9);   // probe knob (units per chunk sweep)
-  const int ns_target = ns;
   // segment tile ranges
   std::vector<std::pair<int, int>> seg;
   std::vector<int> segc;
@@ -283,11 +263,52 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
     segc.push_back(c);
     ntot += te - tb;
   }
-  // stage boundaries as cumulative fractions of every segment
+  // sampled-threshold path (DESIGN.md §6): a sample stage over every stride-th tile records
+  // block maxima, a per-query threshold with >= j1 rows above it is selected, one main stage
+  // scans everything with it; queries left with < R candidates are repaired exactly.
+  const int stride = (int)env_double("LV_SAMPLE_STRIDE", 16.0);
+  int nsamp = 0;
+  for (auto& sg : seg) nsamp += (sg.second - sg.first + stride - 1) / stride;
+  // j1: about j1 * stride database rows score above the j1-th largest sampled block maximum, with a
+  // relative spread ~ 1 / sqrt(j1); take the smallest j1 with j1 s - z sqrt(j1) s >= R (z = 2.9:
+  // ~0.2 % of queries need the repair pass), or gamma R / s if LV_SAMPLE_GAMMA is set
+  int j1 = 1;
+  const char* gam = getenv("LV_SAMPLE_GAMMA");
+  if (gam) {
+    j1 = (int)std::ceil(atof(gam) * R / stride);
+  } else {
+    // GleanVec's cluster-sorted rows crowd a query's top rows into its nearest clusters' blocks,
+    // so a block maximum stands for more rows than on unsorted data and the same z fails less
+    // often: z = 2.5 there (cfg 3: 3.17 -> 3.07 ms per search, no repairs), 2.9 for C = 1
+    const double z = env_double("LV_SAMPLE_Z", ix->C > 1 ? 2.5 : 2.9);
+    while ((double)j1 * stride - z * std::sqrt((double)j1) * stride < (double)R) ++j1;
+  }
+  // 32-row sample blocks while the block-maximum array stays small (<= 8192 blocks); coarser
+  // 64-row blocks at the 10M-row sizes, where the array's HBM traffic would cost more than the
+  // tighter threshold saves
+  const bool fine = (int64_t)lv::score_blocks_per_tile(ix->ds, true) * nsamp <= 8192;
+  const int bpt = lv::score_blocks_per_tile(ix->ds, fine);   // block maxima per sampled tile
+  pl->sampled = env_double("LV_SAMPLED", 1.0) != 0.0 && stride >= 2 && nsamp >= 64 && bpt * nsamp >= 8 * j1 &&
+                bpt * nsamp <= 65535;
+  // candidate slots per query tile (each slot = 4 sub-lists, one per epilogue warp group; the
+  // units of one query tile that run concurrently on different CTAs claim distinct slots).  The
+  // sampled path's main scan needs ~5 concurrent CTAs per query tile, its repair scan (one query
+  // tile, planned as NS chunks) runs on NS CTAs: 16 slots (cfg 2: a one-query repair 0.56 -> 0.35
+  // ms against 8); the staged path keeps 8 (cheaper merges and K4).
+  const int ns_smem = (int)((200 * 1024 - (size_t)ix->D * 4) / ((size_t)pl->Cap * 8)) / 2;
+  const int ns_req = (int)env_double("LV_SLOTS", pl->sampled ? 16.0 : 8.0);
+  if (ns_req > kMaxSlots || ns_req < 1)
+    return fail(LV_EUNSUPPORTED, "LV_SLOTS=%d outside [1, %d] (K4 merges at most %d sub-lists)", ns_req, kMaxSlots,
+                4 * kMaxSlots);
+  const int ns = std::min(ns_req, ns_smem);
+  if (ns < 1) return fail(LV_EUNSUPPORTED, "R=%d too large for the merge", R);
+  // stage boundaries as cumulative fractions of every segment (staged path)
   std::vector<double> cum;   // cumulative fraction after each stage
-  if (ntiles >= 64) {
+  if (ntiles >= 64 && !pl->sampled) {
     const double rows = (double)ntot * 128.0;
-    const double lists = 2.0 * ns_target;   // independent candidate lists per query
+    // stage-size scale: 2 NS (the per-query list count of the original two-sub-list slot layout;
+    // the stage sizes were tuned with it and kept when slots got 4 sub-lists)
+    const double lists = 2.0 * ns;
     // stage 0 only has to produce R keys per query: keep it (and so the first merge) small
     double c0 = std::max(2.0 * R, lists * 32.0) * env_double("LV_STAGE_C0", 1.0);
     // growth per stage: bounded by the slot capacity and kept small so that most of the
@@ -322,33 +343,6 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
     make_chunks(part, partc, pl->QP, G, max_chunks, &ch);
     if (!ch.empty()) pl->chunks.push_back(ch);
   }
-  // sampled-threshold path (DESIGN.md §5): a sample stage over every stride-th tile records
-  // block maxima, a per-query threshold with >= j1 rows above it is selected, one main stage
-  // scans everything with it; queries left with < R candidates are repaired exactly.
-  const int stride = (int)env_double("LV_SAMPLE_STRIDE", 16.0);
-  int nsamp = 0;
-  for (auto& sg : seg) nsamp += (sg.second - sg.first + stride - 1) / stride;
-  // j1: about j1 * stride database rows score above the j1-th largest sampled block maximum, with a
-  // relative spread ~ 1 / sqrt(j1); take the smallest j1 with j1 s - z sqrt(j1) s >= R (z = 2.9:
-  // ~0.2 % of queries need the repair pass), or gamma R / s if LV_SAMPLE_GAMMA is set
-  int j1 = 1;
-  const char* gam = getenv("LV_SAMPLE_GAMMA");
-  if (gam) {
-    j1 = (int)std::ceil(atof(gam) * R / stride);
-  } else {
-    // GleanVec's cluster-sorted rows crowd a query's top rows into its nearest clusters' blocks,
-    // so a block maximum stands for more rows than on unsorted data and the same z fails less
-    // often: z = 2.5 there (cfg 3: 3.17 -> 3.07 ms per search, no repairs), 2.9 for C = 1
-    const double z = env_double("LV_SAMPLE_Z", ix->C > 1 ? 2.5 : 2.9);
-    while ((double)j1 * stride - z * std::sqrt((double)j1) * stride < (double)R) ++j1;
-  }
-  // 32-row sample blocks while the block-maximum array stays small (<= 8192 blocks); coarser
-  // 64-row blocks at the 10M-row sizes, where the array's HBM traffic would cost more than the
-  // tighter threshold saves
-  const bool fine = (int64_t)lv::score_blocks_per_tile(ix->ds, true) * nsamp <= 8192;
-  const int bpt = lv::score_blocks_per_tile(ix->ds, fine);   // block maxima per sampled tile
-  pl->sampled = env_double("LV_SAMPLED", 1.0) != 0.0 && stride >= 2 && nsamp >= 64 && bpt * nsamp >= 8 * j1 &&
-                bpt * nsamp <= 65535;
   if (pl->sampled) {
     pl->stride = stride;
     pl->fine_blocks = fine;
@@ -362,7 +356,9 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
     pl->chunks.push_back(ch);
     make_chunks(seg, segc, pl->QP, G, max_chunks, &ch);
     pl->chunks.push_back(ch);
-    make_chunks(seg, segc, 1, G, max_chunks, &pl->repair_chunks);
+    // repairs scan one query tile (rarely more), which at most NS CTAs can work on at once (one
+    // slot each): NS longer chunks instead of G short ones (no CTAs spinning on slot claims)
+    make_chunks(seg, segc, 1, ns, max_chunks, &pl->repair_chunks);
   }
   int pmax = 0;
   pl->total_units = 0;
@@ -589,7 +585,6 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
   cudaEvent_t* ev = evs.e;
   for (int i = 0; i < 4; ++i) LV_CUDA(cudaEventCreate(&ev[i]));
   LV_CUDA(cudaEventRecord(ev[0], s));
-  int32_t* perm_tmp = nullptr;
   if (C > 1) {
     const int nb = (int)((n + lv::kSortBlock - 1) / lv::kSortBlock);
     int32_t *hist = nullptr, *bad = nullptr;
@@ -615,7 +610,6 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
     LV_CUDA(lv::launch_cluster_scatter(assign, n, C, base, nb, ix->perm, s));
     LV_CUDA(cudaStreamSynchronize(s));
     cudaFree(hist); cudaFree(base); cudaFree(seg); cudaFree(bad);
-    (void)perm_tmp;
   } else {
     ix->n_pad = (n + 127) / 128 * 128;
     hseg[0] = 0;
@@ -665,12 +659,8 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
   const size_t fsz = ix->full == LV_F16 ? 2 : 4;
   if (cudaMalloc(&ix->X_full, fsz * n * ix->D) != cudaSuccess) return fail(LV_ENOMEM, "X_full");
   LV_CUDA(cudaEventRecord(ev[1], s));
-  if (k6_tensor())
-    LV_CUDA(lv::launch_encode_tc(&ix->tmap_b, X, x_dtype == LV_F16, ix->D, ix->Kp, ix->d, ix->C * ix->d, ix->perm, dwrow,
-                                 dorder, nt, ix->X_low, ix->low == LV_BF16, env_double("LV_K6_PLANES", 3.0) >= 3.0, s));
-  else
-    LV_CUDA(lv::launch_rows_gemm(X, x_dtype == LV_F16, ix->D, ix->perm, n, ix->n_pad, ix->B, ix->D, dwrow, ix->d,
-                                 ix->X_low, ix->low, ix->d, ix->n_pad, s));
+  LV_CUDA(lv::launch_encode_tc(&ix->tmap_b, X, x_dtype == LV_F16, ix->D, ix->Kp, ix->d, ix->C * ix->d, ix->perm, dwrow,
+                               dorder, nt, ix->X_low, ix->low == LV_BF16, env_double("LV_K6_PLANES", 3.0) >= 3.0, s));
   LV_CUDA(cudaEventRecord(ev[2], s));
   LV_CUDA(lv::launch_convert(X, x_dtype == LV_F16, ix->X_full, ix->full == LV_F16, n * ix->D, s));
   LV_CUDA(cudaEventRecord(ev[3], s));
@@ -691,10 +681,6 @@ lv_status lv_project_queries(const lv_index* ix, const float* Q, int64_t m, void
   if (m > (1 << 24)) return fail(LV_EINVAL, "lv_project_queries: m too large");
   cudaStream_t s = (cudaStream_t)stream;
   const int Cd = ix->C * ix->ds;   // search width (C = 1 when ds < d: the first ds rows of A)
-  if (!k1_tensor()) {
-    LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, m, ix->A, ix->D, nullptr, Cd, Qp, ix->low, Cd, m, s));
-    return LV_OK;
-  }
   const int64_t m_pad = (m + 127) / 128 * 128;
   void* planes = nullptr;
   LV_CUDA(cudaMallocAsync(&planes, (size_t)3 * m_pad * ix->Kp * 2, s));
@@ -711,15 +697,44 @@ lv_status lv_project_queries(const lv_index* ix, const float* Q, int64_t m, void
   return LV_OK;
 }
 
-lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t R, int32_t* ids, float* scores,
-                    lv_search_debug* dbg, void* stream) {
-  int nsm = 0;
-  lv_status st = check_device(&nsm);
-  if (st) return st;
-  if (!ix || !Q || !ids || !scores || m <= 0) return fail(LV_EINVAL, "lv_search: bad arguments");
+// Query batches of at most LV_MAX_BATCH (default 32768) queries bound the search workspace
+// (candidate lists ~ 64 x Cap x 8 bytes per query).
+static int64_t max_batch() {
+  const int64_t v = (int64_t)env_double("LV_MAX_BATCH", 32768.0);
+  return std::max<int64_t>(128, v / 128 * 128);
+}
+
+static lv_status check_search_args(const lv_index* ix, int64_t m, int32_t k, int32_t R) {
+  if (!ix || m <= 0) return fail(LV_EINVAL, "lv_search: bad arguments");
   if (ix->n <= 0) return fail(LV_EINVAL, "lv_search: index not encoded");
   if (k < 1 || k > R || R > 256 || R > ix->n) return fail(LV_EINVAL, "lv_search: need 1 <= k <= R <= min(n, 256)");
   if (m > (1 << 24)) return fail(LV_EINVAL, "lv_search: m too large");
+  return LV_OK;
+}
+
+// Batch b covers query rows [off_b, off_b + mb): off_b = b * mb, except the last batch, which ends
+// at m (it may overlap the previous one; overlapping rows are recomputed with identical results,
+// so every batch has the same shape and reuses one plan).
+static void batch_layout(int64_t m, int64_t maxB, int64_t* nb, int64_t* mb) {
+  if (m <= maxB) {
+    *nb = 1;
+    *mb = m;
+    return;
+  }
+  int64_t n = (m + maxB - 1) / maxB;
+  const int64_t b = ((m + n - 1) / n + 127) / 128 * 128;
+  *mb = std::min(b, m);
+  *nb = (m + *mb - 1) / *mb;
+}
+
+// One search over m <= the batch limit (lv_search splits larger batches).
+static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t R, int32_t* ids,
+                              float* scores, lv_search_debug* dbg, void* stream) {
+  int nsm = 0;
+  lv_status st = check_device(&nsm);
+  if (st) return st;
+  if (!Q || !ids || !scores) return fail(LV_EINVAL, "lv_search: bad arguments");
+  if ((st = check_search_args(ix, m, k, R))) return st;
   cudaStream_t s = (cudaStream_t)stream;
   const int Cd = ix->C * ix->ds;   // search width (lv_index_set_search_dim)
   PlanCache& pc = ix->plan;
@@ -812,16 +827,10 @@ lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t 
   int launches = 0;
   LV_CUDA(cudaMemsetAsync(pc.zero_lo, 0, pc.zero_hi - pc.zero_lo, s));
   // K1 projection (rows >= m are zero)
-  if (k1_tensor()) {
-    LV_CUDA(lv::launch_split3(Q, m, pl.m_pad, ix->D, ix->Kp, pc.Qplanes, s));
-    LV_CUDA(lv::launch_proj_tc(&pc.tmap_q, &ix->tmap_a, pl.m_pad, Cd, ix->C * ix->d, ix->Kp, Qp, Cd, pl.m_pad,
-                               ix->low == LV_BF16, s));
-    launches += 2;
-  } else {
-    LV_CUDA(lv::launch_rows_gemm(Q, 0, ix->D, nullptr, m, pl.m_pad, ix->A, ix->D, nullptr, Cd, Qp, ix->low, Cd,
-                                 pl.m_pad, s));
-    ++launches;
-  }
+  LV_CUDA(lv::launch_split3(Q, m, pl.m_pad, ix->D, ix->Kp, pc.Qplanes, s));
+  LV_CUDA(lv::launch_proj_tc(&pc.tmap_q, &ix->tmap_a, pl.m_pad, Cd, ix->C * ix->d, ix->Kp, Qp, Cd, pl.m_pad,
+                             ix->low == LV_BF16, s));
+  launches += 2;
   if ((st = mark(1))) return st;
   lv::ScoreArgs sa;
   sa.Qp = Qp;
@@ -1040,41 +1049,179 @@ lv_status lv_timing_collect(lv_index* ix, float* kernel_ms, int32_t* calls) {
   return LV_OK;
 }
 
+lv_status lv_search(lv_index* ix, const float* Q, int64_t m, int32_t k, int32_t R, int32_t* ids, float* scores,
+                    lv_search_debug* dbg, void* stream) {
+  lv_status st = check_device();
+  if (st) return st;
+  if (!Q || !ids || !scores) return fail(LV_EINVAL, "lv_search: bad arguments");
+  if ((st = check_search_args(ix, m, k, R))) return st;
+  int64_t nb, mb;
+  batch_layout(m, max_batch(), &nb, &mb);
+  if (nb == 1) return search_batch(ix, Q, m, k, R, ids, scores, dbg, stream);
+  if (dbg && dbg->raw_scores) return fail(LV_EINVAL, "lv_search: raw_scores needs m <= LV_MAX_BATCH");
+  lv_search_debug acc{};
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t off = (b + 1 < nb) ? b * mb : m - mb;
+    lv_search_debug db{};
+    if (dbg) {
+      db = *dbg;
+      if (dbg->cand_ids) db.cand_ids = dbg->cand_ids + off * R;
+      if (dbg->cand_scores) db.cand_scores = dbg->cand_scores + off * R;
+    }
+    st = search_batch(ix, Q + off * ix->D, mb, k, R, ids + off * k, scores + off * k, dbg ? &db : nullptr, stream);
+    if (st) return st;
+    if (dbg) {
+      for (int i = 0; i < 4; ++i) acc.phase_ms[i] += db.phase_ms[i];
+      for (int i = 0; i < 8; ++i) acc.kernel_ms[i] += db.kernel_ms[i];
+      acc.failed[0] += db.failed[0];
+      acc.failed[1] += db.failed[1];
+      acc.launches += db.launches;
+      acc.units += db.units;
+      acc.slots = db.slots;
+      acc.grid = db.grid;
+      acc.path = db.path;
+    }
+  }
+  if (dbg) {
+    for (int i = 0; i < 4; ++i) dbg->phase_ms[i] = acc.phase_ms[i];
+    for (int i = 0; i < 8; ++i) dbg->kernel_ms[i] = acc.kernel_ms[i];
+    dbg->failed[0] = acc.failed[0];
+    dbg->failed[1] = acc.failed[1];
+    dbg->launches = acc.launches;
+    dbg->units = acc.units;
+    dbg->slots = acc.slots;
+    dbg->grid = acc.grid;
+    dbg->path = acc.path;
+  }
+  return LV_OK;
+}
+
 lv_status lv_search_host(lv_index* ix, const float* Q_host, int64_t m, int32_t k, int32_t R, int32_t* ids_host,
                          float* scores_host, void* stream) {
   lv_status st = check_device();
   if (st) return st;
-  if (!ix || !Q_host || !ids_host || !scores_host || m <= 0 || k <= 0) return fail(LV_EINVAL, "lv_search_host: bad arguments");
+  if (!Q_host || !ids_host || !scores_host) return fail(LV_EINVAL, "lv_search_host: bad arguments");
+  if ((st = check_search_args(ix, m, k, R))) return st;   // before any copy is enqueued
   cudaStream_t s = (cudaStream_t)stream;
   const size_t qb = (size_t)m * ix->D * 4, ob = (size_t)m * k * 4;
-  const size_t need = qb + 2 * ob + 512;
+  const size_t need = qb + 2 * ob + 1024;
   if (need > ix->hs_bytes) {
+    LV_CUDA(cudaStreamSynchronize(s));
     cudaFree(ix->hs);
     ix->hs = nullptr;
     ix->hs_bytes = 0;
     if (cudaMalloc(&ix->hs, need) != cudaSuccess) return fail(LV_ENOMEM, "lv_search_host: staging");
     ix->hs_bytes = need;
   }
+  if (!ix->cs) {
+    LV_CUDA(cudaStreamCreateWithFlags(&ix->cs, cudaStreamNonBlocking));
+    for (int i = 0; i < 4; ++i) LV_CUDA(cudaEventCreateWithFlags(&ix->hev[i], cudaEventDisableTiming));
+  }
   uint8_t* p = reinterpret_cast<uint8_t*>(ix->hs);
   float* dQ = carve<float>(p, (size_t)m * ix->D);
   int32_t* dI = carve<int32_t>(p, (size_t)m * k);
   float* dS = carve<float>(p, (size_t)m * k);
-  LV_CUDA(cudaMemcpyAsync(dQ, Q_host, qb, cudaMemcpyHostToDevice, s));
-  st = lv_search(ix, dQ, m, k, R, dI, dS, nullptr, stream);
-  if (st) return st;
-  LV_CUDA(cudaMemcpyAsync(ids_host, dI, ob, cudaMemcpyDeviceToHost, s));
-  LV_CUDA(cudaMemcpyAsync(scores_host, dS, ob, cudaMemcpyDeviceToHost, s));
+  // two query batches when the batch is large: batch 1's upload (copy stream) overlaps batch 0's
+  // search, batch 0's download overlaps batch 1's search
+  int64_t nb = 1, mb = m;
+  if (m >= 4096) batch_layout(m, std::min<int64_t>(max_batch(), (m + 1) / 2 + 127), &nb, &mb);
+  if (nb > 2) batch_layout(m, max_batch(), &nb, &mb);
+  const int64_t D = ix->D;
+  std::vector<int64_t> lo(nb), hi(nb), off(nb);
+  for (int64_t b = 0; b < nb; ++b) {
+    off[b] = (b + 1 < nb) ? b * mb : m - mb;
+    lo[b] = b == 0 ? 0 : hi[b - 1];   // rows first needed by batch b
+    hi[b] = off[b] + mb;
+  }
+  cudaEvent_t* ev = ix->hev;
+  LV_CUDA(cudaEventRecord(ev[2], s));          // the copy stream starts after prior work on s
+  LV_CUDA(cudaStreamWaitEvent(ix->cs, ev[2], 0));
+  for (int64_t b = 0; b < nb; ++b) {
+    // uploads: batch b's new rows on the copy stream
+    LV_CUDA(cudaMemcpyAsync(dQ + lo[b] * D, Q_host + lo[b] * D, (size_t)(hi[b] - lo[b]) * D * 4, cudaMemcpyHostToDevice,
+                            ix->cs));
+    if (b == 0) LV_CUDA(cudaEventRecord(ev[0], ix->cs));
+  }
+  LV_CUDA(cudaEventRecord(ev[1], ix->cs));
+  int64_t done = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    LV_CUDA(cudaStreamWaitEvent(s, ev[b == 0 ? 0 : 1], 0));
+    st = search_batch(ix, dQ + off[b] * D, mb, k, R, dI + off[b] * k, dS + off[b] * k, nullptr, stream);
+    if (st) {
+      cudaStreamSynchronize(ix->cs);
+      return st;
+    }
+    // downloads of the rows no later batch rewrites: [done, off[b + 1]) (the last batch: to m)
+    const int64_t r1 = (b + 1 < nb) ? off[b + 1] : m;
+    LV_CUDA(cudaEventRecord(ev[3], s));
+    LV_CUDA(cudaStreamWaitEvent(ix->cs, ev[3], 0));
+    if (r1 > done) {
+      LV_CUDA(cudaMemcpyAsync(ids_host + done * k, dI + done * k, (size_t)(r1 - done) * k * 4, cudaMemcpyDeviceToHost,
+                              ix->cs));
+      LV_CUDA(cudaMemcpyAsync(scores_host + done * k, dS + done * k, (size_t)(r1 - done) * k * 4,
+                              cudaMemcpyDeviceToHost, ix->cs));
+      done = r1;
+    }
+  }
+  LV_CUDA(cudaStreamSynchronize(ix->cs));
   LV_CUDA(cudaStreamSynchronize(s));
   return LV_OK;
 }
 
 lv_status lv_assign_tags(const void* X, lv_dtype x_dtype, int64_t n, int32_t D, const float* centres, int32_t C,
                          int32_t* assign, void* stream) {
+  return lv_kmeans_assign(X, x_dtype, n, D, centres, C, assign, nullptr, 0, stream);
+}
+
+lv_status lv_kmeans_assign(const void* X, lv_dtype x_dtype, int64_t n, int32_t D, const float* centres, int32_t C,
+                           int32_t* assign, float* best, int32_t accumulate, void* stream) {
   lv_status st = check_device();
   if (st) return st;
-  if (!X || !centres || !assign || n <= 0 || D <= 0 || C < 1) return fail(LV_EINVAL, "lv_assign_tags: bad arguments");
-  if (x_dtype != LV_F32 && x_dtype != LV_F16) return fail(LV_EINVAL, "lv_assign_tags: x_dtype must be F32/F16");
-  LV_CUDA(lv::launch_assign(X, x_dtype == LV_F16, n, D, centres, C, assign, (cudaStream_t)stream));
+  if (!X || !centres || (!assign && !best) || n <= 0 || D <= 0 || C < 1)
+    return fail(LV_EINVAL, "lv_kmeans_assign: bad arguments");
+  if (x_dtype != LV_F32 && x_dtype != LV_F16) return fail(LV_EINVAL, "lv_kmeans_assign: x_dtype must be F32/F16");
+  LV_CUDA(lv::launch_assign(X, x_dtype == LV_F16, n, D, centres, C, assign, best, accumulate ? 1 : 0,
+                            (cudaStream_t)stream));
+  return LV_OK;
+}
+
+lv_status lv_normalize_rows(const void* X, lv_dtype x_dtype, int64_t n, int32_t D, float* Xn, void* stream) {
+  lv_status st = check_device();
+  if (st) return st;
+  if (!X || !Xn || n <= 0 || D <= 0) return fail(LV_EINVAL, "lv_normalize_rows: bad arguments");
+  if (x_dtype != LV_F32 && x_dtype != LV_F16) return fail(LV_EINVAL, "lv_normalize_rows: x_dtype must be F32/F16");
+  LV_CUDA(lv::launch_normalize(X, x_dtype == LV_F16, n, D, Xn, (cudaStream_t)stream));
+  return LV_OK;
+}
+
+lv_status lv_kmeans_centre_sums(const void* X, lv_dtype x_dtype, int64_t n, int32_t D, const int32_t* assign,
+                                int32_t C, double* sums, int64_t* counts, void* stream) {
+  lv_status st = check_device();
+  if (st) return st;
+  if (!X || !assign || !sums || !counts || n <= 0 || D <= 0 || C < 1)
+    return fail(LV_EINVAL, "lv_kmeans_centre_sums: bad arguments");
+  if (x_dtype != LV_F32 && x_dtype != LV_F16) return fail(LV_EINVAL, "lv_kmeans_centre_sums: x_dtype must be F32/F16");
+  if (lv::centre_sums_smem(C) > 200 * 1024) return fail(LV_EUNSUPPORTED, "lv_kmeans_centre_sums: C=%d > 384", C);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t rpc = 2048;   // rows per chunk
+  const int nch = (int)((n + rpc - 1) / rpc);
+  float* part = nullptr;
+  int32_t* pc = nullptr;
+  double* dsum = nullptr;
+  long long* dcnt = nullptr;
+  LV_CUDA(cudaMallocAsync(&part, sizeof(float) * (size_t)nch * C * D, s));
+  LV_CUDA(cudaMallocAsync(&pc, sizeof(int32_t) * (size_t)nch * C, s));
+  LV_CUDA(cudaMallocAsync(&dsum, sizeof(double) * (size_t)C * D, s));
+  LV_CUDA(cudaMallocAsync(&dcnt, sizeof(long long) * (size_t)C, s));
+  cudaError_t e = lv::launch_centre_sums(X, x_dtype == LV_F16, n, D, assign, C, rpc, nch, part, pc, dsum, dcnt, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(sums, dsum, sizeof(double) * (size_t)C * D, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(counts, dcnt, sizeof(long long) * (size_t)C, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(part, s);
+  cudaFreeAsync(pc, s);
+  cudaFreeAsync(dsum, s);
+  cudaFreeAsync(dcnt, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(LV_ECUDA, "lv_kmeans_centre_sums: %s", cudaGetErrorString(e));
   return LV_OK;
 }
 
@@ -1132,6 +1279,9 @@ void lv_index_destroy(lv_index* ix) {
   for (auto e : ix->ev_pool) cudaEventDestroy(e);
   cudaFree(ix->ws);
   cudaFree(ix->hs);
+  for (auto e : ix->hev)
+    if (e) cudaEventDestroy(e);
+  if (ix->cs) cudaStreamDestroy(ix->cs);
   delete ix;
 }
 

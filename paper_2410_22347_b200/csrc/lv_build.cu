@@ -1,0 +1,266 @@
+// Index-build kernels on CUDA cores (off the search path):
+//  K7 statistics  K = sum x x^T per cluster      (Sec. 3.2)
+//  Eq.(13) tags   c_i = argmax_c <x_i, mu_c>, with the best similarity (k-means++ D^2)
+//  k-means M-step sum_{c_i = c} x~_i per cluster (App. A)
+//  row normalisation x~ = x / ||x||              (Alg. 5 line 1)
+// All products accumulate in fp32 in a fixed order (deterministic); chunk partials are summed
+// in fp64 in chunk order.
+#include <cfloat>
+
+#include "lv_common.cuh"
+#include "lv_internal.h"
+
+namespace lv {
+
+constexpr int GT = 64;   // output tile rows/cols
+constexpr int GK = 32;   // k step
+
+template <typename TIn>
+LV_DEVINL float ldv(const TIn* p) { return to_f32(*p); }
+
+// ------------------------------------------------------------------------- K7 statistics
+// partial[ch][i][j] = sum_{r in chunk ch} x[src(r), i] * x[src(r), j]  (fp32, ascending r)
+template <typename TIn>
+__global__ void __launch_bounds__(256) k_stats(const TIn* __restrict__ in, int64_t ld, const int32_t* __restrict__ rowidx,
+                                               const int64_t* __restrict__ lo_, const int64_t* __restrict__ hi_, int D,
+                                               float* __restrict__ partial) {
+  __shared__ float As[GK][GT + 4];
+  __shared__ float Bs[GK][GT + 4];
+  const int tid = threadIdx.x;
+  const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
+  const int ch = blockIdx.z;
+  const int64_t lo = lo_[ch], hi = hi_[ch];
+  const int tx = tid & 15, ty = tid >> 4;
+  float acc[4][4] = {}, comp[4][4] = {};
+  for (int64_t rb = lo; rb < hi; rb += GK) {
+    // 32 rows x 64 cols for each side: 2048 elements, 8 per thread
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int e = tid + t * 256;
+      const int rr = e >> 6, cc = e & 63;
+      const int64_t r = rb + rr;
+      float va = 0.f, vb = 0.f;
+      if (r < hi) {
+        const int64_t src = rowidx ? rowidx[r] : r;
+        if (i0 + cc < D) va = ldv(in + src * ld + i0 + cc);
+        if (j0 + cc < D) vb = ldv(in + src * ld + j0 + cc);
+      }
+      As[rr][cc] = va;
+      Bs[rr][cc] = vb;
+    }
+    __syncthreads();
+    // 32-row partial in fp32, then a compensated (Kahan) add into the running sum: the chunk
+    // sum's error stays at the 32-term level instead of growing with the chunk length.
+    float t[4][4] = {};
+#pragma unroll 8
+    for (int k = 0; k < GK; ++k) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[k][ty * 4 + i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) bv[i] = Bs[k][tx * 4 + i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t[i][j] = fmaf(av[i], bv[j], t[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float y = __fsub_rn(t[i][j], comp[i][j]);
+        const float s = __fadd_rn(acc[i][j], y);
+        comp[i][j] = __fsub_rn(__fsub_rn(s, acc[i][j]), y);
+        acc[i][j] = s;
+      }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gi = i0 + ty * 4 + i, gj = j0 + tx * 4 + j;
+      if (gi < D && gj < D) partial[((size_t)ch * D + gi) * D + gj] = acc[i][j];
+    }
+}
+
+cudaError_t launch_stats(const void* in, int in_f16, int64_t ld, const int32_t* rowidx, int nchunks,
+                         const int64_t* chunk_lo, const int64_t* chunk_hi, int D, float* partial, cudaStream_t s) {
+  dim3 grid((D + GT - 1) / GT, (D + GT - 1) / GT, nchunks);
+  if (in_f16)
+    k_stats<__half><<<grid, 256, 0, s>>>((const __half*)in, ld, rowidx, chunk_lo, chunk_hi, D, partial);
+  else
+    k_stats<float><<<grid, 256, 0, s>>>((const float*)in, ld, rowidx, chunk_lo, chunk_hi, D, partial);
+  return cudaGetLastError();
+}
+
+// out[o][i][j] = sum over chunks owned by o, in chunk order, of partial (fp64)
+__global__ void k_stats_reduce(const float* __restrict__ partial, int nchunks, const int32_t* __restrict__ owner,
+                               int nowners, int D, double* __restrict__ out) {
+  const size_t DD = (size_t)D * D;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < DD * nowners; e += (size_t)gridDim.x * blockDim.x) {
+    const int o = (int)(e / DD);
+    const size_t ij = e % DD;
+    double s = 0.0;
+    for (int ch = 0; ch < nchunks; ++ch)
+      if (owner[ch] == o) s += (double)partial[(size_t)ch * DD + ij];
+    out[e] = s;
+  }
+}
+
+cudaError_t launch_stats_reduce(const float* partial, int nchunks, const int32_t* chunk_owner, int nowners, int D,
+                                double* out, cudaStream_t s) {
+  k_stats_reduce<<<592, 256, 0, s>>>(partial, nchunks, chunk_owner, nowners, D, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------- dtype conversion
+template <typename TI, typename TO>
+__global__ void k_convert(const TI* __restrict__ in, TO* __restrict__ out, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = from_f32<TO>(to_f32(in[i]));
+}
+
+cudaError_t launch_convert(const void* in, int in_f16, void* out, int out_f16, int64_t count, cudaStream_t s) {
+  if (in_f16 == out_f16) {
+    return cudaMemcpyAsync(out, in, (size_t)count * (in_f16 ? 2 : 4), cudaMemcpyDeviceToDevice, s);
+  }
+  if (in_f16) k_convert<__half, float><<<1184, 256, 0, s>>>((const __half*)in, (float*)out, count);
+  else k_convert<float, __half><<<1184, 256, 0, s>>>((const float*)in, (__half*)out, count);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------- Eq.(13) tags
+// One warp per row: lanes split D, fp32 dot per centre (centres from global/L1), argmax with
+// the lowest index on ties.  Optional outputs for spherical k-means (App. A):
+// best[i] = max_c <x_i, mu_c> (the similarity to the assigned centre; k-means++ D^2 = 2 - 2 best),
+// or with accumulate, best[i] = max(best[i], max_c <x_i, mu_c>) (k-means++ adds one centre at a time).
+template <typename TIn>
+__global__ void __launch_bounds__(256) k_assign(const TIn* __restrict__ X, int64_t n, int D,
+                                                const float* __restrict__ mu, int C, int32_t* __restrict__ assign,
+                                                float* __restrict__ best_out, int accumulate) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (row >= n) return;
+  float best = -FLT_MAX;
+  int bi = 0;
+  for (int c = 0; c < C; ++c) {
+    float acc = 0.f;
+    for (int k = lane; k < D; k += 32) acc = fmaf(to_f32(X[row * D + k]), mu[(size_t)c * D + k], acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (acc > best) {
+      best = acc;
+      bi = c;
+    }
+  }
+  if (lane == 0) {
+    if (assign) assign[row] = bi;
+    if (best_out) best_out[row] = accumulate ? fmaxf(best_out[row], best) : best;
+  }
+}
+
+cudaError_t launch_assign(const void* X, int x_f16, int64_t n, int D, const float* centres, int C, int32_t* assign,
+                          float* best, int accumulate, cudaStream_t s) {
+  const int64_t blocks = (n * 32 + 255) / 256;
+  if (x_f16) k_assign<__half><<<(unsigned)blocks, 256, 0, s>>>((const __half*)X, n, D, centres, C, assign, best, accumulate);
+  else k_assign<float><<<(unsigned)blocks, 256, 0, s>>>((const float*)X, n, D, centres, C, assign, best, accumulate);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------- x~ = x / ||x||
+// Alg. 5 line 1: one warp per row, fp32 sum of squares, out = x * (1 / sqrt(sum)).
+template <typename TIn>
+__global__ void __launch_bounds__(256) k_normalize(const TIn* __restrict__ X, int64_t n, int D, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (row >= n) return;
+  float ss = 0.f;
+  for (int k = lane; k < D; k += 32) {
+    const float v = to_f32(X[row * D + k]);
+    ss = fmaf(v, v, ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float inv = ss > 0.f ? 1.0f / sqrtf(ss) : 0.f;
+  for (int k = lane; k < D; k += 32) out[row * D + k] = to_f32(X[row * D + k]) * inv;
+}
+
+cudaError_t launch_normalize(const void* X, int x_f16, int64_t n, int D, float* out, cudaStream_t s) {
+  const int64_t blocks = (n * 32 + 255) / 256;
+  if (x_f16) k_normalize<__half><<<(unsigned)blocks, 256, 0, s>>>((const __half*)X, n, D, out);
+  else k_normalize<float><<<(unsigned)blocks, 256, 0, s>>>((const float*)X, n, D, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------- k-means M-step sums
+// partial[ch][c][j] = sum_{r in chunk ch, assign[r] = c} X[r, j] (App. A M-step), fp32 in
+// ascending row order; one thread per column j of a 128-column block owns its smem accumulators
+// acc[c][j] (no atomics, deterministic); column block 0 also counts the rows of every cluster.
+constexpr int kCsCols = 128;
+template <typename TIn>
+__global__ void __launch_bounds__(kCsCols) k_centre_sums(const TIn* __restrict__ X, int64_t n, int D,
+                                                         const int32_t* __restrict__ assign, int C, int64_t rows_per_chunk,
+                                                         float* __restrict__ partial, int32_t* __restrict__ pcount) {
+  extern __shared__ float s_acc[];   // [C][kCsCols], then int counts [C]
+  int* s_cnt = reinterpret_cast<int*>(s_acc + (size_t)C * kCsCols);
+  const int j = blockIdx.x * kCsCols + threadIdx.x;
+  const int ch = blockIdx.y;
+  for (int c = 0; c < C; ++c) s_acc[c * kCsCols + threadIdx.x] = 0.f;
+  for (int c = threadIdx.x; c < C; c += kCsCols) s_cnt[c] = 0;
+  __syncthreads();
+  const int64_t lo = (int64_t)ch * rows_per_chunk, hi = min(n, lo + rows_per_chunk);
+  for (int64_t r = lo; r < hi; ++r) {
+    const int c = __ldg(assign + r);
+    if (j < D) s_acc[c * kCsCols + threadIdx.x] += to_f32(X[r * D + j]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) s_cnt[c] += 1;
+  }
+  __syncthreads();
+  if (j < D)
+    for (int c = 0; c < C; ++c) partial[((size_t)ch * C + c) * D + j] = s_acc[c * kCsCols + threadIdx.x];
+  if (blockIdx.x == 0)
+    for (int c = threadIdx.x; c < C; c += kCsCols) pcount[(size_t)ch * C + c] = s_cnt[c];
+}
+
+// sums[c][j] = sum over chunks (in chunk order, fp64) of partial[ch][c][j]; counts likewise
+__global__ void k_centre_reduce(const float* __restrict__ partial, const int32_t* __restrict__ pcount, int nch, int C,
+                                int D, double* __restrict__ sums, long long* __restrict__ counts) {
+  const int64_t tot = (int64_t)C * D;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot + C; e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < tot) {
+      double s = 0.0;
+      for (int ch = 0; ch < nch; ++ch) s += (double)partial[(size_t)ch * tot + e];
+      sums[e] = s;
+    } else {
+      const int c = (int)(e - tot);
+      long long k = 0;
+      for (int ch = 0; ch < nch; ++ch) k += pcount[(size_t)ch * C + c];
+      counts[c] = k;
+    }
+  }
+}
+
+size_t centre_sums_smem(int C) { return (size_t)C * kCsCols * 4 + (size_t)C * 4; }
+
+cudaError_t launch_centre_sums(const void* X, int x_f16, int64_t n, int D, const int32_t* assign, int C,
+                               int64_t rows_per_chunk, int nch, float* partial, int32_t* pcount, double* sums,
+                               long long* counts, cudaStream_t s) {
+  const size_t smem = centre_sums_smem(C);
+  const dim3 grid((unsigned)((D + kCsCols - 1) / kCsCols), (unsigned)nch);
+  cudaError_t e;
+  if (x_f16) {
+    e = cudaFuncSetAttribute(k_centre_sums<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_centre_sums<__half><<<grid, kCsCols, smem, s>>>((const __half*)X, n, D, assign, C, rows_per_chunk, partial, pcount);
+  } else {
+    e = cudaFuncSetAttribute(k_centre_sums<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_centre_sums<float><<<grid, kCsCols, smem, s>>>((const float*)X, n, D, assign, C, rows_per_chunk, partial, pcount);
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_centre_reduce<<<296, 256, 0, s>>>(partial, pcount, nch, C, D, sums, counts);
+  return cudaGetLastError();
+}
+
+}  // namespace lv

@@ -80,10 +80,6 @@ cudaError_t launch_rerank_topk(const RerankArgs& a, cudaStream_t s);   // K5
 cudaError_t launch_tau_merge(uint64_t* cand, int32_t* cnt, uint64_t* tau, int NS, int m, int m_pad, int Cap, int R,
                              cudaStream_t s);
 
-// out[r, j] = RNE(sum_k in[rowidx[r], k] * W[wrow(r) + j, k]) for 64-row tiles.
-cudaError_t launch_rows_gemm(const void* in, int in_f16, int64_t ld_in, const int32_t* rowidx, int64_t rows_valid,
-                             int64_t nrows, const float* W, int K, const int32_t* tile_wrow64, int ncols,
-                             void* out, int out_dtype, int64_t ld_out, int64_t rows_store, cudaStream_t s);
 // K1 on tensor cores (lv_proj.cu): three-plane bf16 split and the six-product GEMM.
 cudaError_t launch_split3(const float* in, int64_t rows_valid, int64_t rows_pad, int D, int Kp, void* out,
                           cudaStream_t s);
@@ -113,7 +109,12 @@ cudaError_t launch_cluster_scatter(const int32_t* assign, int64_t n, int C, cons
 
 cudaError_t launch_convert(const void* in, int in_f16, void* out, int out_f16, int64_t count, cudaStream_t s);
 cudaError_t launch_assign(const void* X, int x_f16, int64_t n, int D, const float* centres, int C, int32_t* assign,
-                          cudaStream_t s);
+                          float* best, int accumulate, cudaStream_t s);
+cudaError_t launch_normalize(const void* X, int x_f16, int64_t n, int D, float* out, cudaStream_t s);
+size_t centre_sums_smem(int C);
+cudaError_t launch_centre_sums(const void* X, int x_f16, int64_t n, int D, const int32_t* assign, int C,
+                               int64_t rows_per_chunk, int nch, float* partial, int32_t* pcount, double* sums,
+                               long long* counts, cudaStream_t s);
 
 constexpr int kSortBlock = 4096;
 

@@ -12,7 +12,6 @@
 
 namespace lv {
 
-constexpr int kRrThreads = 256;
 constexpr int kMaxR = 512;
 
 // In-place descending bitonic sort of n (power of two) 64-bit keys in smem by the whole block.

@@ -5,9 +5,10 @@ D x D eigendecompositions that replace Alg. 2's SVDs:
   W   = (K_Q / m_learn)^{1/2}              (eig of K_Q; P:228-231 with the 1/sqrt(m) scale, R2)
   P_c = top-d eigenvectors of W K_X[c] W    (per cluster for GleanVec)
   A_c = P_c W^+,  B_c = P_c W               (pseudoinverse per P:194)
-GleanVec's spherical k-means (App. A) runs its E-step (Eq.(13) tags) and
-k-means++ similarities on the GPU (lv_assign_tags); the M-step centre sums use the same
-GPU statistics path.  The host only samples k-means++ seeds and normalises C centres.
+GleanVec's spherical k-means (App. A) runs every pass over the rows on the GPU:
+row normalisation (lv_normalize_rows), E-step tags and k-means++ similarities
+(lv_kmeans_assign), M-step sums (lv_kmeans_centre_sums).  The host only draws the k-means++
+seeds from the D^2 weights and normalises the C centre sums.
 """
 from __future__ import annotations
 
@@ -65,57 +66,57 @@ def leanvec_sphering_fit(Q_learn: torch.Tensor, X_learn: torch.Tensor, d: int) -
 
 def gleanvec_fit(Q_learn: torch.Tensor, X_learn: torch.Tensor, C: int, d: int, draws: np.ndarray,
                  max_iter: int = 50) -> dict:
-    """Alg. 5: normalise, spherical k-means, per-cluster Alg. 2 with a shared W."""
-    Xn = X_learn.float()
-    Xn = Xn / torch.linalg.vector_norm(Xn, dim=1, keepdim=True)
-    centres, assign = spherical_kmeans(Xn, C, draws, max_iter)
+    """Alg. 5: normalise, spherical k-means, tags of the learning rows
+    with the final centres, per-cluster Alg. 2 with one shared W via the statistics."""
+    Xn = lv.lv_normalize_rows(X_learn)
+    if C == 1:
+        sums, _ = lv.lv_kmeans_centre_sums(Xn, torch.zeros(Xn.shape[0], dtype=torch.int32, device=Xn.device), 1)
+        centres = sums / np.linalg.norm(sums[0])
+    else:
+        centres, _ = spherical_kmeans(Xn, C, draws, max_iter)
+    assign, _ = lv.lv_kmeans_assign(Xn, torch.as_tensor(centres, dtype=torch.float32, device=Xn.device))
     KQ, KX = lv.lv_fit_stats(Q_learn, X_learn, assign, C)
     out = fit_from_stats(KQ, KX, Q_learn.shape[0], d)
     out.update({"centres": centres, "assign_learn": assign, "KQ": KQ, "KX": KX})
     return out
 
 
-def _centre_sums(Xn: torch.Tensor, assign: torch.Tensor, C: int) -> np.ndarray:
-    """M-step sums sum_{c_i = c} x~_i via the statistics kernel: with rows [x~; 1]
-    the per-cluster second moment holds sum x~ in its last column."""
-    n, D = Xn.shape
-    aug = torch.zeros((n, D + 4), dtype=torch.float32, device=Xn.device)   # keep rows 16-byte aligned
-    aug[:, :D] = Xn
-    aug[:, D] = 1.0
-    ones = torch.zeros((1, D + 4), dtype=torch.float32, device=Xn.device)
-    ones[0, 0] = 1.0
-    _, KX = lv.lv_fit_stats(ones, aug, assign, C)
-    # K_X[c][:D, D] = sum_{c_i=c} x~_i * 1
-    return KX[:, :D, D]
-
-
 def spherical_kmeans(Xn: torch.Tensor, C: int, draws: np.ndarray, max_iter: int = 50):
-    """App. A on unit rows Xn (CUDA fp32).  k-means++ seeding with D^2 = 2 - 2 max<x,mu>
-    (the per-row max similarity is one lv_assign_tags-style pass per new centre), then EM:
-    E-step = Eq.(13) tags on the GPU (lv_assign_tags), M-step = normalised per-cluster sums."""
+    """App. A on unit rows Xn (CUDA fp32), every pass over the rows on the GPU:
+    k-means++ seeding with D^2(x) = 2 - 2 max_c <x, mu_c> (lv_kmeans_assign keeps the
+    running maximum; the host draws the next seed from the D^2 weights by inverse CDF with the
+    shared uniform draws), then EM: E-step = Eq.(13) tags (lv_kmeans_assign), M-step =
+    per-cluster sums (lv_kmeans_centre_sums) normalised on the host (C x D).  Stops when the tags do
+    not change or after max_iter passes; an empty cluster takes the row least similar to its own
+    centre (R14).  Returns (centres fp64 [C, D], last tags)."""
     n, D = Xn.shape
+    dev = Xn.device
     mu = np.empty((C, D))
     first = min(int(draws[0] * n), n - 1)
     mu[0] = Xn[first].double().cpu().numpy()
-    best = (Xn @ Xn[first]).double().cpu().numpy()   # TODO(lv): move to a kernel
+    _, best = lv.lv_kmeans_assign(Xn, Xn[first:first + 1], assign=False)
     for j in range(1, C):
-        w = np.maximum(2.0 - 2.0 * best, 0.0)
+        w = np.maximum(2.0 - 2.0 * best.double().cpu().numpy(), 0.0)
         cdf = np.cumsum(w)
         if cdf[-1] <= 0:
             pick = min(int(draws[j] * n), n - 1)
         else:
             pick = min(int(np.searchsorted(cdf, draws[j] * cdf[-1], side="right")), n - 1)
         mu[j] = Xn[pick].double().cpu().numpy()
-        best = np.maximum(best, (Xn @ Xn[pick]).double().cpu().numpy())
+        lv.lv_kmeans_assign(Xn, Xn[pick:pick + 1], assign=False, best=best, accumulate=True)
     assign = None
     for _ in range(max_iter):
-        new = lv.lv_assign_tags(Xn, torch.as_tensor(mu, dtype=torch.float32, device=Xn.device))
+        new, best = lv.lv_kmeans_assign(Xn, torch.as_tensor(mu, dtype=torch.float32, device=dev))
         if assign is not None and torch.equal(new, assign):
             break
         assign = new
-        sums = _centre_sums(Xn, assign, C)
+        sums, counts = lv.lv_kmeans_centre_sums(Xn, assign, C)
+        far = None
         for c in range(C):
-            nrm = np.linalg.norm(sums[c])
-            if nrm > 0:
-                mu[c] = sums[c] / nrm
+            if counts[c] == 0:
+                if far is None:
+                    far = int(np.argmin(best.cpu().numpy()))   # lowest index among the minima
+                mu[c] = Xn[far].double().cpu().numpy()
+            else:
+                mu[c] = sums[c] / np.linalg.norm(sums[c])
     return mu, assign

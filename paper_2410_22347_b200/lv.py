@@ -22,7 +22,7 @@ _TORCH_DT = {LV_F32: torch.float32, LV_F16: torch.float16, LV_BF16: torch.bfloat
 EXPORTS = ["lv_last_error", "lv_version", "lv_fit_stats", "lv_index_create", "lv_encode_database",
            "lv_project_queries", "lv_search", "lv_search_host", "lv_timing_collect", "lv_encode_timing", "lv_assign_tags",
            "lv_index_info", "lv_index_export", "lv_index_destroy", "lv_index_set_search_dim",
-           "lv_index_get_search_dim"]
+           "lv_index_get_search_dim", "lv_normalize_rows", "lv_kmeans_assign", "lv_kmeans_centre_sums"]
 
 
 class LVError(RuntimeError):
@@ -64,6 +64,9 @@ def lib():
             "lv_index_set_search_dim": [vp, i32],
             "lv_index_get_search_dim": [vp, ctypes.POINTER(i32)],
             "lv_assign_tags": [vp, i32, i64, i32, vp, i32, vp, vp],
+            "lv_normalize_rows": [vp, i32, i64, i32, vp, vp],
+            "lv_kmeans_assign": [vp, i32, i64, i32, vp, i32, vp, vp, i32, vp],
+            "lv_kmeans_centre_sums": [vp, i32, i64, i32, vp, i32, vp, vp, vp],
             "lv_index_info": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32),
                               ctypes.POINTER(i32), ctypes.POINTER(i32)],
             "lv_index_export": [vp, vp, vp, vp, vp],
@@ -97,6 +100,17 @@ def _dev(t: torch.Tensor, dtype=None) -> torch.Tensor:
     if dtype is not None and t.dtype != dtype:
         raise LVError(f"expected dtype {dtype}, got {t.dtype}")
     return t.contiguous()
+
+
+def _out(t, shape, dtype, what: str, host: bool = False):
+    """Caller-supplied output buffer: exact shape, dtype, device and contiguity (the library writes
+    [shape] elements through the raw pointer)."""
+    if not isinstance(t, torch.Tensor):
+        raise LVError(f"{what}: expected a torch tensor")
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype or not t.is_contiguous() or t.is_cuda == host:
+        raise LVError(f"{what}: need a contiguous {'host' if host else 'CUDA'} {dtype} tensor of shape {tuple(shape)}, "
+                      f"got {t.dtype} {tuple(t.shape)} on {t.device} (contiguous={t.is_contiguous()})")
+    return t
 
 
 def _xdtype(t: torch.Tensor) -> int:
@@ -194,7 +208,8 @@ def lv_search(index: Index, Q: torch.Tensor, k: int, R: int, cand: bool = False,
         ids = torch.empty((m, k), dtype=torch.int32, device=Q.device)
         sc = torch.empty((m, k), dtype=torch.float32, device=Q.device)
     else:
-        ids, sc = out
+        ids = _out(out[0], (m, k), torch.int32, "lv_search ids")
+        sc = _out(out[1], (m, k), torch.float32, "lv_search scores")
     dbg = SearchDebug()
     keep = {}
     if cand:
@@ -234,11 +249,15 @@ def lv_encode_timing(index: Index):
 def lv_search_host(index: Index, Q_host: torch.Tensor, k: int, R: int, ids_host=None, scores_host=None):
     """lv_search on HOST buffers (copies inside the call).  Q_host: CPU fp32 (pinned is faster)."""
     Q = Q_host.contiguous()
-    assert Q.dtype == torch.float32 and not Q.is_cuda
+    if Q.dtype != torch.float32 or Q.is_cuda or Q.dim() != 2 or Q.shape[1] != index.D:
+        raise LVError(f"lv_search_host: need a host fp32 [m, {index.D}] query tensor")
     m = Q.shape[0]
     if ids_host is None:
         ids_host = torch.empty((m, k), dtype=torch.int32, pin_memory=Q.is_pinned())
         scores_host = torch.empty((m, k), dtype=torch.float32, pin_memory=Q.is_pinned())
+    else:
+        _out(ids_host, (m, k), torch.int32, "lv_search_host ids", host=True)
+        _out(scores_host, (m, k), torch.float32, "lv_search_host scores", host=True)
     _check(lib().lv_search_host(index.h, ctypes.c_void_p(Q.data_ptr()), m, k, R,
                                 ctypes.c_void_p(ids_host.data_ptr()), ctypes.c_void_p(scores_host.data_ptr()),
                                 _stream()), "lv_search_host")
@@ -252,6 +271,45 @@ def lv_assign_tags(X: torch.Tensor, centres: torch.Tensor) -> torch.Tensor:
     _check(lib().lv_assign_tags(_ptr(X), _xdtype(X), X.shape[0], X.shape[1], _ptr(mu), mu.shape[0], _ptr(out),
                                 _stream()), "lv_assign_tags")
     return out
+
+
+def lv_normalize_rows(X: torch.Tensor) -> torch.Tensor:
+    """x~ = x / ||x|| (Alg. 5 line 1), fp32 out."""
+    X = _dev(X)
+    out = torch.empty(X.shape, dtype=torch.float32, device=X.device)
+    _check(lib().lv_normalize_rows(_ptr(X), _xdtype(X), X.shape[0], X.shape[1], _ptr(out), _stream()),
+           "lv_normalize_rows")
+    return out
+
+
+def lv_kmeans_assign(X: torch.Tensor, centres: torch.Tensor, assign: bool = True, best: torch.Tensor | None = None,
+                     accumulate: bool = False):
+    """E-step tags and/or the best similarity max_c <x, mu_c> (k-means++: accumulate=True keeps the
+    running max in `best`).  Returns (assign or None, best)."""
+    X = _dev(X)
+    mu = _dev(centres, torch.float32)
+    a = torch.empty(X.shape[0], dtype=torch.int32, device=X.device) if assign else None
+    if best is None:
+        if accumulate:
+            raise LVError("lv_kmeans_assign: accumulate needs a best tensor")
+        best = torch.empty(X.shape[0], dtype=torch.float32, device=X.device)
+    else:
+        _out(best, (X.shape[0],), torch.float32, "lv_kmeans_assign best")
+    _check(lib().lv_kmeans_assign(_ptr(X), _xdtype(X), X.shape[0], X.shape[1], _ptr(mu), mu.shape[0], _ptr(a),
+                                  _ptr(best), int(accumulate), _stream()), "lv_kmeans_assign")
+    return a, best
+
+
+def lv_kmeans_centre_sums(X: torch.Tensor, assign: torch.Tensor, C: int):
+    """M-step sums per cluster (fp64 [C, D]) and counts (int64 [C]), host numpy."""
+    X = _dev(X)
+    a = _dev(assign, torch.int32)
+    sums = np.zeros((C, X.shape[1]), dtype=np.float64)
+    counts = np.zeros(C, dtype=np.int64)
+    _check(lib().lv_kmeans_centre_sums(_ptr(X), _xdtype(X), X.shape[0], X.shape[1], _ptr(a), C,
+                                       sums.ctypes.data_as(ctypes.c_void_p), counts.ctypes.data_as(ctypes.c_void_p),
+                                       _stream()), "lv_kmeans_centre_sums")
+    return sums, counts
 
 
 def lv_index_export(index: Index):

@@ -17,8 +17,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 TOL_RED = 2e-3
 TOL_RR = 1e-5
-N_SAMPLE = 16
-CHUNK = 1 << 19
+CHUNK = 1 << 17
 
 
 @pytest.fixture(scope="module")
@@ -45,12 +44,16 @@ def _oracle_topR(Qp_s, X, B32, assign, R, store):
     return np.stack(best_i), np.stack(best_s)
 
 
-@pytest.mark.parametrize("cfg_id", [2, 3, 4, 5])
-def test_fullsize_sampled_parity(lv, cfg_id):
+@pytest.mark.parametrize("cfg_id,family,n_sample", [(2, None, 1000), (3, None, 1000), (4, "ood", 256), (4, "id", 256),
+                                                    (5, None, 256)])
+def test_fullsize_sampled_parity(lv, cfg_id, family, n_sample):
+    """Gates G2-G6 on n_sample evenly spaced queries of the full 10^4-query search (1 000 at the
+    1M-row configs, 256 at the 10M-row configs, where the oracle's full scan costs ~0.2 s/query)."""
+    from test_gpu_parity import check_topk_order
     c = lvgen.get_config(cfg_id)
     X = lvgen.database(c)
-    Q = lvgen.queries(c, "test")
-    Ql = lvgen.queries(c, "learn")
+    Q = lvgen.queries(c, "test", family=family)
+    Ql = lvgen.queries(c, "learn", family=family)
     Xl = X[lvgen.learn_rows(c)].astype(np.float64)
     if c.C == 1:
         f = O.sphering_fit(Ql, Xl, c.d)
@@ -68,7 +71,7 @@ def test_fullsize_sampled_parity(lv, cfg_id):
     del Xd
     ids, sc, dbg = lv.lv_search(ix, torch.from_numpy(Q).cuda(), c.k, c.R, cand=True, timing=1)
     assert dbg["path"] == 1   # the sampled-threshold path bench.py times at these sizes
-    sel = np.linspace(0, Q.shape[0] - 1, N_SAMPLE).astype(np.int64)
+    sel = np.linspace(0, Q.shape[0] - 1, n_sample).astype(np.int64)
     ids = ids.cpu().numpy()[sel].astype(np.int64)
     sc = sc.cpu().numpy()[sel].astype(np.float64)
     cid = dbg["cand_ids"].cpu().numpy()[sel].astype(np.int64)
@@ -104,7 +107,8 @@ def test_fullsize_sampled_parity(lv, cfg_id):
             fi = float(2.0 ** -7 * O.reduced_scores(np.abs(Qp[j:j + 1]), np.abs(xi), ai)[0, 0])
             assert abs(si - thr[j]) <= TOL_RED * max(abs(thr[j]), 1e-2) + fi + fR, (j, i, si, thr[j])
     assert n_ok >= 0.999 * n_all, (n_ok, n_all)
-    # G4: re-rank scores vs fp64 <q, x> on the canonical vectors
+    # G4: re-rank scores vs fp64 <q, x> on the canonical vectors; rows ordered (score desc, id asc)
+    check_topk_order(ids, sc)
     ex = np.einsum("md,mkd->mk", Qs.astype(np.float64), X[ids].astype(np.float64))
     assert (np.abs(sc - ex) <= TOL_RR * np.maximum(np.abs(ex), 1e-2)).all(), np.abs(sc - ex).max()
     # G5: final ids = the oracle's re-rank top-k of its own N_low, except boundary cases
@@ -116,3 +120,7 @@ def test_fullsize_sampled_parity(lv, cfg_id):
                 near_k = abs(rr - o_sc[j, -1]) <= TOL_RR * max(abs(o_sc[j, -1]), 1e-2)
                 in_band = (i in set(cid[j].tolist())) != (i in set(ref_i[j].tolist()))
                 assert near_k or in_band, (j, i)
+    # G6: 10-recall@10 on the sample against exact search, GPU vs the emulated oracle
+    gt, _ = O.exact_topk(Qs, X, 10)
+    r_gpu, r_ora = O.recall_at_k(ids, gt, 10), O.recall_at_k(o_ids, gt, 10)
+    assert abs(r_gpu - r_ora) <= 1e-3 + 1e-12, (r_gpu, r_ora)

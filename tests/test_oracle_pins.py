@@ -306,6 +306,25 @@ def test_reduced_search_vs_full_sort_with_ties():
             assert ids[j].tolist() == order
 
 
+def test_exact_topk_chunk_merge_vs_full_sort():
+    """exact_topk (the recall ground truth) with chunk = 64 over 300 rows (5 chunks and a
+    ragged tail) equals the first k of a full stable sort by (-<q, x>, id), exact ties included."""
+    rng = _rng(17)
+    n, D, m = 300, 6, 7
+    X = rng.standard_normal((n, D))
+    X[200] = X[3]
+    X[290] = X[3]            # exact ties across chunks
+    X[100:140] = 0.0         # equal (zero) scores spanning a chunk boundary
+    Q = rng.standard_normal((m, D))
+    S = Q @ X.T
+    for k in (1, 10, 70, n):
+        ids, sc = O.exact_topk(Q, X, k, chunk=64)
+        for j in range(m):
+            order = sorted(range(n), key=lambda i: (-S[j, i], i))[:k]
+            assert ids[j].tolist() == order
+            assert np.allclose(sc[j], S[j, order], rtol=0, atol=1e-12)
+
+
 def test_grouped_scores_select_cluster_view():
     """Eq.(15)/Alg. 4: each row is scored with its own cluster's query view; equals the
     lazy form <A_{c_i} q, x_low_i> (Alg. 3) computed per pair."""
