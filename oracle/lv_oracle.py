@@ -17,6 +17,9 @@ Functions (pin in tests/test_oracle_pins.py named in brackets):
   reduced_search       Alg. 1 l.2 exhaustive + top-R        [brute force vs full sort, S:469]
   rerank_topk          Alg. 1 l.3                           [R=n -> exact k-NN]
   exact_topk, recall_at_k   P:46-48 (MIPS), P:545-546     [S:469, S:476-478]
+  flexible_fit         §3.1 A' = P'W^+, B' = P'W, D x D     [<A'q, B'x> = <q,x>, prefix = smaller fit]
+  eig_fit_from_stats   §3.2 eig route from K_Q, K_X          [equals the SVD route]
+  StreamingIndex       §3.2 insert/remove/observe/refresh    [K_X = definition, x' = B'_new x, Eq.(12)]
 """
 from __future__ import annotations
 
@@ -356,3 +359,83 @@ def search(Q, X, A_stack, B_stack, assign, R: int, k: int, store: str | None = N
     cand, cand_sc = reduced_search(Qp, X_low, assign, R)
     ids, sc = rerank_topk(Q, X, cand, k)
     return {"ids": ids, "scores": sc, "cand": cand, "cand_scores": cand_sc, "Qp": Qp, "X_low": X_low}
+
+
+# ----------------------------------------------------------------------------------
+# Flexible target dimensionality and streaming (Sections 3.1-3.2)
+# ----------------------------------------------------------------------------------
+def flexible_fit(Q_learn, X_learn) -> dict:
+    """Sec. 3.1: P' = all D left singular vectors of W X sorted by decreasing singular
+    value (Alg. 2 with d = D), A' = P'W^+, B' = P'W; x' = B'x is stored and the first d rows of A'
+    and coordinates of x' give the d-dimensional reduction."""
+    X = np.asarray(X_learn, dtype=np.float64)
+    return sphering_fit(Q_learn, X, X.shape[1])
+
+
+def eig_fit_from_stats(K_Q, m_q: int, K_X) -> dict:
+    """Sec. 3.2: the two SVDs of Alg. 2 replaced by eigendecompositions:
+    W = (K_Q / m_q)^{1/2} from eig(K_Q) (the SVD of Q gives W = U S U^T with S^2 = eig(Q Q^T); the
+    1/sqrt(m) scale as in sphering_fit), P' = eigenvectors of W K_X W by decreasing eigenvalue
+    (the left singular vectors of W X), sign-canonical rows; A' = P'W^+, B' = P'W (all D rows)."""
+    lam, U = np.linalg.eigh(np.asarray(K_Q, dtype=np.float64) / float(m_q))
+    sq = np.sqrt(np.maximum(lam, 0.0))
+    W = (U * sq[None, :]) @ U.T
+    cut = PINV_EPS * (sq.max() if sq.size else 0.0)
+    sinv = np.where(sq > cut, 1.0 / np.where(sq > cut, sq, 1.0), 0.0)
+    Wp = (U * sinv[None, :]) @ U.T
+    M = W @ np.asarray(K_X, dtype=np.float64) @ W
+    mu, V = np.linalg.eigh(0.5 * (M + M.T))
+    order = np.argsort(mu)[::-1]
+    P = _sign_canonical_rows(V[:, order].T.copy())
+    return {"W": W, "Wp": Wp, "P": P, "A": P @ Wp, "B": P @ W, "eig": mu[order]}
+
+
+class StreamingIndex:
+    """Sec. 3.2, literally: the database X_t changes by inserts and removals of vectors
+    with unique ids; K_X = sum_{x in X_t} x x^T and K_Q = sum q q^T are updated by adding or
+    subtracting outer products (P:292-295); the stored vectors are x' = P'_{t'} W_{t'} x (P:301);
+    a refresh recomputes W, P' by the eig route and applies
+    P'_{t'+1} W_{t'+1} (P'_{t'} W_{t'})^{-1} to every stored x'; new vectors are
+    stored as P'_{t'+1} W_{t'+1} x.  fp64; the raw vectors are kept here only to define
+    K_X updates and to check the stored x' (the oracle is not memory-constrained)."""
+
+    def __init__(self, D: int, A_prime, B_prime):
+        self.D = D
+        self.A = np.asarray(A_prime, dtype=np.float64)
+        self.B = np.asarray(B_prime, dtype=np.float64)
+        self.x = {}
+        self.xp = {}
+        self.K_X = np.zeros((D, D))
+        self.K_Q = np.zeros((D, D))
+        self.m_q = 0
+
+    def insert(self, ids, X):
+        for i, v in zip(np.asarray(ids).tolist(), np.asarray(X, dtype=np.float64)):
+            assert i not in self.x
+            self.x[i] = v
+            self.xp[i] = self.B @ v
+            self.K_X += np.outer(v, v)
+
+    def remove(self, ids):
+        for i in np.asarray(ids).tolist():
+            v = self.x.pop(i)
+            self.xp.pop(i)
+            self.K_X -= np.outer(v, v)
+
+    def observe(self, Q):
+        Q = np.asarray(Q, dtype=np.float64)
+        self.K_Q += Q.T @ Q
+        self.m_q += Q.shape[0]
+
+    def refresh(self):
+        f = eig_fit_from_stats(self.K_Q, self.m_q, self.K_X)
+        T = f["B"] @ np.linalg.inv(self.B)          # P'_{t'+1} W_{t'+1} (P'_{t'} W_{t'})^{-1}
+        for i in self.xp:
+            self.xp[i] = T @ self.xp[i]
+        self.A, self.B = f["A"], f["B"]
+        return f
+
+    def current(self):
+        ids = np.array(sorted(self.x), dtype=np.int64)
+        return ids, np.stack([self.x[i] for i in ids]), np.stack([self.xp[i] for i in ids])
+

@@ -184,6 +184,73 @@ def test_flexible_d_prefix_is_the_smaller_fit():
         assert np.allclose(s_pre, s_d2, rtol=0, atol=1e-12)
 
 
+def test_flexible_fit_exact_rerank_eq12():
+    """Eq.(12): with A' = P'W^+, B' = P'W (D x D), <A'q, x'> = <q, x> for any q and x,
+    not only the learning sets (the 'undistorted similarities' claim); x' = B'x is invertible by
+    A'^T (A'^T B' = I)."""
+    rng = _rng(21)
+    Q, X = _ood_pair(rng)
+    f = O.flexible_fit(Q, X)
+    q = rng.standard_normal((7, X.shape[1]))
+    x = rng.standard_normal((11, X.shape[1]))
+    assert np.allclose((q @ f["A"].T) @ (x @ f["B"].T).T, q @ x.T, rtol=0, atol=1e-9)
+    assert np.allclose(f["A"].T @ f["B"], np.eye(X.shape[1]), atol=1e-10)
+
+
+def test_eig_route_from_stats_equals_svd_route():
+    """§3.2: eigendecompositions of K_Q and W K_X W give the same W and the same P' (up to
+    the sign rule) as Alg. 2's two SVDs; checked on every prefix d with a spectral gap via
+    M_d = A'_d^T B'_d (invariant to the sign and to rotations inside degenerate blocks)."""
+    Q, X = _ood_pair(_rng(22))
+    svd = O.flexible_fit(Q, X)
+    eig = O.eig_fit_from_stats(Q.T @ Q, Q.shape[0], X.T @ X)
+    assert np.allclose(eig["W"], svd["W"], atol=1e-12)
+    lam = eig["eig"]
+    for d in range(1, X.shape[1]):
+        if lam[d - 1] / lam[d] - 1 > 1e-6:
+            Ms = svd["A"][:d].T @ svd["B"][:d]
+            Me = eig["A"][:d].T @ eig["B"][:d]
+            assert np.abs(Ms - Me).max() < 1e-8 * max(1.0, np.abs(Ms).max())
+
+
+def test_streaming_stats_reprojection_and_fresh_fit():
+    """§3.2: after inserts, removals and new queries, (1) K_X equals sum x x^T over the
+    CURRENT set and K_Q sum q q^T over every observed query (their definitions, P:292-294);
+    (2) after a refresh, every stored x' = T x'_old equals P'_{t'+1} W_{t'+1} x of its raw vector
+    (the undo/redo identity of P:302-307), and vectors inserted afterwards are stored the same way
+    (P:308); (3) the refreshed A', B' equal a fresh Alg. 2 SVD fit on the current set with all
+    observed queries (route equivalence), so the index equals a fresh fit + encode."""
+    rng = _rng(23)
+    D = 10
+    Q0, X0 = _ood_pair(rng, m=300, n=400, D=D)
+    Q1, X1 = _ood_pair(_rng(24), m=200, n=150, D=D)
+    f0 = O.flexible_fit(Q0, X0)
+    st = O.StreamingIndex(D, f0["A"], f0["B"])
+    st.insert(np.arange(400), X0)
+    st.observe(Q0)
+    st.insert(np.arange(1000, 1150), X1)
+    gone = rng.choice(np.concatenate([np.arange(400), np.arange(1000, 1150)]), 120, replace=False)
+    st.remove(gone)
+    st.observe(Q1)
+    ids, X, Xp = st.current()
+    assert ids.size == 550 - 120 and not set(gone.tolist()) & set(ids.tolist())
+    Kx = X.T @ X
+    assert np.abs(st.K_X - Kx).max() <= 1e-10 * np.abs(Kx).max()
+    Qall = np.vstack([Q0, Q1])
+    assert np.abs(st.K_Q - Qall.T @ Qall).max() <= 1e-10 * np.abs(Qall.T @ Qall).max()
+    f1 = st.refresh()
+    ids, X, Xp = st.current()
+    assert np.allclose(Xp, X @ f1["B"].T, rtol=0, atol=1e-10)
+    st.insert([5000], X1[:1] * 0.5)
+    ids, X, Xp = st.current()
+    assert np.allclose(Xp, X @ f1["B"].T, rtol=0, atol=1e-10)
+    fresh = O.flexible_fit(Qall, X[ids != 5000])
+    lam = f1["eig"]
+    for d in (2, 4, 7):
+        if lam[d - 1] / lam[d] - 1 > 1e-6:
+            assert np.abs(fresh["A"][:d].T @ fresh["B"][:d] - f1["A"][:d].T @ f1["B"][:d]).max() < 1e-8
+
+
 def test_scale_invariance_of_AtB():
     """Q -> cQ leaves A^T B unchanged."""
     Q, X = _ood_pair(_rng(8))
