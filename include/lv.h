@@ -236,6 +236,49 @@ lv_status lv_kmeans_centre_sums(const void* X, lv_dtype x_dtype, int64_t n, int3
 lv_status lv_index_set_search_dim(lv_index* index, int32_t d_search);
 lv_status lv_index_get_search_dim(const lv_index* index, int32_t* d_search);
 
+/*
+ * Flexible target dimensionality with the x' store, and streaming updates (§3.1-3.2).
+ *
+ * lv_index_create_flex — a LeanVec-Sphering index that stores x' = P'W x (Eq.(10))
+ *   instead of the raw vectors.  Ap = A' = P'W^+ and Bp = B' = P'W, device fp32 [D, D] (copied),
+ *   rows ordered by decreasing eigenvalue of W K_X W (the full spectrum of Alg. 2's P).
+ *   d = stored prefix width of the scan's reduced vectors (32 <= d <= min(D, 192), d % 32 == 0):
+ *   X_low = RNE(x'[0:d]) in low_dtype; lv_index_set_search_dim picks any 32-multiple d_search <= d
+ *   per search ("select the value of d during search").  The re-rank computes
+ *   <A'q, x'> = <q, x> in fp32 (Eq.(12)): no secondary copy of the database.
+ *   Ids are external, in [0, id_capacity).  C = 1; full vectors fp32 (x').
+ *   lv_encode_database on such an index: x' = B' x for rows 0..n-1 (ids = row numbers; n <=
+ *   id_capacity; assign must be NULL), K_X = sum x x^T restarts from this database.
+ *   Memory: X' fp32 [n, D] + X_low [n, d] (+ 4 bytes per row and per id) — the raw X is not kept.
+ *
+ * Streaming.  Not thread-safe; each call synchronises `stream`.
+ * lv_stream_insert — X device [b, D] (F32/F16) raw vectors with HOST ids[b] (absent, distinct):
+ *   x' = B' x appended, K_X += sum x x^T.  The allocation grows as needed.
+ * lv_stream_remove — HOST ids[b] (present, distinct; at least one vector must stay): K_X -=
+ *   sum x x^T with x = A'^T x' recovered from the stored x' (A'^T B' = I), then the last rows
+ *   move into the holes (rows stay dense; ids do not change).
+ * lv_stream_observe_queries — Q device fp32 [m, D]: K_Q += sum q q^T, m_q += m.
+ * lv_stream_stats — HOST fp64 K_Q [D, D], K_X [D, D], m_q and n (any may be NULL): the inputs of
+ *   the eig route (W = (K_Q / m_q)^{1/2}, P' = eigenvectors of W K_X W) the host uses to
+ *   compute new A', B' every s updates.
+ * lv_stream_reproject — Ap, Bp device fp32 [D, D], the refreshed A'_{t'+1}, B'_{t'+1}: every stored
+ *   x' <- B'_{t'+1} A'_{t'}^T x' = P'_{t'+1} W_{t'+1} (P'_{t'} W_{t'})^{-1} x', in place
+ *   by the fp32-faithful tensor-core GEMM, X_low re-derived, A', B' replaced.
+ * lv_index_export_xprime — test/debug: Xp device fp32 [n, D] (row order) and ids device int32 [n]
+ *   (the id of each row); either may be NULL.  Synchronises `stream`.
+ * Errors: LV_EINVAL (not a flexible index, bad sizes), LV_EDATA (ids), LV_ENOMEM, LV_ECUDA.
+ */
+lv_status lv_index_create_flex(lv_index** out, int32_t D, int32_t d, lv_dtype low_dtype,
+                               const float* Ap, const float* Bp, int64_t id_capacity);
+lv_status lv_stream_insert(lv_index* index, const void* X, lv_dtype x_dtype, int64_t b,
+                           const int32_t* ids, void* stream);
+lv_status lv_stream_remove(lv_index* index, const int32_t* ids, int64_t b, void* stream);
+lv_status lv_stream_observe_queries(lv_index* index, const float* Q, int64_t m, void* stream);
+lv_status lv_stream_stats(const lv_index* index, double* K_Q, double* K_X, int64_t* m_q, int64_t* n_x,
+                          void* stream);
+lv_status lv_stream_reproject(lv_index* index, const float* Ap, const float* Bp, void* stream);
+lv_status lv_index_export_xprime(const lv_index* index, float* Xp, int32_t* ids, void* stream);
+
 /* Sizes of the encoded index (HOST out pointers, any may be NULL). */
 lv_status lv_index_info(const lv_index* index, int64_t* n, int64_t* n_pad, int32_t* D,
                         int32_t* d, int32_t* C);

@@ -11,8 +11,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblv.so")
-SOURCES = ["lv_api.cu", "lv_score.cu", "lv_rerank.cu", "lv_proj.cu", "lv_build.cu", "lv_sort.cu"]
-HEADERS = ["lv_common.cuh", "lv_tc.cuh", "lv_internal.h", os.path.join("..", "..", "include", "lv.h")]
+SOURCES = ["lv_api.cu", "lv_stream.cu", "lv_score.cu", "lv_rerank.cu", "lv_proj.cu", "lv_build.cu", "lv_sort.cu"]
+HEADERS = ["lv_common.cuh", "lv_tc.cuh", "lv_internal.h", "lv_index.h", os.path.join("..", "..", "include", "lv.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

@@ -11,86 +11,14 @@
 #include <vector>
 
 #include "lv_common.cuh"
-#include "lv_internal.h"
+#include "lv_index.h"
 
 namespace lv {
 size_t score_smem_bytes(int d, int stages);
 }
 
-// Work decomposition of one lv_search shape (m, R) and its carve of the index workspace.
-// Chunk records are lv::kChunkInts ints: tile_begin, tile_end, cluster, tile_stride, sample_base.
-struct Plan {
-  int m_pad, QP, NS, Cap, grid, stages;
-  size_t smem;
-  bool sampled = false;       // sampled-threshold path (else: staged path)
-  bool fine_blocks = false;   // sample stage records 32-row (not 64-row) block maxima
-  int stride = 1, nblk = 0, j1 = 0, j2 = 0;
-  std::vector<std::vector<int32_t>> chunks;   // staged: one list per stage; sampled: {sample, main}
-  std::vector<int32_t> repair_chunks;         // sampled: full database, planned for one query tile
-  int total_units = 0;
-};
-struct PlanCache {
-  bool valid = false;
-  int64_t m = -1;
-  int R = -1, nsm = -1;
-  Plan pl;
-  void* Qp = nullptr;
-  void* Qr = nullptr;          // repair: gathered Q' rows
-  uint64_t* cand = nullptr;
-  int32_t* cnt = nullptr;
-  uint64_t* tau = nullptr;
-  void* Qplanes = nullptr;     // bf16 [3][m_pad][Kp]: Q split for the K1 GEMM
-  CUtensorMap tmap_q;
-  uint64_t* tau2 = nullptr;    // sampled: per-query repair threshold
-  float* bmax = nullptr;       // sampled: block maxima of the sample stage
-  int32_t* fail = nullptr;     // [4]: fail counts of the two checks, repair row counts
-  int32_t* unit_ctr = nullptr; // [kMaxScans]: zeroed work-unit counter per scan launch (dynamic unit order)
-  int32_t* fail_list = nullptr;   // [2][m_pad]
-  int32_t* slot_busy = nullptr;
-  int32_t* sel_ids = nullptr;  // [m_pad][R]
-  int32_t* sel_n = nullptr;    // [m_pad]
-  uint8_t *zero_lo = nullptr, *zero_hi = nullptr;
-  std::vector<int32_t*> chunk_info;
-  int32_t* repair_info = nullptr;
-};
-
-struct lv_index {
-  int32_t D = 0, d = 0, C = 0;
-  int32_t ds = 0;              // search dimension <= d (§3.1 flexible d: the first ds reduced coordinates)
-  lv_dtype low = LV_BF16, full = LV_F32;
-  float* A = nullptr;          // [C*d, D]
-  float* B = nullptr;          // [C*d, D]
-  int32_t Kp = 0;              // D rounded up to 64 (K1 operand planes)
-  void* A_planes = nullptr;    // bf16 [3][C*d][Kp]: A split v = h + m + l (lv_proj.cu)
-  CUtensorMap tmap_a;          // A planes, 128-row x 64-column boxes
-  void* B_planes = nullptr;    // bf16 [3][C*d][Kp]: B split, K6 operand
-  CUtensorMap tmap_b;          // B planes, d-row x 64-column boxes
-  float enc_ms[3] = {0, 0, 0}; // last encode: sort, K6, full copy (lv_encode_timing)
-  bool enc_timed = false;
-  int64_t n = 0, n_pad = 0;
-  void* X_low = nullptr;       // [n_pad, d] low dtype, cluster-sorted, 128-row padded segments
-  int32_t* perm = nullptr;     // [n_pad] sorted position -> original id (-1 padding)
-  int32_t* tile_valid = nullptr;  // [n_pad/128]
-  std::vector<int64_t> offsets;   // host [C+1] padded segment starts
-  void* X_full = nullptr;      // [n, D] full dtype, original order
-  CUtensorMap tmap_xlow;      // X_low, d columns
-  CUtensorMap tmap_xlow_s;    // X_low's first ds columns (row pitch d): the scan's B operand
-  unsigned long long* dbg_stats = nullptr;   // [8] scan event counters (debug flag 2)
-  // search workspace
-  void* ws = nullptr;
-  size_t ws_bytes = 0;
-  PlanCache plan;               // last search shape: plan + device chunk tables (uploaded once)
-  // per-kernel timing (lv_search timing = 2): event groups of 8 marks, pending until collected
-  std::vector<cudaEvent_t> ev_pool;
-  std::vector<std::vector<cudaEvent_t>> ev_pending;
-  // host-buffer staging for lv_search_host: device buffers, a copy stream, its events
-  void* hs = nullptr;
-  size_t hs_bytes = 0;
-  cudaStream_t cs = nullptr;
-  cudaEvent_t hev[4] = {};
-};
-
-namespace {
+namespace lv {
+namespace host {
 
 thread_local std::string g_err;
 
@@ -104,14 +32,8 @@ lv_status fail(lv_status s, const char* fmt, ...) {
   return s;
 }
 
-#define LV_CUDA(call)                                                                          \
-  do {                                                                                         \
-    cudaError_t e_ = (call);                                                                   \
-    if (e_ != cudaSuccess) return fail(LV_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
-  } while (0)
-
 // Device check (cached per device: cudaGetDeviceProperties costs milliseconds per call).
-lv_status check_device(int* nsm = nullptr) {
+lv_status check_device(int* nsm) {
   static int cached_sm[64] = {0};   // 0 = unknown, -1 = unsupported, else SM count
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return fail(LV_EUNSUPPORTED, "no CUDA device");
@@ -147,7 +69,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 // 2D row-major [rows, cols] of 16-bit elements (row pitch ld >= cols elements, default cols);
 // box [box_rows, ch cols]; swizzle = ch*2 bytes.
 lv_status make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int ch, bool bf16, int box_rows,
-                    int64_t ld = 0) {
+                    int64_t ld) {
   auto enc = get_encode();
   if (!enc) return fail(LV_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -173,12 +95,12 @@ double env_double(const char* name, double dflt) {
   return v ? atof(v) : dflt;
 }
 
-template <typename T>
-T* carve(uint8_t*& p, size_t count) {
-  T* r = reinterpret_cast<T*>(p);
-  p += (count * sizeof(T) + 255) / 256 * 256;
-  return r;
-}
+}  // namespace host
+}  // namespace lv
+
+using namespace lv::host;
+
+namespace {
 
 // Chunks of the given segments (tile ranges) so that units = P * QP spread evenly over the grid.
 // With stride > 1 only every stride-th tile of a segment is scanned (sample stage); the scanned
@@ -379,16 +301,6 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
 
 }  // namespace
 
-namespace lv {
-void set_error(const char* fmt, ...) {
-  char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof buf, fmt, ap);
-  va_end(ap);
-  g_err = buf;
-}
-}  // namespace lv
 
 extern "C" {
 
@@ -491,6 +403,103 @@ lv_status lv_fit_stats(const float* Q_learn, int64_t m_learn, const void* X_lear
   return LV_OK;
 }
 
+}  // extern "C"
+
+namespace lv {
+namespace host {
+// A and B stacks of the index ([a_rows, D] fp32 each, copied from device pointers) and their
+// three-bf16-plane splits: A's feeds K1 (128-row boxes), B's feeds K6 (d-row boxes) or, for the
+// flexible index, the x' GEMM (128-row boxes).  Replaces any previous operands.
+lv_status set_operands(lv_index* ix, const float* A_src, const float* B_src, cudaStream_t s) {
+  const int D = ix->D;
+  const int64_t Nc = ix->a_rows;
+  const size_t bytes = sizeof(float) * (size_t)Nc * D;
+  const size_t pbytes = (size_t)3 * Nc * ix->Kp * 2;
+  if (!ix->A && (cudaMalloc(&ix->A, bytes) != cudaSuccess || cudaMalloc(&ix->B, bytes) != cudaSuccess ||
+                 cudaMalloc(&ix->A_planes, pbytes) != cudaSuccess || cudaMalloc(&ix->B_planes, pbytes) != cudaSuccess))
+    return fail(LV_ENOMEM, "index operands: cudaMalloc failed");
+  LV_CUDA(cudaMemcpyAsync(ix->A, A_src, bytes, cudaMemcpyDeviceToDevice, s));
+  LV_CUDA(cudaMemcpyAsync(ix->B, B_src, bytes, cudaMemcpyDeviceToDevice, s));
+  LV_CUDA(lv::launch_split3(ix->A, false, Nc, Nc, D, ix->Kp, ix->A_planes, s));
+  LV_CUDA(lv::launch_split3(ix->B, false, Nc, Nc, D, ix->Kp, ix->B_planes, s));
+  if (ix->flex) {
+    ix->hA.resize((size_t)Nc * D);
+    LV_CUDA(cudaMemcpyAsync(ix->hA.data(), ix->A, bytes, cudaMemcpyDeviceToHost, s));
+  }
+  LV_CUDA(cudaStreamSynchronize(s));
+  lv_status st = make_tmap(&ix->tmap_a, ix->A_planes, 3 * Nc, ix->Kp, 64, true, 128);
+  if (!st && !ix->flex) st = make_tmap(&ix->tmap_b, ix->B_planes, 3 * Nc, ix->Kp, 64, true, ix->d);
+  if (!st && ix->flex) st = make_tmap(&ix->tmap_b128, ix->B_planes, 3 * Nc, ix->Kp, 64, true, 128);
+  return st;
+}
+
+// out[r, i] = sum_k in[r, k] W[i, k] for r < rows, i < Nc: K1's fp32-faithful tensor-core GEMM
+// (three bf16 planes of both operands, six products, fp32 TMEM) with W given by its plane tensor
+// map (w_rows rows per plane); `in` row stride D; rows in chunks of 64K (plane scratch).
+lv_status gemm3(const lv_index* ix, const void* in, bool in_f16, int64_t rows, const CUtensorMap* tw, int w_rows,
+                int Nc, void* out, int out_type, int64_t ld_out, cudaStream_t s) {
+  if (rows <= 0) return LV_OK;
+  const int D = ix->D, Kp = ix->Kp;
+  const int64_t CH = 65536;
+  const int64_t cap_pad = (std::min(rows, CH) + 127) / 128 * 128;
+  void* planes = nullptr;
+  LV_CUDA(cudaMallocAsync(&planes, (size_t)3 * cap_pad * Kp * 2, s));
+  const size_t isz = in_f16 ? 2 : 4, osz = out_type == 2 ? 4 : 2;
+  lv_status st = LV_OK;
+  for (int64_t lo = 0; lo < rows && !st; lo += CH) {
+    const int64_t r = std::min(CH, rows - lo), r_pad = (r + 127) / 128 * 128;
+    CUtensorMap tq;
+    st = make_tmap(&tq, planes, 3 * r_pad, Kp, 64, true, 128);
+    if (st) break;
+    cudaError_t e = lv::launch_split3(reinterpret_cast<const uint8_t*>(in) + (size_t)lo * D * isz, in_f16, r, r_pad, D,
+                                      Kp, planes, s);
+    if (e == cudaSuccess)
+      e = lv::launch_proj_tc(&tq, tw, (int)r_pad, Nc, w_rows, Kp, reinterpret_cast<uint8_t*>(out) + (size_t)lo * ld_out * osz,
+                             ld_out, (int)r, out_type, s);
+    if (e != cudaSuccess) st = fail(LV_ECUDA, "gemm3: %s", cudaGetErrorString(e));
+  }
+  cudaFreeAsync(planes, s);
+  return st;
+}
+
+// dst (device fp64 [D, D]) += sign * sum_r in[r] in[r]^T (K7 statistics kernel, fp32 chunks of
+// 8192 rows, fp64 reduce)
+lv_status accum_outer(const void* in, bool in_f16, int64_t rows, int D, double* dst, double sign, cudaStream_t s) {
+  if (rows <= 0) return LV_OK;
+  const int64_t kChunk = 8192;
+  const int nch = (int)((rows + kChunk - 1) / kChunk);
+  std::vector<int64_t> hl(2 * nch);
+  std::vector<int32_t> ho(nch, 0);
+  for (int c = 0; c < nch; ++c) {
+    hl[c] = c * kChunk;
+    hl[nch + c] = std::min(rows, (c + 1) * kChunk);
+  }
+  const size_t DD = (size_t)D * D;
+  float* part = nullptr;
+  int64_t* dlo = nullptr;
+  int32_t* down = nullptr;
+  double* tmp = nullptr;
+  LV_CUDA(cudaMallocAsync(&part, sizeof(float) * DD * nch, s));
+  LV_CUDA(cudaMallocAsync(&dlo, sizeof(int64_t) * 2 * nch, s));
+  LV_CUDA(cudaMallocAsync(&down, sizeof(int32_t) * nch, s));
+  LV_CUDA(cudaMallocAsync(&tmp, sizeof(double) * DD, s));
+  LV_CUDA(cudaMemcpyAsync(dlo, hl.data(), sizeof(int64_t) * 2 * nch, cudaMemcpyHostToDevice, s));
+  LV_CUDA(cudaMemcpyAsync(down, ho.data(), sizeof(int32_t) * nch, cudaMemcpyHostToDevice, s));
+  LV_CUDA(lv::launch_stats(in, in_f16, D, nullptr, nch, dlo, dlo + nch, D, part, s));
+  LV_CUDA(lv::launch_stats_reduce(part, nch, down, 1, D, tmp, s));
+  LV_CUDA(lv::launch_axpy_f64(dst, tmp, sign, (int64_t)DD, s));
+  cudaFreeAsync(part, s);
+  cudaFreeAsync(dlo, s);
+  cudaFreeAsync(down, s);
+  cudaFreeAsync(tmp, s);
+  LV_CUDA(cudaStreamSynchronize(s));   // the host vectors above are copy sources
+  return LV_OK;
+}
+}  // namespace host
+}  // namespace lv
+
+extern "C" {
+
 lv_status lv_index_create(lv_index** out, int32_t D, int32_t d, int32_t C, lv_dtype low_dtype, lv_dtype full_dtype,
                           const float* A_stack, const float* B_stack) {
   lv_status st = check_device();
@@ -509,44 +518,52 @@ lv_status lv_index_create(lv_index** out, int32_t D, int32_t d, int32_t C, lv_dt
   ix->C = C;
   ix->low = low_dtype;
   ix->full = full_dtype;
-  const size_t bytes = sizeof(float) * (size_t)C * d * D;
-  if (cudaMalloc(&ix->A, bytes) != cudaSuccess || cudaMalloc(&ix->B, bytes) != cudaSuccess) {
-    lv_index_destroy(ix);
-    return fail(LV_ENOMEM, "lv_index_create: cudaMalloc failed");
-  }
-  if (cudaMemcpy(ix->A, A_stack, bytes, cudaMemcpyDeviceToDevice) != cudaSuccess ||
-      cudaMemcpy(ix->B, B_stack, bytes, cudaMemcpyDeviceToDevice) != cudaSuccess) {
-    lv_index_destroy(ix);
-    return fail(LV_ECUDA, "lv_index_create: copy failed");
-  }
-  // K1 operand: A split into three bf16 planes once per index
   ix->Kp = (D + 63) / 64 * 64;
-  const int64_t Nc = (int64_t)C * d;
-  if (cudaMalloc(&ix->A_planes, (size_t)3 * Nc * ix->Kp * 2) != cudaSuccess) {
-    lv_index_destroy(ix);
-    return fail(LV_ENOMEM, "lv_index_create: cudaMalloc failed");
-  }
-  if (lv::launch_split3(ix->A, Nc, Nc, D, ix->Kp, ix->A_planes, 0) != cudaSuccess ||
-      cudaDeviceSynchronize() != cudaSuccess) {
-    lv_index_destroy(ix);
-    return fail(LV_ECUDA, "lv_index_create: split failed");
-  }
-  st = make_tmap(&ix->tmap_a, ix->A_planes, 3 * Nc, ix->Kp, 64, true, 128);
+  ix->a_rows = C * d;
+  st = lv::host::set_operands(ix, A_stack, B_stack, 0);
   if (st) {
     lv_index_destroy(ix);
     return st;
   }
-  // K6 operand: B split the same way
-  if (cudaMalloc(&ix->B_planes, (size_t)3 * Nc * ix->Kp * 2) != cudaSuccess) {
+  *out = ix;
+  return LV_OK;
+}
+
+lv_status lv_index_create_flex(lv_index** out, int32_t D, int32_t d, lv_dtype low_dtype, const float* Ap,
+                               const float* Bp, int64_t id_capacity) {
+  lv_status st = check_device();
+  if (st) return st;
+  if (!out || !Ap || !Bp) return fail(LV_EINVAL, "lv_index_create_flex: NULL argument");
+  if (d < 32 || d > D || d % 32 != 0 || d > 192)
+    return fail(LV_EINVAL, "lv_index_create_flex: need 32 <= d <= min(D,192), d %% 32 == 0 (d=%d)", d);
+  if (D % 4) return fail(LV_EINVAL, "lv_index_create_flex: D=%d breaks 16-byte fp32 rows", D);
+  if (low_dtype != LV_BF16 && low_dtype != LV_F16) return fail(LV_EINVAL, "lv_index_create_flex: low_dtype must be BF16/F16");
+  if (id_capacity < 1 || id_capacity > (int64_t)INT32_MAX - 256)
+    return fail(LV_EINVAL, "lv_index_create_flex: id_capacity outside [1, 2^31 - 256)");
+  lv_index* ix = new lv_index();
+  ix->flex = true;
+  ix->D = D;
+  ix->d = d;
+  ix->ds = d;
+  ix->C = 1;
+  ix->low = low_dtype;
+  ix->full = LV_F32;
+  ix->Kp = (D + 63) / 64 * 64;
+  ix->a_rows = D;
+  ix->id_cap = id_capacity;
+  const size_t DD = (size_t)D * D;
+  if (cudaMalloc(&ix->KQ, DD * 8) != cudaSuccess || cudaMalloc(&ix->KX, DD * 8) != cudaSuccess ||
+      cudaMalloc(&ix->inv, sizeof(int32_t) * (size_t)id_capacity) != cudaSuccess) {
     lv_index_destroy(ix);
-    return fail(LV_ENOMEM, "lv_index_create: cudaMalloc failed");
+    return fail(LV_ENOMEM, "lv_index_create_flex: cudaMalloc failed");
   }
-  if (lv::launch_split3(ix->B, Nc, Nc, D, ix->Kp, ix->B_planes, 0) != cudaSuccess ||
-      cudaDeviceSynchronize() != cudaSuccess) {
+  if (cudaMemset(ix->KQ, 0, DD * 8) != cudaSuccess || cudaMemset(ix->KX, 0, DD * 8) != cudaSuccess ||
+      cudaMemset(ix->inv, 0xFF, sizeof(int32_t) * (size_t)id_capacity) != cudaSuccess) {
     lv_index_destroy(ix);
-    return fail(LV_ECUDA, "lv_index_create: split failed");
+    return fail(LV_ECUDA, "lv_index_create_flex: memset failed");
   }
-  st = make_tmap(&ix->tmap_b, ix->B_planes, 3 * Nc, ix->Kp, 64, true, d);
+  ix->h_inv.assign((size_t)id_capacity, -1);
+  st = lv::host::set_operands(ix, Ap, Bp, 0);
   if (st) {
     lv_index_destroy(ix);
     return st;
@@ -572,6 +589,7 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
   if (st) return st;
   if (!ix || !X || n <= 0) return fail(LV_EINVAL, "lv_encode_database: bad arguments");
   if (x_dtype != LV_F32 && x_dtype != LV_F16) return fail(LV_EINVAL, "lv_encode_database: x_dtype must be F32/F16");
+  if (ix->flex) return lv::host::flex_encode(ix, X, x_dtype, n, assign, (cudaStream_t)stream);
   if (ix->C > 1 && !assign) return fail(LV_EINVAL, "lv_encode_database: assign required when C > 1");
   if (n > (int64_t)INT32_MAX - 128 * (int64_t)ix->C) return fail(LV_EINVAL, "lv_encode_database: n too large");
   cudaStream_t s = (cudaStream_t)stream;
@@ -690,9 +708,9 @@ lv_status lv_project_queries(const lv_index* ix, const float* Q, int64_t m, void
     cudaFreeAsync(planes, s);
     return st;
   }
-  LV_CUDA(lv::launch_split3(Q, m, m_pad, ix->D, ix->Kp, planes, s));
-  LV_CUDA(lv::launch_proj_tc(&tq, &ix->tmap_a, (int)m_pad, Cd, ix->C * ix->d, ix->Kp, Qp, Cd, (int)m,
-                             ix->low == LV_BF16, s));
+  LV_CUDA(lv::launch_split3(Q, false, m, m_pad, ix->D, ix->Kp, planes, s));
+  LV_CUDA(lv::launch_proj_tc(&tq, &ix->tmap_a, (int)m_pad, Cd, ix->a_rows, ix->Kp, Qp, Cd, (int)m,
+                             ix->low == LV_BF16 ? 0 : 1, s));
   LV_CUDA(cudaFreeAsync(planes, s));
   return LV_OK;
 }
@@ -755,6 +773,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
                   (nchunk_ints * 4 + 256 * (pl.chunks.size() + 2));
     if (pl.sampled)
       need += (mp * Cd * 2 + 256) + (mp * 8 + 256) + ((size_t)pl.nblk * mp * 4 + 256) + (2 * mp * 4 + 256);
+    if (ix->flex) need += mp * (size_t)ix->D * 4 + 256;
     if (need > ix->ws_bytes) {
       LV_CUDA(cudaStreamSynchronize(s));   // the old workspace may still be in use on s
       cudaFree(ix->ws);
@@ -784,6 +803,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
       pc.bmax = carve<float>(p, (size_t)pl.nblk * mp);
       pc.fail_list = carve<int32_t>(p, 2 * mp);
     }
+    pc.Qx = ix->flex ? carve<float>(p, mp * (size_t)ix->D) : nullptr;
     pc.chunk_info.assign(pl.chunks.size(), nullptr);
     for (size_t k = 0; k < pl.chunks.size(); ++k) pc.chunk_info[k] = carve<int32_t>(p, pl.chunks[k].size() + 1);
     pc.repair_info = carve<int32_t>(p, pl.repair_chunks.size() + 1);
@@ -827,10 +847,15 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
   int launches = 0;
   LV_CUDA(cudaMemsetAsync(pc.zero_lo, 0, pc.zero_hi - pc.zero_lo, s));
   // K1 projection (rows >= m are zero)
-  LV_CUDA(lv::launch_split3(Q, m, pl.m_pad, ix->D, ix->Kp, pc.Qplanes, s));
-  LV_CUDA(lv::launch_proj_tc(&pc.tmap_q, &ix->tmap_a, pl.m_pad, Cd, ix->C * ix->d, ix->Kp, Qp, Cd, pl.m_pad,
-                             ix->low == LV_BF16, s));
+  LV_CUDA(lv::launch_split3(Q, false, m, pl.m_pad, ix->D, ix->Kp, pc.Qplanes, s));
+  LV_CUDA(lv::launch_proj_tc(&pc.tmap_q, &ix->tmap_a, pl.m_pad, Cd, ix->a_rows, ix->Kp, Qp, Cd, pl.m_pad,
+                             ix->low == LV_BF16 ? 0 : 1, s));
   launches += 2;
+  if (ix->flex) {
+    // the re-rank's query side A'q (all D rows of A', fp32): <A'q, x'> = <q, x> (Eq.(12))
+    LV_CUDA(lv::launch_proj_tc(&pc.tmap_q, &ix->tmap_a, pl.m_pad, ix->D, ix->a_rows, ix->Kp, pc.Qx, ix->D, pl.m_pad, 2, s));
+    ++launches;
+  }
   if ((st = mark(1))) return st;
   lv::ScoreArgs sa;
   sa.Qp = Qp;
@@ -844,7 +869,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
   sa.Cap = pl.Cap;
   sa.stages = pl.stages;
   sa.tile_valid = ix->tile_valid;
-  sa.perm = ix->C > 1 ? ix->perm : nullptr;
+  sa.perm = (ix->C > 1 || ix->flex) ? ix->perm : nullptr;   // keys carry original / external ids
   sa.cand = pc.cand;
   sa.cnt = pc.cnt;
   sa.tau = pc.tau;
@@ -900,9 +925,10 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
   ra.Cap = pl.Cap;
   ra.cand = pc.cand;
   ra.cnt = pc.cnt;
-  ra.Q = Q;
+  ra.Q = ix->flex ? pc.Qx : Q;                 // flex: <A'q, x'> (Eq.(12)); else <q, x>
   ra.X = ix->X_full;
   ra.full_f16 = ix->full == LV_F16;
+  ra.row_of_id = ix->flex ? ix->inv : nullptr;
   ra.ids = ids;
   ra.scores = scores;
   ra.cand_ids = dbg ? dbg->cand_ids : nullptr;
@@ -1124,7 +1150,8 @@ lv_status lv_search_host(lv_index* ix, const float* Q_host, int64_t m, int32_t k
   // two query batches when the batch is large: batch 1's upload (copy stream) overlaps batch 0's
   // search, batch 0's download overlaps batch 1's search
   int64_t nb = 1, mb = m;
-  if (m >= 4096) batch_layout(m, std::min<int64_t>(max_batch(), (m + 1) / 2 + 127), &nb, &mb);
+  const bool split = env_double("LV_HOST_BATCHES", 2.0) >= 2.0;   // 1: one batch (no copy/compute overlap)
+  if (m >= 4096 && split) batch_layout(m, std::min<int64_t>(max_batch(), (m + 1) / 2 + 127), &nb, &mb);
   if (nb > 2) batch_layout(m, max_batch(), &nb, &mb);
   const int64_t D = ix->D;
   std::vector<int64_t> lo(nb), hi(nb), off(nb);
@@ -1269,6 +1296,9 @@ lv_status lv_index_export(const lv_index* ix, void* X_low, int32_t* perm, int64_
 void lv_index_destroy(lv_index* ix) {
   if (!ix) return;
   free_db(ix);
+  cudaFree(ix->inv);
+  cudaFree(ix->KQ);
+  cudaFree(ix->KX);
   cudaFree(ix->A);
   cudaFree(ix->B);
   cudaFree(ix->dbg_stats);

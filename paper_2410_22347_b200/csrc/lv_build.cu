@@ -5,6 +5,7 @@
 //  row normalisation x~ = x / ||x||              (Alg. 5 line 1)
 // All products accumulate in fp32 in a fixed order (deterministic); chunk partials are summed
 // in fp64 in chunk order.
+#include <algorithm>
 #include <cfloat>
 
 #include "lv_common.cuh"
@@ -260,6 +261,67 @@ cudaError_t launch_centre_sums(const void* X, int x_f16, int64_t n, int D, const
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_centre_reduce<<<296, 256, 0, s>>>(partial, pcount, nch, C, D, sums, counts);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------- flexible / streaming index
+// X_low[r, 0:d] = RNE(x'_r[0:d]): the stored reduced vectors are the first d coordinates of the
+// stored x' = P'W x (Eq.(10)), rounded once to the storage dtype.
+template <typename TO>
+__global__ void k_prefix_round(const float* __restrict__ Xp, int D, int64_t lo, int64_t hi, TO* __restrict__ out, int d) {
+  const int64_t total = (hi - lo) * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = lo + e / d;
+    const int j = (int)(e % d);
+    out[r * d + j] = from_f32<TO>(Xp[r * D + j]);
+  }
+}
+
+cudaError_t launch_prefix_round(const float* Xp, int D, int64_t lo, int64_t hi, void* X_low, int d, bool bf16,
+                                cudaStream_t s) {
+  if (hi <= lo) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>(((hi - lo) * d + 255) / 256, 148 * 16);
+  if (bf16) k_prefix_round<__nv_bfloat16><<<blocks, 256, 0, s>>>(Xp, D, lo, hi, (__nv_bfloat16*)X_low, d);
+  else k_prefix_round<__half><<<blocks, 256, 0, s>>>(Xp, D, lo, hi, (__half*)X_low, d);
+  return cudaGetLastError();
+}
+
+// removal compaction: row dst[i] takes row src[i] (sources are rows past the new end, targets are
+// holes before it, so no row is both read and written)
+__global__ void k_move_rows(float* __restrict__ Xp, int D, uint16_t* __restrict__ X_low, int d,
+                            const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int npairs) {
+  const int i = blockIdx.x;
+  if (i >= npairs) return;
+  const int64_t a = src[i], b = dst[i];
+  for (int j = threadIdx.x; j < D; j += blockDim.x) Xp[b * D + j] = Xp[a * D + j];
+  for (int j = threadIdx.x; j < d; j += blockDim.x) X_low[b * d + j] = X_low[a * d + j];
+}
+
+cudaError_t launch_move_rows(float* Xp, int D, void* X_low, int d, const int32_t* src, const int32_t* dst, int npairs,
+                             cudaStream_t s) {
+  if (npairs <= 0) return cudaSuccess;
+  k_move_rows<<<npairs, 256, 0, s>>>(Xp, D, (uint16_t*)X_low, d, src, dst, npairs);
+  return cudaGetLastError();
+}
+
+__global__ void k_gather_rows(const float* __restrict__ Xp, int D, const int32_t* __restrict__ rows, float* __restrict__ out) {
+  const int64_t r = rows[blockIdx.x];
+  for (int j = threadIdx.x; j < D; j += blockDim.x) out[(int64_t)blockIdx.x * D + j] = Xp[r * D + j];
+}
+
+cudaError_t launch_gather_rows(const float* Xp, int D, const int32_t* rows, int nrows, float* out, cudaStream_t s) {
+  if (nrows <= 0) return cudaSuccess;
+  k_gather_rows<<<nrows, 256, 0, s>>>(Xp, D, rows, out);
+  return cudaGetLastError();
+}
+
+__global__ void k_axpy_f64(double* __restrict__ K, const double* __restrict__ T, double alpha, int64_t count) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x)
+    K[e] += alpha * T[e];
+}
+
+cudaError_t launch_axpy_f64(double* K, const double* T, double alpha, int64_t count, cudaStream_t s) {
+  k_axpy_f64<<<296, 256, 0, s>>>(K, T, alpha, count);
   return cudaGetLastError();
 }
 

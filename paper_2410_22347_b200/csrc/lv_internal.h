@@ -11,7 +11,6 @@
 
 namespace lv {
 
-void set_error(const char* fmt, ...);
 
 constexpr int kChunkInts = 5;   // chunk_info record: tile_begin, tile_end, cluster, tile_stride, sample_base
 
@@ -41,7 +40,8 @@ struct ScoreArgs {
   const int32_t* m_dev;        // device query count (repair passes; overrides m and QP), or nullptr
   int64_t n_pad;
   int flags;                   // debug: bit0 = epilogue skips top-R (MMA/TMA throughput probe),
-                               //        bit1 = count events into stats, bit2 = detect hits but drop them
+                               //        bit1 = count events into stats, bit2 = detect hits but drop them,
+                               //        bit5 = no TMA loads (stale tiles), bit6 = one MMA K step per tile
   unsigned long long* stats;   // debug counters [8] or nullptr: hit warp-tiles, appends, compactions, wait spins
   int32_t* unit_ctr;           // zeroed work-unit counter of this launch (dynamic unit order), or nullptr (static)
 };
@@ -64,6 +64,7 @@ struct RerankArgs {
   float* cand_scores;          // [m, R] or nullptr
   const int32_t* qmap;         // list row -> query (Q row, output row), or nullptr (identity)
   const int32_t* m_dev;        // device row count (rows >= it exit), or nullptr (m)
+  const int32_t* row_of_id;    // X row of a candidate id (flexible / streaming index), or nullptr (row = id)
   int checked;                 // rows with < R keys are not answered but appended to fail_list
   int32_t* fail_count;
   int32_t* fail_list;
@@ -81,11 +82,12 @@ cudaError_t launch_tau_merge(uint64_t* cand, int32_t* cnt, uint64_t* tau, int NS
                              cudaStream_t s);
 
 // K1 on tensor cores (lv_proj.cu): three-plane bf16 split and the six-product GEMM.
-cudaError_t launch_split3(const float* in, int64_t rows_valid, int64_t rows_pad, int D, int Kp, void* out,
+cudaError_t launch_split3(const void* in, bool in_f16, int64_t rows_valid, int64_t rows_pad, int D, int Kp, void* out,
                           cudaStream_t s);
-// Q' [m_pad rows, Nc columns] = the first Nc rows of the A stack (a_rows rows per plane) times Q
+// Q' [m_pad rows, Nc columns] = the first Nc rows of the A stack (a_rows rows per plane) times Q;
+// out_type 0 = bf16, 1 = fp16, 2 = fp32
 cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a, int m_pad, int Nc, int a_rows, int Kp,
-                           void* out, int64_t ld_out, int rows_store, bool out_bf16, cudaStream_t s);
+                           void* out, int64_t ld_out, int rows_store, int out_type, cudaStream_t s);
 // K6 on tensor cores: out[r, :] = RNE(B_{c(r)} X[perm[r], :]) for 128-row tiles (tile_wrow[2t] = c*d),
 // CTA i encodes tile order[i] (nullptr: tile i)
 // (three bf16 planes; two for bf16 storage when !planes3)
@@ -108,6 +110,16 @@ cudaError_t launch_cluster_scatter(const int32_t* assign, int64_t n, int C, cons
                                    int32_t* perm, cudaStream_t s);
 
 cudaError_t launch_convert(const void* in, int in_f16, void* out, int out_f16, int64_t count, cudaStream_t s);
+// X_low[r, 0:d] = RNE(Xp[r, 0:d]) for rows [lo, hi) (Xp fp32, row stride D)
+cudaError_t launch_prefix_round(const float* Xp, int D, int64_t lo, int64_t hi, void* X_low, int d, bool bf16,
+                                cudaStream_t s);
+// rows dst[i] <- src[i] of Xp (D floats) and X_low (d 16-bit elements), i < npairs (disjoint sets)
+cudaError_t launch_move_rows(float* Xp, int D, void* X_low, int d, const int32_t* src, const int32_t* dst, int npairs,
+                             cudaStream_t s);
+// out[i, :] = Xp[rows[i], :] (D floats)
+cudaError_t launch_gather_rows(const float* Xp, int D, const int32_t* rows, int nrows, float* out, cudaStream_t s);
+// K += alpha * T (fp64, count elements)
+cudaError_t launch_axpy_f64(double* K, const double* T, double alpha, int64_t count, cudaStream_t s);
 cudaError_t launch_assign(const void* X, int x_f16, int64_t n, int D, const float* centres, int C, int32_t* assign,
                           float* best, int accumulate, cudaStream_t s);
 cudaError_t launch_normalize(const void* X, int x_f16, int64_t n, int D, float* out, cudaStream_t s);

@@ -34,14 +34,15 @@ constexpr size_t kPjSmem = kPjStages * kPjStageBytes + 1024 + 256;
 // plane pairs (Q plane, A plane) of the six retained products
 __constant__ int kPjProd[6][2] = {{0, 0}, {0, 1}, {1, 0}, {0, 2}, {2, 0}, {1, 1}};
 
-// in fp32 [rows_valid, D] (row stride D) -> out bf16 [3][rows_pad][Kp] (zero padded)
-__global__ void k_split3(const float* __restrict__ in, int64_t rows_valid, int64_t rows_pad, int D, int Kp,
+// in fp32 / fp16 [rows_valid, D] (row stride D) -> out bf16 [3][rows_pad][Kp] (zero padded)
+template <typename TIn>
+__global__ void k_split3(const TIn* __restrict__ in, int64_t rows_valid, int64_t rows_pad, int D, int Kp,
                          __nv_bfloat16* __restrict__ out) {
   const int64_t total = rows_pad * Kp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / Kp;
     const int k = (int)(e - r * Kp);
-    const float v = (r < rows_valid && k < D) ? in[r * D + k] : 0.f;
+    const float v = (r < rows_valid && k < D) ? to_f32(in[r * D + k]) : 0.f;
     const __nv_bfloat16 h = __float2bfloat16_rn(v);
     const float r1 = v - __bfloat162float(h);   // exact in fp32
     const __nv_bfloat16 mm = __float2bfloat16_rn(r1);
@@ -53,7 +54,9 @@ __global__ void k_split3(const float* __restrict__ in, int64_t rows_valid, int64
   }
 }
 
-template <bool kOutBF16>
+// kOut: 0 = bf16, 1 = fp16 (one RNE of the fp32 sum), 2 = fp32 (the fp32 sum itself: x' = B' x,
+// A' q and the streaming re-projection of §3.1-3.2)
+template <int kOut>
 __global__ void __launch_bounds__(kPjThreads, 1)
     k_proj_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_a, int m_pad,
               int Nc, int a_rows, int Kp, void* __restrict__ out, int64_t ld_out, int rows_store) {
@@ -151,11 +154,19 @@ __global__ void __launch_bounds__(kPjThreads, 1)
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] += t[j];
       const int c0 = n0 + cb * 32;
-      if (row < rows_store && c0 < Nc) {
+      if (kOut == 2 && row < rows_store && c0 < Nc) {
+        float* dst = reinterpret_cast<float*>(out) + (size_t)row * ld_out + c0;
+        if (c0 + 32 <= Nc) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) reinterpret_cast<float4*>(dst)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        } else {
+          for (int j = 0; j < Nc - c0; ++j) dst[j] = v[j];
+        }
+      } else if (row < rows_store && c0 < Nc) {
         uint32_t w[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          if (kOutBF16) {
+          if (kOut == 0) {
             const __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
             w[j] = *reinterpret_cast<const uint32_t*>(&h2);
           } else {
@@ -179,17 +190,20 @@ __global__ void __launch_bounds__(kPjThreads, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-cudaError_t launch_split3(const float* in, int64_t rows_valid, int64_t rows_pad, int D, int Kp, void* out,
+cudaError_t launch_split3(const void* in, bool in_f16, int64_t rows_valid, int64_t rows_pad, int D, int Kp, void* out,
                           cudaStream_t s) {
   const int64_t total = rows_pad * Kp;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  k_split3<<<blocks, 256, 0, s>>>(in, rows_valid, rows_pad, D, Kp, reinterpret_cast<__nv_bfloat16*>(out));
+  if (in_f16)
+    k_split3<__half><<<blocks, 256, 0, s>>>((const __half*)in, rows_valid, rows_pad, D, Kp, reinterpret_cast<__nv_bfloat16*>(out));
+  else
+    k_split3<float><<<blocks, 256, 0, s>>>((const float*)in, rows_valid, rows_pad, D, Kp, reinterpret_cast<__nv_bfloat16*>(out));
   return cudaGetLastError();
 }
 
 cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a, int m_pad, int Nc, int a_rows, int Kp,
-                           void* out, int64_t ld_out, int rows_store, bool out_bf16, cudaStream_t s) {
-  auto kern = out_bf16 ? k_proj_tc<true> : k_proj_tc<false>;
+                           void* out, int64_t ld_out, int rows_store, int out_type, cudaStream_t s) {
+  auto kern = out_type == 0 ? k_proj_tc<0> : (out_type == 1 ? k_proj_tc<1> : k_proj_tc<2>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPjSmem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((Nc + 127) / 128), (unsigned)(m_pad / 128));

@@ -352,7 +352,8 @@ __global__ void __launch_bounds__(128) k_rerank_topk(const RerankArgs a) {
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         id[g] = i0 + g < R ? ids[i0 + g] : ids[i0];
-        const uint4* row = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(a.X) + (size_t)id[g] * rowbytes);
+        const int64_t xrow = a.row_of_id ? __ldg(a.row_of_id + id[g]) : id[g];
+        const uint4* row = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(a.X) + (size_t)xrow * rowbytes);
 #pragma unroll
         for (int j = 0; j < kVPL; ++j) {
           const int v = lane + 32 * j;

@@ -338,9 +338,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int t0 = ci[0], t1 = ci[1], ts_ = ci[3];
         for (int t = t0; t < t1; t += ts_) {
           tc::mbar_wait_sleep(b_empty + stage, phase ^ 1);
-          tc::mbar_arrive_expect_tx(b_full + stage, nch * box_bytes);
-          for (int k = 0; k < nch; ++k)
-            tc::tma_load_2d(sB + (stage * nch + k) * box_bytes, &tmap_xlow, b_full + stage, k * kCH, t * kN);
+          if (a.flags & 32) {   // probe: no loads (the MMA reads stale tiles): the scan without L2 -> smem traffic
+            tc::mbar_arrive(b_full + stage);
+          } else {
+            tc::mbar_arrive_expect_tx(b_full + stage, nch * box_bytes);
+            for (int k = 0; k < nch; ++k)
+              tc::tma_load_2d(sB + (stage * nch + k) * box_bytes, &tmap_xlow, b_full + stage, k * kCH, t * kN);
+          }
           if (++stage == a.stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -373,8 +377,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (issuer) {
           const uint64_t bd0 = tc::make_sdesc(sB_addr + (uint32_t)stage * nch * box_bytes, kCH * 2);
           const uint32_t dt = tmem_base + acc_col0 + (uint32_t)acc * kN;
+          const int nk = (a.flags & 64) ? 1 : d / 16;   // probe: one K step per tile (no tensor-pipe bound)
 #pragma unroll
           for (int kk = 0; kk < d / 16; ++kk) {
+            if (kk >= nk) break;
             // K step kk: box kk*16/kCH, byte offset (kk*16 % kCH)*2 inside the swizzled row
             const uint32_t off16 = (((uint32_t)((kk * 16) / kCH) * box_bytes) + (uint32_t)((kk * 16) % kCH) * 2u) >> 4;
             tc::mma_f16_ts(dt, at + (uint32_t)kk * 8u, bd0 + off16, idesc, kk > 0 ? 1u : 0u);

@@ -56,6 +56,24 @@ def fit_from_stats(KQ: np.ndarray, KX: np.ndarray, m_learn: int, d: int) -> dict
     return {"A": A, "B": B, "W": W, "Wp": Wp, "gaps": gaps}
 
 
+def flexible_from_stats(KQ: np.ndarray, KX: np.ndarray, m_learn: int) -> dict:
+    """§3.1-3.2: A' = P'W^+, B' = P'W with all D eigenvectors P' of W K_X W by decreasing
+    eigenvalue (the stored x' = B'x admits any prefix d, and <A'q, x'> = <q, x>, Eq.(12)); used for
+    lv_index_create_flex and for every streaming refresh (lv_stream_stats -> lv_stream_reproject)."""
+    D = KQ.shape[0]
+    f = fit_from_stats(KQ, np.asarray(KX).reshape(1, D, D), m_learn, D)
+    return {"A": f["A"][0], "B": f["B"][0], "W": f["W"], "Wp": f["Wp"]}
+
+
+def stream_refresh(index) -> dict:
+    """One refresh of the streaming index: statistics -> eig route -> re-projection of
+    every stored x' on the GPU."""
+    KQ, KX, m_q, _ = lv.lv_stream_stats(index)
+    f = flexible_from_stats(KQ, KX, m_q)
+    lv.lv_stream_reproject(index, f["A"], f["B"])
+    return f
+
+
 def leanvec_sphering_fit(Q_learn: torch.Tensor, X_learn: torch.Tensor, d: int) -> dict:
     """Alg. 2 through the statistics route: lv_fit_stats on the GPU + host eig."""
     KQ, KX = lv.lv_fit_stats(Q_learn, X_learn, None, 1)

@@ -22,7 +22,9 @@ _TORCH_DT = {LV_F32: torch.float32, LV_F16: torch.float16, LV_BF16: torch.bfloat
 EXPORTS = ["lv_last_error", "lv_version", "lv_fit_stats", "lv_index_create", "lv_encode_database",
            "lv_project_queries", "lv_search", "lv_search_host", "lv_timing_collect", "lv_encode_timing", "lv_assign_tags",
            "lv_index_info", "lv_index_export", "lv_index_destroy", "lv_index_set_search_dim",
-           "lv_index_get_search_dim", "lv_normalize_rows", "lv_kmeans_assign", "lv_kmeans_centre_sums"]
+           "lv_index_get_search_dim", "lv_normalize_rows", "lv_kmeans_assign", "lv_kmeans_centre_sums",
+           "lv_index_create_flex", "lv_stream_insert", "lv_stream_remove", "lv_stream_observe_queries",
+           "lv_stream_stats", "lv_stream_reproject", "lv_index_export_xprime"]
 
 
 class LVError(RuntimeError):
@@ -65,6 +67,13 @@ def lib():
             "lv_index_get_search_dim": [vp, ctypes.POINTER(i32)],
             "lv_assign_tags": [vp, i32, i64, i32, vp, i32, vp, vp],
             "lv_normalize_rows": [vp, i32, i64, i32, vp, vp],
+            "lv_index_create_flex": [ctypes.POINTER(vp), i32, i32, i32, vp, vp, i64],
+            "lv_stream_insert": [vp, vp, i32, i64, vp, vp],
+            "lv_stream_remove": [vp, vp, i64, vp],
+            "lv_stream_observe_queries": [vp, vp, i64, vp],
+            "lv_stream_stats": [vp, vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64), vp],
+            "lv_stream_reproject": [vp, vp, vp, vp],
+            "lv_index_export_xprime": [vp, vp, vp, vp],
             "lv_kmeans_assign": [vp, i32, i64, i32, vp, i32, vp, vp, i32, vp],
             "lv_kmeans_centre_sums": [vp, i32, i64, i32, vp, i32, vp, vp, vp],
             "lv_index_info": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32),
@@ -142,12 +151,19 @@ def lv_fit_stats(Q_learn: torch.Tensor, X_learn: torch.Tensor, assign_learn: tor
 class Index:
     """Owns an lv_index* (freed by lv_index_destroy)."""
 
-    def __init__(self, D: int, d: int, C: int, low: str, full: str, A_stack, B_stack):
+    def __init__(self, D: int, d: int, C: int, low: str, full: str, A_stack, B_stack, id_capacity: int = 0):
         A = _dev(torch.as_tensor(A_stack, dtype=torch.float32, device="cuda"), torch.float32)
         B = _dev(torch.as_tensor(B_stack, dtype=torch.float32, device="cuda"), torch.float32)
         h = ctypes.c_void_p()
-        _check(lib().lv_index_create(ctypes.byref(h), D, d, C, _DT[low], _DT[full], _ptr(A), _ptr(B)),
-               "lv_index_create")
+        self.flex = id_capacity > 0
+        if self.flex:
+            if tuple(A.shape) != (D, D) or tuple(B.shape) != (D, D):
+                raise LVError("lv_index_create_flex: A', B' must be [D, D]")
+            _check(lib().lv_index_create_flex(ctypes.byref(h), D, d, _DT[low], _ptr(A), _ptr(B), int(id_capacity)),
+                   "lv_index_create_flex")
+        else:
+            _check(lib().lv_index_create(ctypes.byref(h), D, d, C, _DT[low], _DT[full], _ptr(A), _ptr(B)),
+                   "lv_index_create")
         self.h = h
         self.D, self.d, self.C, self.low, self.full = D, d, C, low, full
         torch.cuda.synchronize()
@@ -170,6 +186,64 @@ class Index:
 
 def lv_index_create(D, d, C, low, full, A_stack, B_stack) -> Index:
     return Index(D, d, C, low, full, A_stack, B_stack)
+
+
+def lv_index_create_flex(D: int, d: int, low: str, A_prime, B_prime, id_capacity: int) -> Index:
+    """§3.1 index storing x' = B'x (A' = P'W^+, B' = P'W, [D, D]); X_low = the first d coordinates."""
+    return Index(D, d, 1, low, "fp32", A_prime, B_prime, id_capacity=id_capacity)
+
+
+def _host_ids(ids) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(ids, dtype=np.int32))
+    if a.ndim != 1:
+        raise LVError("ids must be a 1-D array")
+    return a
+
+
+def lv_stream_insert(index: Index, X: torch.Tensor, ids):
+    X = _dev(X)
+    a = _host_ids(ids)
+    if a.shape[0] != X.shape[0]:
+        raise LVError("lv_stream_insert: one id per row")
+    _check(lib().lv_stream_insert(index.h, _ptr(X), _xdtype(X), X.shape[0], a.ctypes.data_as(ctypes.c_void_p),
+                                  _stream()), "lv_stream_insert")
+
+
+def lv_stream_remove(index: Index, ids):
+    a = _host_ids(ids)
+    _check(lib().lv_stream_remove(index.h, a.ctypes.data_as(ctypes.c_void_p), a.shape[0], _stream()), "lv_stream_remove")
+
+
+def lv_stream_observe_queries(index: Index, Q: torch.Tensor):
+    Q = _dev(Q, torch.float32)
+    _check(lib().lv_stream_observe_queries(index.h, _ptr(Q), Q.shape[0], _stream()), "lv_stream_observe_queries")
+
+
+def lv_stream_stats(index: Index):
+    """(K_Q, K_X) fp64 [D, D] numpy, m_q, n."""
+    KQ = np.zeros((index.D, index.D))
+    KX = np.zeros((index.D, index.D))
+    mq, n = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().lv_stream_stats(index.h, KQ.ctypes.data_as(ctypes.c_void_p), KX.ctypes.data_as(ctypes.c_void_p),
+                                 ctypes.byref(mq), ctypes.byref(n), _stream()), "lv_stream_stats")
+    return KQ, KX, mq.value, n.value
+
+
+def lv_stream_reproject(index: Index, A_prime, B_prime):
+    A = _dev(torch.as_tensor(A_prime, dtype=torch.float32, device="cuda"), torch.float32)
+    B = _dev(torch.as_tensor(B_prime, dtype=torch.float32, device="cuda"), torch.float32)
+    if tuple(A.shape) != (index.D, index.D) or tuple(B.shape) != (index.D, index.D):
+        raise LVError("lv_stream_reproject: A', B' must be [D, D]")
+    _check(lib().lv_stream_reproject(index.h, _ptr(A), _ptr(B), _stream()), "lv_stream_reproject")
+
+
+def lv_index_export_xprime(index: Index):
+    """(x' fp32 [n, D], ids int32 [n]) in row order (CUDA tensors)."""
+    n = index.info()["n"]
+    Xp = torch.empty((n, index.D), dtype=torch.float32, device="cuda")
+    ids = torch.empty(n, dtype=torch.int32, device="cuda")
+    _check(lib().lv_index_export_xprime(index.h, _ptr(Xp), _ptr(ids), _stream()), "lv_index_export_xprime")
+    return Xp, ids
 
 
 def lv_encode_database(index: Index, X: torch.Tensor, assign: torch.Tensor | None = None):

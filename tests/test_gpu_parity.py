@@ -79,7 +79,11 @@ def _g1_ok(got, ref, absdot, dtype, D):
     import ml_dtypes
     t = ml_dtypes.bfloat16 if dtype == "bf16" else np.float16
     bb = ref.astype(t)
-    one = np.abs(np.nextafter(bb, np.array(np.inf, dtype=t)).astype(np.float64) - bb.astype(np.float64))
+    # one storage ulp in either direction: at a power of two the neighbour away from zero is twice
+    # as far as the one towards zero, and a flip may go either way
+    up = np.abs(np.nextafter(bb, np.array(np.inf, dtype=t)).astype(np.float64) - bb.astype(np.float64))
+    dn = np.abs(np.nextafter(bb, np.array(-np.inf, dtype=t)).astype(np.float64) - bb.astype(np.float64))
+    one = np.maximum(up, dn)
     ok = np.abs(got - ref) <= one + D * 2.0 ** -24 * absdot
     return ok.all(), float((got != ref).mean())
 
@@ -267,8 +271,8 @@ def check_g2_strict(lv, ix, Qt, cid, csc, C):
     X_low, perm, offs = lv.lv_index_export(ix)
     perm = perm.cpu().numpy()
     Qp = lv.lv_project_queries(ix, Qt).float().cpu().numpy().astype(np.float64)
-    xl = X_low.float().cpu().numpy().astype(np.float64)
-    d = xl.shape[1]
+    d = Qp.shape[1] // C                            # the search width (a prefix of the stored d)
+    xl = X_low.float().cpu().numpy().astype(np.float64)[:, :d]
     pos = np.full(perm.max() + 1, -1, dtype=np.int64)
     valid = perm >= 0
     pos[perm[valid]] = np.nonzero(valid)[0]
