@@ -20,6 +20,9 @@ Functions (pin in tests/test_oracle_pins.py named in brackets):
   flexible_fit         §3.1 A' = P'W^+, B' = P'W, D x D     [<A'q, B'x> = <q,x>, prefix = smaller fit]
   eig_fit_from_stats   §3.2 eig route from K_Q, K_X          [equals the SVD route]
   StreamingIndex       §3.2 insert/remove/observe/refresh    [K_X = definition, x' = B'_new x, Eq.(12)]
+  quantize_db_i8 / quantize_queries_i8 / search_i8
+                       P:129, P:211 scalar quantisation (R21) [rounding bound, |code| <= 127, extremes at
+                                                               +-127, exact-integer special case]
 """
 from __future__ import annotations
 
@@ -284,10 +287,11 @@ def reduced_scores(Qp, Xlow, assign=None) -> np.ndarray:
     return S
 
 
-def reduced_search(Qp, Xlow, assign, R: int, chunk: int = 1 << 18):
+def reduced_search(Qp, Xlow, assign, R: int, chunk: int = 1 << 18, score_fp32: bool = False):
     """Alg. 1 line 2 as an exhaustive scan: N_low(j) = the R best ids under
     (reduced score desc, id asc).  Chunked over database rows, merging running lists.
-    Returns ids [m, R] int64 and scores [m, R]."""
+    score_fp32: the scores are rounded to fp32 before ranking (the int8 path, whose scores the
+    precision contract defines as fp32 values, R21).  Returns ids [m, R] int64 and scores [m, R]."""
     Xlow = np.asarray(Xlow, dtype=np.float64)
     n = Xlow.shape[0]
     assign = np.zeros(n, dtype=np.int32) if assign is None else np.asarray(assign)
@@ -298,6 +302,8 @@ def reduced_search(Qp, Xlow, assign, R: int, chunk: int = 1 << 18):
     for lo in range(0, n, chunk):
         hi = min(n, lo + chunk)
         S = reduced_scores(Qp, Xlow[lo:hi], assign[lo:hi])
+        if score_fp32:
+            S = S.astype(np.float32).astype(np.float64)
         ids = np.arange(lo, hi, dtype=np.int64)
         for j in range(m):
             cid, csc = topk_total_order(S[j], ids, R)
@@ -438,4 +444,56 @@ class StreamingIndex:
     def current(self):
         ids = np.array(sorted(self.x), dtype=np.int64)
         return ids, np.stack([self.x[i] for i in ids]), np.stack([self.xp[i] for i in ids])
+
+
+# ----------------------------------------------------------------------------------
+# 8-bit reduced vectors (scalar quantisation of B x; reading R21)
+# ----------------------------------------------------------------------------------
+def quantize_db_i8(X_low, assign, C: int):
+    """Per cluster c and coordinate e: delta_{c,e} = max_{i: c_i = c} |x_{i,e}| / 127 and
+    code_{i,e} = RNE(x_{i,e} / delta_{c_i,e}) clipped to [-127, 127] (a zero column: delta = 1).
+    x is the fp32 value of the reduced vector (the fp64 product rounded once to fp32); every
+    operation is an fp32 operation with RNE (the quantiser's decisions are taken in fp32 on both
+    sides, R21).  Returns (codes int8 [n, d], delta fp32 [C, d])."""
+    x = np.asarray(X_low, dtype=np.float64).astype(np.float32)
+    a = np.zeros(x.shape[0], dtype=np.int64) if assign is None else np.asarray(assign, dtype=np.int64)
+    delta = np.ones((C, x.shape[1]), dtype=np.float32)
+    for c in range(C):
+        rows = x[a == c]
+        if rows.shape[0]:
+            amax = np.abs(rows).max(axis=0)
+            delta[c] = np.where(amax > 0, amax / np.float32(127.0), np.float32(1.0))
+    codes = np.clip(np.rint(x / delta[a]), -127, 127).astype(np.int8)
+    return codes, delta
+
+
+def quantize_queries_i8(Qp, delta):
+    """Query side of the int8 scan: per query j and view c, q~ = q'_{j,c} * delta_c (fp32 product),
+    s_{j,c} = max_e |q~_e| / 127 and codes = RNE(q~ / s_{j,c}) clipped to [-127, 127] (an all-zero
+    view: s = 1).  Then s_{j,c} * <codes_{j,c}, x codes_i> = sum_e (q'_e delta_e)(x_e / delta_e)
+    approximates <q'_{j,c}, x_i>.  Qp [m, C, d] (fp64, rounded to fp32 here).
+    Returns (codes int8 [m, C, d], s fp32 [m, C])."""
+    q = np.asarray(Qp, dtype=np.float64).astype(np.float32)
+    qt = q * np.asarray(delta, dtype=np.float32)[None]
+    amax = np.abs(qt).max(axis=2)
+    s = np.where(amax > 0, amax / np.float32(127.0), np.float32(1.0)).astype(np.float32)
+    codes = np.clip(np.rint(qt / s[:, :, None]), -127, 127).astype(np.int8)
+    return codes, s
+
+
+def search_i8(Q, X, A_stack, B_stack, assign, R: int, k: int, C: int | None = None):
+    """The hot path with 8-bit reduced vectors: the reduced score of (q_j, x_i) is the fp32 value
+    fl32(s_{j,c_i} * <q codes_{j,c_i}, x codes_i>) (an exact integer dot product scaled once),
+    exhaustive top-R on it (Alg. 1 l.2), fp64 re-rank on the canonical vectors and top-k (l.3)."""
+    A = np.asarray(A_stack, dtype=np.float64)
+    C = C or (1 if A.ndim == 2 else A.shape[0])
+    Qp = project(Q, A_stack)                                   # [m, C, d] fp64
+    X_low = encode(X, B_stack, assign)                         # fp64
+    xc, delta = quantize_db_i8(X_low, assign, C)
+    qc, s = quantize_queries_i8(Qp, delta)
+    Qeff = s[:, :, None].astype(np.float64) * qc.astype(np.float64)   # exact: s * code
+    cand, cand_sc = reduced_search(Qeff, xc.astype(np.float64), assign, R, score_fp32=True)
+    ids, sc = rerank_topk(Q, X, cand, k)
+    return {"ids": ids, "scores": sc, "cand": cand, "cand_scores": cand_sc, "q_codes": qc, "q_scales": s,
+            "x_codes": xc, "delta": delta, "Qeff": Qeff}
 

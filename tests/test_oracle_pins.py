@@ -251,6 +251,46 @@ def test_streaming_stats_reprojection_and_fresh_fit():
             assert np.abs(fresh["A"][:d].T @ fresh["B"][:d] - f1["A"][:d].T @ f1["B"][:d]).max() < 1e-8
 
 
+def test_i8_quantiser_bounds_and_exact_case():
+    """R21 (scalar quantisation of B x): every code within [-127, 127], each column's
+    extreme maps to +-127, |x - delta code| <= delta / 2 (round to nearest); the quantised score
+    s <q_code, x_code> differs from <q', x> by at most the closed-form rounding bound
+    sum_e (s/2 |x_code_e| + |q~_e| / 2); integer data with column maximum 127 and query maximum 127
+    quantise exactly (delta = s = 1), so the int8 search equals the plain search."""
+    rng = _rng(31)
+    n, d, C = 500, 16, 3
+    X = rng.standard_normal((n, d)) * np.linspace(3, 0.1, d)
+    a = rng.integers(0, C, n)
+    codes, delta = O.quantize_db_i8(X, a, C)
+    x32 = X.astype(np.float32).astype(np.float64)
+    assert codes.dtype == np.int8 and np.abs(codes.astype(int)).max() <= 127
+    for c in range(C):
+        assert (np.abs(codes[a == c].astype(int)).max(axis=0) == 127).all()
+    rec = codes.astype(np.float64) * delta[a].astype(np.float64)
+    assert (np.abs(x32 - rec) <= delta[a].astype(np.float64) / 2 * (1 + 1e-6)).all()
+    Qp = rng.standard_normal((7, C, d))
+    qc, s = O.quantize_queries_i8(Qp, delta)
+    q32 = Qp.astype(np.float32).astype(np.float64)
+    for j in range(7):
+        for i in range(0, n, 37):
+            c = a[i]
+            approx = float(s[j, c]) * float(qc[j, c].astype(np.int64) @ codes[i].astype(np.int64))
+            exact = float(q32[j, c] @ x32[i])
+            qt = np.abs(q32[j, c] * delta[c])
+            bound = float(np.sum(s[j, c] / 2 * np.abs(codes[i].astype(np.float64)) + qt / 2)) * (1 + 1e-5)
+            assert abs(approx - exact) <= bound
+    # exact special case: integer reduced vectors with column max 127 and integer queries with max 127
+    Xi = rng.integers(-127, 128, (200, 8)).astype(np.float64)
+    Xi[0] = 127
+    Bi = np.eye(8)
+    Qi = rng.integers(-127, 128, (5, 8)).astype(np.float64)
+    Qi[:, 0] = 127
+    r8 = O.search_i8(Qi, Xi, Bi, Bi, None, 30, 5)
+    rp = O.search(Qi, Xi, Bi, Bi, None, 30, 5)
+    assert np.array_equal(r8["delta"], np.ones((1, 8), np.float32)) and np.array_equal(r8["q_scales"], np.ones((5, 1)))
+    assert np.array_equal(r8["cand"], rp["cand"]) and np.array_equal(r8["ids"], rp["ids"])
+
+
 def test_scale_invariance_of_AtB():
     """Q -> cQ leaves A^T B unchanged."""
     Q, X = _ood_pair(_rng(8))
