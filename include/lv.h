@@ -50,7 +50,7 @@ typedef enum {
     LV_EUNSUPPORTED = 7   /* no sm_100 device, or a shape the kernels do not support      */
 } lv_status;
 
-typedef enum { LV_F32 = 0, LV_F16 = 1, LV_BF16 = 2 } lv_dtype;
+typedef enum { LV_F32 = 0, LV_F16 = 1, LV_BF16 = 2, LV_I8 = 3 } lv_dtype;
 
 typedef struct lv_index lv_index;   /* opaque, owned by the library */
 
@@ -122,7 +122,12 @@ lv_status lv_fit_stats(const float* Q_learn, int64_t m_learn,
  * lv_index_create — an empty index for dimension D, reduced dimension d and C clusters.
  *   A_stack, B_stack  device fp32 [C, d, D]: A_c (query side, f_c(q) = A_c q) and
  *                     B_c (database side, g_c(x) = B_c x); copied.
- *   low_dtype         LV_BF16 or LV_F16: storage of x_low and q' (P:129 reduced footprint)
+ *   low_dtype         LV_BF16 or LV_F16: storage of x_low and q' (P:129 reduced footprint), or
+ *                     LV_I8: 8-bit scalar quantisation of the reduced vectors (NEXT-4,
+ *                     DESIGN.md R21): x codes = RNE(x_low / delta_{c,e}), delta_{c,e} = max over the
+ *                     rows of cluster c of |x_low_e| / 127; query codes per (query, view) = RNE(q~ / s)
+ *                     with q~ = q' * delta_c, s = max |q~| / 127; scores fl(s * <q codes, x codes>)
+ *                     on the int8 tensor cores (kind::i8, exact int32 dot products)
  *   full_dtype        LV_F32 or LV_F16: storage of the full vectors used by the re-rank
  * Constraints: 32 <= d <= min(D, 192), d % 32 == 0, D % 4 == 0 (LV_F32) / D % 8 == 0 (LV_F16),
  *              1 <= C <= 1024.  Errors: LV_EINVAL, LV_ENOMEM, LV_EUNSUPPORTED.
@@ -158,6 +163,15 @@ lv_status lv_encode_database(lv_index* index, const void* X, lv_dtype x_dtype, i
  */
 lv_status lv_project_queries(const lv_index* index, const float* Q, int64_t m, void* Qp,
                              void* stream);
+
+/*
+ * lv_project_queries_i8 — the int8 index's query side: codes device int8 [m, C*d_search] and
+ * scales device fp32 [m, C] (see low_dtype LV_I8 of lv_index_create).
+ * lv_index_i8_scales — delta HOST fp32 [C, d] of an encoded int8 index.
+ */
+lv_status lv_project_queries_i8(const lv_index* index, const float* Q, int64_t m, int8_t* codes, float* scales,
+                                void* stream);
+lv_status lv_index_i8_scales(const lv_index* index, float* delta);
 
 /*
  * lv_search — the hot path, Alg. 1 with an exhaustive main step:

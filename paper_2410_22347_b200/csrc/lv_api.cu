@@ -13,9 +13,6 @@
 #include "lv_common.cuh"
 #include "lv_index.h"
 
-namespace lv {
-size_t score_smem_bytes(int d, int stages);
-}
 
 namespace lv {
 namespace host {
@@ -84,10 +81,41 @@ lv_status make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t co
   return LV_OK;
 }
 
+// 2D row-major [rows, cols] of bytes (int8 codes), row pitch ld bytes; box [box_rows, ch bytes];
+// swizzle = ch bytes (32, 64 or 128).
+lv_status make_tmap_u8(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int ch, int box_rows,
+                       int64_t ld) {
+  auto enc = get_encode();
+  if (!enc) return fail(LV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)(ld > 0 ? ld : cols)};
+  cuuint32_t box[2] = {(cuuint32_t)ch, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle sw =
+      ch == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : (ch == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LV_ECUDA, "cuTensorMapEncodeTiled (u8) failed (%d)", (int)r);
+  return LV_OK;
+}
+
 // The scan's view of X_low: its first ds columns (boxes of the width the scan kernel for ds uses).
 lv_status make_search_tmap(lv_index* ix) {
-  return make_tmap(&ix->tmap_xlow_s, ix->X_low, ix->n_pad, ix->ds, (ix->ds % 64 == 0) ? 64 : 32, ix->low == LV_BF16,
+  const int ch = lv::score_box_cols(ix->ds, ix->esz());
+  if (ix->low == LV_I8)
+    return make_tmap_u8(&ix->tmap_xlow_s, ix->X_low, ix->n_pad, ix->ds, ch, lv::score_tile_rows(ix->ds), ix->d);
+  return make_tmap(&ix->tmap_xlow_s, ix->X_low, ix->n_pad, ix->ds, ch, ix->low == LV_BF16,
                    lv::score_tile_rows(ix->ds), ix->d);
+}
+
+// Full-width map of X_low (debug / export consumers) plus the scan's view.
+lv_status make_xlow_tmap(lv_index* ix) {
+  const int ch = lv::score_box_cols(ix->d, ix->esz());
+  lv_status st = ix->low == LV_I8
+                     ? make_tmap_u8(&ix->tmap_xlow, ix->X_low, ix->n_pad, ix->d, ch, lv::score_tile_rows(ix->d), ix->d)
+                     : make_tmap(&ix->tmap_xlow, ix->X_low, ix->n_pad, ix->d, ch, ix->low == LV_BF16,
+                                 lv::score_tile_rows(ix->d));
+  return st ? st : make_search_tmap(ix);
 }
 
 double env_double(const char* name, double dflt) {
@@ -208,8 +236,8 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   // 32-row sample blocks while the block-maximum array stays small (<= 8192 blocks); coarser
   // 64-row blocks at the 10M-row sizes, where the array's HBM traffic would cost more than the
   // tighter threshold saves
-  const bool fine = (int64_t)lv::score_blocks_per_tile(ix->ds, true) * nsamp <= 8192;
-  const int bpt = lv::score_blocks_per_tile(ix->ds, fine);   // block maxima per sampled tile
+  const bool fine = (int64_t)lv::score_blocks_per_tile(ix->ds, true, ix->esz()) * nsamp <= 8192;
+  const int bpt = lv::score_blocks_per_tile(ix->ds, fine, ix->esz());   // block maxima per sampled tile
   pl->sampled = env_double("LV_SAMPLED", 1.0) != 0.0 && stride >= 2 && nsamp >= 64 && bpt * nsamp >= 8 * j1 &&
                 bpt * nsamp <= 65535;
   // candidate slots per query tile (each slot = 4 sub-lists, one per epilogue warp group; the
@@ -292,10 +320,10 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   pl->grid = (int)std::min<int64_t>(G, (int64_t)pmax * pl->QP);
   const size_t budget = 227 * 1024 - 1024 - 256;
   int st = std::max(2, std::min(8, (int)env_double("LV_STAGES", 8.0)));   // LV_STAGES: probe knob
-  while (st >= 2 && lv::score_smem_bytes(ix->ds, st) > budget) --st;
+  while (st >= 2 && lv::score_smem_bytes(ix->ds, st, ix->esz()) > budget) --st;
   if (st < 2) return fail(LV_EUNSUPPORTED, "d=%d leaves no room for a 2-stage pipeline", ix->ds);
   pl->stages = st;
-  pl->smem = lv::score_smem_bytes(ix->ds, st);
+  pl->smem = lv::score_smem_bytes(ix->ds, st, ix->esz());
   return LV_OK;
 }
 
@@ -507,7 +535,8 @@ lv_status lv_index_create(lv_index** out, int32_t D, int32_t d, int32_t C, lv_dt
   if (!out || !A_stack || !B_stack) return fail(LV_EINVAL, "lv_index_create: NULL argument");
   if (d < 1 || d > D || d % 32 != 0 || d > 192) return fail(LV_EINVAL, "lv_index_create: need 32 <= d <= min(D,192), d %% 32 == 0 (d=%d)", d);
   if (C < 1 || C > 1024) return fail(LV_EINVAL, "lv_index_create: need 1 <= C <= 1024");
-  if (low_dtype != LV_BF16 && low_dtype != LV_F16) return fail(LV_EINVAL, "lv_index_create: low_dtype must be BF16/F16");
+  if (low_dtype != LV_BF16 && low_dtype != LV_F16 && low_dtype != LV_I8)
+    return fail(LV_EINVAL, "lv_index_create: low_dtype must be BF16/F16/I8");
   if (full_dtype != LV_F32 && full_dtype != LV_F16) return fail(LV_EINVAL, "lv_index_create: full_dtype must be F32/F16");
   if ((full_dtype == LV_F32 && D % 4) || (full_dtype == LV_F16 && D % 8))
     return fail(LV_EINVAL, "lv_index_create: D=%d breaks 16-byte rows", D);
@@ -521,6 +550,8 @@ lv_status lv_index_create(lv_index** out, int32_t D, int32_t d, int32_t C, lv_dt
   ix->Kp = (D + 63) / 64 * 64;
   ix->a_rows = C * d;
   st = lv::host::set_operands(ix, A_stack, B_stack, 0);
+  if (!st && low_dtype == LV_I8 && cudaMalloc(&ix->i8_delta, sizeof(float) * (size_t)C * d) != cudaSuccess)
+    st = fail(LV_ENOMEM, "lv_index_create: cudaMalloc failed");
   if (st) {
     lv_index_destroy(ix);
     return st;
@@ -669,24 +700,39 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
     LV_CUDA(cudaMemcpyAsync(dorder, order.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, s));
     LV_CUDA(cudaStreamSynchronize(s));   // `order` is pageable and leaves scope
   }
-  // X_low = RNE(B_c x) (K6)
-  const size_t esz = 2;
+  // X_low = RNE(B_c x) (K6); int8: the fp32 products first, then per-(cluster, coordinate) scales and codes
+  const size_t esz = ix->esz();
   if (cudaMalloc(&ix->X_low, esz * ix->n_pad * ix->d) != cudaSuccess) return fail(LV_ENOMEM, "X_low");
+  float* xf = nullptr;
+  uint32_t* amax = nullptr;
+  if (ix->low == LV_I8 && (cudaMalloc(&xf, sizeof(float) * ix->n_pad * ix->d) != cudaSuccess ||
+                           cudaMalloc(&amax, sizeof(uint32_t) * (size_t)C * ix->d) != cudaSuccess)) {
+    cudaFree(xf);
+    return fail(LV_ENOMEM, "lv_encode_database: int8 staging");
+  }
   // full-precision copy for the re-rank (allocated before the timed kernels: a host-side
   // cudaMalloc between two event records would count as kernel time)
   const size_t fsz = ix->full == LV_F16 ? 2 : 4;
   if (cudaMalloc(&ix->X_full, fsz * n * ix->D) != cudaSuccess) return fail(LV_ENOMEM, "X_full");
   LV_CUDA(cudaEventRecord(ev[1], s));
-  LV_CUDA(lv::launch_encode_tc(&ix->tmap_b, X, x_dtype == LV_F16, ix->D, ix->Kp, ix->d, ix->C * ix->d, ix->perm, dwrow,
-                               dorder, nt, ix->X_low, ix->low == LV_BF16, env_double("LV_K6_PLANES", 3.0) >= 3.0, s));
+  if (ix->low == LV_I8) {
+    LV_CUDA(lv::launch_encode_tc(&ix->tmap_b, X, x_dtype == LV_F16, ix->D, ix->Kp, ix->d, ix->C * ix->d, ix->perm, dwrow,
+                                 dorder, nt, xf, 2, true, s));
+    LV_CUDA(lv::launch_i8_db_scales(xf, nt, ix->d, dwrow, C, amax, ix->i8_delta, s));
+    LV_CUDA(lv::launch_i8_db_codes(xf, nt, ix->d, dwrow, ix->i8_delta, reinterpret_cast<int8_t*>(ix->X_low), s));
+  } else {
+    LV_CUDA(lv::launch_encode_tc(&ix->tmap_b, X, x_dtype == LV_F16, ix->D, ix->Kp, ix->d, ix->C * ix->d, ix->perm, dwrow,
+                                 dorder, nt, ix->X_low, ix->low == LV_BF16 ? 0 : 1,
+                                 env_double("LV_K6_PLANES", 3.0) >= 3.0, s));
+  }
   LV_CUDA(cudaEventRecord(ev[2], s));
   LV_CUDA(lv::launch_convert(X, x_dtype == LV_F16, ix->X_full, ix->full == LV_F16, n * ix->D, s));
   LV_CUDA(cudaEventRecord(ev[3], s));
-  lv_status ts = make_tmap(&ix->tmap_xlow, ix->X_low, ix->n_pad, ix->d, (ix->d % 64 == 0) ? 64 : 32, ix->low == LV_BF16,
-                           lv::score_tile_rows(ix->d));
-  if (!ts) ts = make_search_tmap(ix);
+  lv_status ts = make_xlow_tmap(ix);
   LV_CUDA(cudaStreamSynchronize(s));
   cudaFree(dwrow);
+  cudaFree(xf);
+  cudaFree(amax);
   for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&ix->enc_ms[i], ev[i], ev[i + 1]);
   ix->enc_timed = true;
   return ts;
@@ -696,6 +742,7 @@ lv_status lv_project_queries(const lv_index* ix, const float* Q, int64_t m, void
   lv_status st = check_device();
   if (st) return st;
   if (!ix || !Q || !Qp || m <= 0) return fail(LV_EINVAL, "lv_project_queries: bad arguments");
+  if (ix->low == LV_I8) return fail(LV_EINVAL, "lv_project_queries: an int8 index needs lv_project_queries_i8");
   if (m > (1 << 24)) return fail(LV_EINVAL, "lv_project_queries: m too large");
   cudaStream_t s = (cudaStream_t)stream;
   const int Cd = ix->C * ix->ds;   // search width (C = 1 when ds < d: the first ds rows of A)
@@ -712,6 +759,39 @@ lv_status lv_project_queries(const lv_index* ix, const float* Q, int64_t m, void
   LV_CUDA(lv::launch_proj_tc(&tq, &ix->tmap_a, (int)m_pad, Cd, ix->a_rows, ix->Kp, Qp, Cd, (int)m,
                              ix->low == LV_BF16 ? 0 : 1, s));
   LV_CUDA(cudaFreeAsync(planes, s));
+  return LV_OK;
+}
+
+lv_status lv_project_queries_i8(const lv_index* ix, const float* Q, int64_t m, int8_t* codes, float* scales,
+                                void* stream) {
+  lv_status st = check_device();
+  if (st) return st;
+  if (!ix || !Q || !codes || !scales || m <= 0) return fail(LV_EINVAL, "lv_project_queries_i8: bad arguments");
+  if (ix->low != LV_I8) return fail(LV_EINVAL, "lv_project_queries_i8: not an int8 index");
+  if (m > (1 << 24)) return fail(LV_EINVAL, "lv_project_queries_i8: m too large");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int Cd = ix->C * ix->ds;
+  const int64_t m_pad = (m + 127) / 128 * 128;
+  void* planes = nullptr;
+  float* qf = nullptr;
+  LV_CUDA(cudaMallocAsync(&planes, (size_t)3 * m_pad * ix->Kp * 2, s));
+  LV_CUDA(cudaMallocAsync(&qf, sizeof(float) * (size_t)m_pad * Cd, s));
+  CUtensorMap tq;
+  st = make_tmap(&tq, planes, 3 * m_pad, ix->Kp, 64, true, 128);
+  cudaError_t e = st ? cudaSuccess : lv::launch_split3(Q, false, m, m_pad, ix->D, ix->Kp, planes, s);
+  if (!st && e == cudaSuccess)
+    e = lv::launch_proj_tc(&tq, &ix->tmap_a, (int)m_pad, Cd, ix->a_rows, ix->Kp, qf, Cd, (int)m, 2, s);
+  if (!st && e == cudaSuccess) e = lv::launch_i8_queries(qf, m, ix->C, ix->ds, ix->i8_delta, ix->d, codes, scales, s);
+  cudaFreeAsync(planes, s);
+  cudaFreeAsync(qf, s);
+  if (!st && e != cudaSuccess) st = fail(LV_ECUDA, "lv_project_queries_i8: %s", cudaGetErrorString(e));
+  return st;
+}
+
+lv_status lv_index_i8_scales(const lv_index* ix, float* delta) {
+  if (!ix || !delta) return fail(LV_EINVAL, "lv_index_i8_scales: bad arguments");
+  if (ix->low != LV_I8 || ix->n <= 0) return fail(LV_EINVAL, "lv_index_i8_scales: not an encoded int8 index");
+  LV_CUDA(cudaMemcpy(delta, ix->i8_delta, sizeof(float) * (size_t)ix->C * ix->d, cudaMemcpyDeviceToHost));
   return LV_OK;
 }
 
@@ -774,6 +854,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
     if (pl.sampled)
       need += (mp * Cd * 2 + 256) + (mp * 8 + 256) + ((size_t)pl.nblk * mp * 4 + 256) + (2 * mp * 4 + 256);
     if (ix->flex) need += mp * (size_t)ix->D * 4 + 256;
+    if (ix->low == LV_I8) need += (mp * (size_t)Cd * 4 + 256) + 2 * (mp * (size_t)ix->C * 4 + 256);
     if (need > ix->ws_bytes) {
       LV_CUDA(cudaStreamSynchronize(s));   // the old workspace may still be in use on s
       cudaFree(ix->ws);
@@ -804,6 +885,9 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
       pc.fail_list = carve<int32_t>(p, 2 * mp);
     }
     pc.Qx = ix->flex ? carve<float>(p, mp * (size_t)ix->D) : nullptr;
+    pc.Qf = ix->low == LV_I8 ? carve<float>(p, mp * (size_t)Cd) : nullptr;
+    pc.qscale = ix->low == LV_I8 ? carve<float>(p, mp * (size_t)ix->C) : nullptr;
+    pc.qscale_r = ix->low == LV_I8 ? carve<float>(p, mp * (size_t)ix->C) : nullptr;
     pc.chunk_info.assign(pl.chunks.size(), nullptr);
     for (size_t k = 0; k < pl.chunks.size(); ++k) pc.chunk_info[k] = carve<int32_t>(p, pl.chunks[k].size() + 1);
     pc.repair_info = carve<int32_t>(p, pl.repair_chunks.size() + 1);
@@ -848,9 +932,17 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
   LV_CUDA(cudaMemsetAsync(pc.zero_lo, 0, pc.zero_hi - pc.zero_lo, s));
   // K1 projection (rows >= m are zero)
   LV_CUDA(lv::launch_split3(Q, false, m, pl.m_pad, ix->D, ix->Kp, pc.Qplanes, s));
-  LV_CUDA(lv::launch_proj_tc(&pc.tmap_q, &ix->tmap_a, pl.m_pad, Cd, ix->a_rows, ix->Kp, Qp, Cd, pl.m_pad,
-                             ix->low == LV_BF16 ? 0 : 1, s));
-  launches += 2;
+  if (ix->low == LV_I8) {
+    // int8 (NEXT-4): q' in fp32, then per (query, view) codes and scales
+    LV_CUDA(lv::launch_proj_tc(&pc.tmap_q, &ix->tmap_a, pl.m_pad, Cd, ix->a_rows, ix->Kp, pc.Qf, Cd, pl.m_pad, 2, s));
+    LV_CUDA(lv::launch_i8_queries(pc.Qf, pl.m_pad, ix->C, ix->ds, ix->i8_delta, ix->d, reinterpret_cast<int8_t*>(Qp),
+                                  pc.qscale, s));
+    launches += 3;
+  } else {
+    LV_CUDA(lv::launch_proj_tc(&pc.tmap_q, &ix->tmap_a, pl.m_pad, Cd, ix->a_rows, ix->Kp, Qp, Cd, pl.m_pad,
+                               ix->low == LV_BF16 ? 0 : 1, s));
+    launches += 2;
+  }
   if (ix->flex) {
     // the re-rank's query side A'q (all D rows of A', fp32): <A'q, x'> = <q, x> (Eq.(12))
     LV_CUDA(lv::launch_proj_tc(&pc.tmap_q, &ix->tmap_a, pl.m_pad, ix->D, ix->a_rows, ix->Kp, pc.Qx, ix->D, pl.m_pad, 2, s));
@@ -870,6 +962,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
   sa.stages = pl.stages;
   sa.tile_valid = ix->tile_valid;
   sa.perm = (ix->C > 1 || ix->flex) ? ix->perm : nullptr;   // keys carry original / external ids
+  sa.qscale = pc.qscale;
   sa.cand = pc.cand;
   sa.cnt = pc.cnt;
   sa.tau = pc.tau;
@@ -899,7 +992,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
     sa.unit_ctr = (dyn_units && nscan < kMaxScans) ? pc.unit_ctr + nscan : nullptr;
     ++nscan;
     if (sa.stats) LV_CUDA(cudaMemsetAsync(sa.stats, 0, 8 * sizeof(unsigned long long), s));
-    LV_CUDA(lv::launch_score(&ix->tmap_xlow_s, sa, ix->low == LV_BF16, grid, pl.smem, s));
+    LV_CUDA(lv::launch_score(&ix->tmap_xlow_s, sa, ix->fmt(), grid, pl.smem, s));
     ++launches;
     if (sa.stats) {
       unsigned long long h[8];
@@ -989,9 +1082,10 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
       int32_t* flist = pc.fail_list + (size_t)round * pl.m_pad;
       int32_t* fcount = pc.fail + round;
       int32_t* mdev = pc.fail + 4 + round;
-      LV_CUDA(lv::launch_repair_setup(Qp, Cd, flist, fcount, pc.Qr, round == 0 ? pc.tau2 : nullptr, pc.tau, pc.cnt,
-                                      NS2, pl.m_pad, (int)m, mdev, s));
+      LV_CUDA(lv::launch_repair_setup(Qp, Cd * ix->esz() / 2, flist, fcount, pc.Qr, round == 0 ? pc.tau2 : nullptr,
+                                      pc.tau, pc.cnt, NS2, pl.m_pad, (int)m, mdev, pc.qscale, pc.qscale_r, ix->C, s));
       sa.Qp = pc.Qr;
+      sa.qscale = pc.qscale_r;
       sa.m_dev = mdev;
       st = scan(pc.repair_info, pl.repair_chunks, 1, round == 0 ? "repair-1" : "repair-2");
       if (st) return st;
@@ -1005,6 +1099,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
       launches += 3;
     }
     sa.Qp = Qp;
+    sa.qscale = pc.qscale;
     sa.m_dev = nullptr;
     if (sa.stats) {
       int32_t hf[2];
@@ -1286,7 +1381,8 @@ lv_status lv_index_export(const lv_index* ix, void* X_low, int32_t* perm, int64_
   if (!ix) return fail(LV_EINVAL, "lv_index_export: NULL index");
   if (ix->n <= 0) return fail(LV_EINVAL, "lv_index_export: index not encoded");
   cudaStream_t s = (cudaStream_t)stream;
-  if (X_low) LV_CUDA(cudaMemcpyAsync(X_low, ix->X_low, (size_t)ix->n_pad * ix->d * 2, cudaMemcpyDeviceToDevice, s));
+  if (X_low)
+    LV_CUDA(cudaMemcpyAsync(X_low, ix->X_low, (size_t)ix->n_pad * ix->d * ix->esz(), cudaMemcpyDeviceToDevice, s));
   if (perm) LV_CUDA(cudaMemcpyAsync(perm, ix->perm, (size_t)ix->n_pad * 4, cudaMemcpyDeviceToDevice, s));
   if (offsets) std::copy(ix->offsets.begin(), ix->offsets.end(), offsets);
   LV_CUDA(cudaStreamSynchronize(s));
@@ -1301,6 +1397,7 @@ void lv_index_destroy(lv_index* ix) {
   cudaFree(ix->KX);
   cudaFree(ix->A);
   cudaFree(ix->B);
+  cudaFree(ix->i8_delta);
   cudaFree(ix->dbg_stats);
   cudaFree(ix->A_planes);
   cudaFree(ix->B_planes);

@@ -325,4 +325,86 @@ cudaError_t launch_axpy_f64(double* K, const double* T, double alpha, int64_t co
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------- int8 reduced vectors
+// NEXT-4 (scalar quantisation of B x, P:129 / P:211), reading R21: per cluster c and
+// coordinate e, delta_{c,e} = max_{i in c} |x_{i,e}| / 127 (fp32), code = RNE(x / delta) in [-127, 127];
+// every division is an IEEE fp32 division and every rounding RNE, so the oracle can repeat them.
+// amax holds |x| as float bits (non-negative floats order like their bit patterns).
+__global__ void k_i8_colmax(const float* __restrict__ Xf, int d, const int32_t* __restrict__ tile_wrow,
+                            uint32_t* __restrict__ amax) {
+  const int64_t t = blockIdx.x;
+  const int c0 = tile_wrow[2 * t];   // c * d
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float m = 0.f;
+    for (int r = 0; r < 128; ++r) m = fmaxf(m, fabsf(Xf[(t * 128 + r) * d + j]));
+    atomicMax(amax + c0 + j, __float_as_uint(m));
+  }
+}
+
+__global__ void k_i8_delta(const uint32_t* __restrict__ amax, int n, float* __restrict__ delta) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float m = __uint_as_float(amax[i]);
+  delta[i] = m > 0.f ? __fdiv_rn(m, 127.0f) : 1.0f;
+}
+
+LV_DEVINL int8_t i8_code(float x, float delta) {
+  const int c = __float2int_rn(__fdiv_rn(x, delta));
+  return (int8_t)max(-127, min(127, c));
+}
+
+__global__ void k_i8_codes(const float* __restrict__ Xf, int64_t total, int d, const int32_t* __restrict__ tile_wrow,
+                           const float* __restrict__ delta, int8_t* __restrict__ codes) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / d;
+    const int j = (int)(e - r * d);
+    const int c0 = tile_wrow[2 * (r / 128)];
+    codes[e] = i8_code(Xf[e], delta[c0 + j]);
+  }
+}
+
+cudaError_t launch_i8_db_scales(const float* Xf, int64_t ntiles, int d, const int32_t* tile_wrow, int C,
+                                uint32_t* amax, float* delta, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(uint32_t) * (size_t)C * d, s);
+  if (e != cudaSuccess) return e;
+  k_i8_colmax<<<(unsigned)ntiles, 128, 0, s>>>(Xf, d, tile_wrow, amax);
+  k_i8_delta<<<(C * d + 255) / 256, 256, 0, s>>>(amax, C * d, delta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_i8_db_codes(const float* Xf, int64_t ntiles, int d, const int32_t* tile_wrow, const float* delta,
+                               int8_t* codes, cudaStream_t s) {
+  const int64_t total = ntiles * 128 * d;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_i8_codes<<<blocks, 256, 0, s>>>(Xf, total, d, tile_wrow, delta, codes);
+  return cudaGetLastError();
+}
+
+// one warp per (query row, cluster view): q~_e = q'_e delta_{c,e} (e < ds), s = max|q~| / 127,
+// codes = RNE(q~ / s); an all-zero view (padded rows) gets s = 1 and zero codes
+__global__ void __launch_bounds__(256) k_i8_queries(const float* __restrict__ Qf, int64_t rows, int C, int ds,
+                                                    const float* __restrict__ delta, int d, int8_t* __restrict__ codes,
+                                                    float* __restrict__ qscale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= rows * C) return;
+  const int64_t r = w / C;
+  const int c = (int)(w - r * C);
+  const float* q = Qf + (size_t)r * C * ds + (size_t)c * ds;
+  float m = 0.f;
+  for (int e = lane; e < ds; e += 32) m = fmaxf(m, fabsf(__fmul_rn(q[e], delta[c * d + e])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const float sc = m > 0.f ? __fdiv_rn(m, 127.0f) : 1.0f;
+  for (int e = lane; e < ds; e += 32) codes[(size_t)r * C * ds + (size_t)c * ds + e] = i8_code(__fmul_rn(q[e], delta[c * d + e]), sc);
+  if (lane == 0) qscale[r * C + c] = sc;
+}
+
+cudaError_t launch_i8_queries(const float* Qf, int64_t rows, int C, int ds, const float* delta, int d, int8_t* codes,
+                              float* qscale, cudaStream_t s) {
+  const int64_t blocks = (rows * C * 32 + 255) / 256;
+  k_i8_queries<<<(unsigned)blocks, 256, 0, s>>>(Qf, rows, C, ds, delta, d, codes, qscale);
+  return cudaGetLastError();
+}
+
 }  // namespace lv

@@ -43,6 +43,9 @@ struct PlanCache {
   int32_t* sel_ids = nullptr;  // [m_pad][R]
   int32_t* sel_n = nullptr;    // [m_pad]
   float* Qx = nullptr;         // flex: A'q fp32 [m_pad, D] (the re-rank's query side, Eq.(12))
+  float* Qf = nullptr;         // int8: q' fp32 [m_pad, C*ds] before quantisation
+  float* qscale = nullptr;     // int8: [m_pad][C] scale of each (query, view)
+  float* qscale_r = nullptr;   // int8: the repair pass's gathered scales
   uint8_t *zero_lo = nullptr, *zero_hi = nullptr;
   std::vector<int32_t*> chunk_info;
   int32_t* repair_info = nullptr;
@@ -62,6 +65,9 @@ struct lv_index {
   int64_t m_q = 0;
   std::vector<float> hA;       // flex: host copy of A' (row-major D x D)
   CUtensorMap tmap_b128;       // flex: B' planes, 128-row boxes (weight operand of the x' GEMM)
+  float* i8_delta = nullptr;   // low = LV_I8: per (cluster, coordinate) scale delta_{c,e} [C, d] (NEXT-4)
+  int fmt() const { return low == LV_I8 ? 2 : (low == LV_BF16 ? 1 : 0); }   // scan kernel format
+  int esz() const { return low == LV_I8 ? 1 : 2; }                          // bytes per reduced element
   int32_t ds = 0;              // search dimension <= d (§3.1 flexible d: the first ds reduced coordinates)
   lv_dtype low = LV_BF16, full = LV_F32;
   float* A = nullptr;          // [C*d, D]
@@ -103,6 +109,8 @@ lv_status check_device(int* nsm = nullptr);
 lv_status make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int ch, bool bf16, int box_rows,
                     int64_t ld = 0);
 lv_status make_search_tmap(lv_index* ix);
+lv_status make_tmap_u8(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int ch, int box_rows, int64_t ld);
+lv_status make_xlow_tmap(lv_index* ix);
 double env_double(const char* name, double dflt);
 lv_status set_operands(lv_index* ix, const float* A_src, const float* B_src, cudaStream_t s);
 lv_status gemm3(const lv_index* ix, const void* in, bool in_f16, int64_t rows, const CUtensorMap* tw, int w_rows,

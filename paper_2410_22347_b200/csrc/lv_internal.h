@@ -44,12 +44,16 @@ struct ScoreArgs {
                                //        bit5 = no TMA loads (stale tiles), bit6 = one MMA K step per tile
   unsigned long long* stats;   // debug counters [8] or nullptr: hit warp-tiles, appends, compactions, wait spins
   int32_t* unit_ctr;           // zeroed work-unit counter of this launch (dynamic unit order), or nullptr (static)
+  const float* qscale;         // int8 scan: [m_pad][C] scale of each (query, cluster view), else nullptr
 };
 
-cudaError_t launch_score(const CUtensorMap* tmap_xlow, const ScoreArgs& a, bool bf16, int grid, size_t smem,
+// fmt: 0 fp16, 1 bf16, 2 int8 (NEXT-4)
+cudaError_t launch_score(const CUtensorMap* tmap_xlow, const ScoreArgs& a, int fmt, int grid, size_t smem,
                          cudaStream_t s);
 int score_tile_rows(int d);
-int score_blocks_per_tile(int d, bool fine);   // sample stage: block maxima per tile and query (fine: 32-row blocks)
+int score_box_cols(int d, int esz);             // elements per row of one X_low TMA box (the swizzle width)
+int score_blocks_per_tile(int d, bool fine, int esz);   // sample stage: block maxima per tile and query (fine: 32-row blocks)
+size_t score_smem_bytes(int d, int stages, int esz);
 
 struct RerankArgs {
   int m, m_pad, D, R, k, NS, Cap;
@@ -73,9 +77,9 @@ struct RerankArgs {
 };
 cudaError_t launch_bmax_select(const float* bmax, int nblk, int m, int m_pad, int j1, int j2, uint64_t* tau,
                                int32_t* cnt, int NS, uint64_t* tau2, cudaStream_t s);
-cudaError_t launch_repair_setup(const void* Qp, int Cd, const int32_t* fail_list, const int32_t* fail_count, void* Qr,
-                                const uint64_t* tau_src, uint64_t* tau, int32_t* cnt, int NS, int m_pad, int m_max,
-                                int32_t* m_out, cudaStream_t s);
+cudaError_t launch_repair_setup(const void* Qp, int row_u16, const int32_t* fail_list, const int32_t* fail_count,
+                                void* Qr, const uint64_t* tau_src, uint64_t* tau, int32_t* cnt, int NS, int m_pad,
+                                int m_max, int32_t* m_out, const float* qs_src, float* qs_dst, int C, cudaStream_t s);
 cudaError_t launch_select_topr(const RerankArgs& a, cudaStream_t s);   // K4
 cudaError_t launch_rerank_topk(const RerankArgs& a, cudaStream_t s);   // K5
 cudaError_t launch_tau_merge(uint64_t* cand, int32_t* cnt, uint64_t* tau, int NS, int m, int m_pad, int Cap, int R,
@@ -92,9 +96,19 @@ cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a,
 // CTA i encodes tile order[i] (nullptr: tile i)
 // (three bf16 planes; two for bf16 storage when !planes3)
 size_t encode_smem(int d, int np);
+// out_type: 0 bf16, 1 fp16, 2 fp32 (the int8 path's unrounded x_low)
 cudaError_t launch_encode_tc(const CUtensorMap* tmap_b, const void* X, bool x_f16, int D, int Kp, int d, int Nc,
                              const int32_t* perm, const int32_t* tile_wrow, const int32_t* order, int64_t ntiles,
-                             void* out, bool out_bf16, bool planes3, cudaStream_t s);
+                             void* out, int out_type, bool planes3, cudaStream_t s);
+// int8 reduced vectors (NEXT-4): per (cluster, coordinate) scale delta = max |x| / 127 over the
+// cluster's rows, codes = RNE(x / delta) in [-127, 127]; queries per (query, view): q~ = q' * delta,
+// s = max |q~| / 127, codes = RNE(q~ / s)
+cudaError_t launch_i8_db_scales(const float* Xf, int64_t ntiles, int d, const int32_t* tile_wrow, int C,
+                                uint32_t* amax, float* delta, cudaStream_t s);
+cudaError_t launch_i8_db_codes(const float* Xf, int64_t ntiles, int d, const int32_t* tile_wrow, const float* delta,
+                               int8_t* codes, cudaStream_t s);
+cudaError_t launch_i8_queries(const float* Qf, int64_t rows, int C, int ds, const float* delta, int d, int8_t* codes,
+                              float* qscale, cudaStream_t s);
 cudaError_t launch_iota_perm(int32_t* perm, int64_t n, int64_t n_pad, cudaStream_t s);
 
 cudaError_t launch_stats(const void* in, int in_f16, int64_t ld, const int32_t* rowidx, int nchunks,

@@ -243,7 +243,7 @@ size_t encode_smem(int d, int np) { return enc_stages(d, np) * enc_stage_bytes(d
 // kNP = 3: v = h + m + l, six products (the default); kNP = 2: v = h + m (16 significant bits),
 // products hh, hm, mh, bf16 storage only, opt-in (LV_K6_PLANES=2): the dropped terms are
 // <= 2^-18 sum|b x| and flip 0.34 % of the bf16 outputs (three planes: 0.015 %; R18).
-template <bool kXF16, int kD, bool kOutBF16, int kNP>
+template <bool kXF16, int kD, int kOut, int kNP>
 __global__ void __launch_bounds__(kEnThreads, 1)
     k_encode_tc(const __grid_constant__ CUtensorMap tmap_b, const void* __restrict__ X, int D, int Kp, int Nc, int vec,
                 const int32_t* __restrict__ perm, const int32_t* __restrict__ tile_wrow,
@@ -458,10 +458,15 @@ __global__ void __launch_bounds__(kEnThreads, 1)
       tc::tmem_wait_ld();
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] += t[j];
+      if constexpr (kOut == 2) {
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + ((size_t)tile * 128 + row) * kD + cb * 32);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      } else {
       uint32_t w[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        if (kOutBF16) {
+        if (kOut == 0) {
           const __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
           w[j] = *reinterpret_cast<const uint32_t*>(&h2);
         } else {
@@ -472,6 +477,7 @@ __global__ void __launch_bounds__(kEnThreads, 1)
       uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(out) + ((size_t)tile * 128 + row) * kD + cb * 32);
 #pragma unroll
       for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+      }
     }
   }
   tc::tc_fence_before();
@@ -479,7 +485,7 @@ __global__ void __launch_bounds__(kEnThreads, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-template <bool F, int D, bool O, int NP>
+template <bool F, int D, int O, int NP>
 static cudaError_t launch_enc_t(const CUtensorMap* tb, const void* X, int Dx, int Kp, int Nc, const int32_t* perm,
                                 const int32_t* tile_wrow, const int32_t* order, int64_t ntiles, void* out, cudaStream_t s) {
   auto kern = k_encode_tc<F, D, O, NP>;
@@ -492,7 +498,7 @@ static cudaError_t launch_enc_t(const CUtensorMap* tb, const void* X, int Dx, in
   return cudaGetLastError();
 }
 
-template <bool F, bool O, int NP>
+template <bool F, int O, int NP>
 static cudaError_t launch_enc_d(int d, const CUtensorMap* tb, const void* X, int Dx, int Kp, int Nc, const int32_t* perm,
                                 const int32_t* tile_wrow, const int32_t* order, int64_t ntiles, void* out, cudaStream_t s) {
   switch (d) {
@@ -509,15 +515,18 @@ static cudaError_t launch_enc_d(int d, const CUtensorMap* tb, const void* X, int
 // three planes (six products); two planes (three products) for bf16 storage when !planes3
 cudaError_t launch_encode_tc(const CUtensorMap* tmap_b, const void* X, bool x_f16, int D, int Kp, int d, int Nc,
                              const int32_t* perm, const int32_t* tile_wrow, const int32_t* order, int64_t ntiles,
-                             void* out, bool out_bf16, bool planes3, cudaStream_t s) {
-  if (!out_bf16)
-    return x_f16 ? launch_enc_d<true, false, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
-                 : launch_enc_d<false, false, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+                             void* out, int out_type, bool planes3, cudaStream_t s) {
+  if (out_type == 2)
+    return x_f16 ? launch_enc_d<true, 2, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
+                 : launch_enc_d<false, 2, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+  if (out_type == 1)
+    return x_f16 ? launch_enc_d<true, 1, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
+                 : launch_enc_d<false, 1, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
   if (planes3)
-    return x_f16 ? launch_enc_d<true, true, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
-                 : launch_enc_d<false, true, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
-  return x_f16 ? launch_enc_d<true, true, 2>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
-               : launch_enc_d<false, true, 2>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    return x_f16 ? launch_enc_d<true, 0, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
+                 : launch_enc_d<false, 0, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+  return x_f16 ? launch_enc_d<true, 0, 2>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
+               : launch_enc_d<false, 0, 2>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
 }
 
 }  // namespace lv

@@ -527,13 +527,14 @@ cudaError_t launch_bmax_select(const float* bmax, int nblk, int m, int m_pad, in
   return cudaGetLastError();
 }
 
-// Repair set-up: rows r < F (F = *fail_count) of Qr <- rows fail_list[r] of Qp (Cd 16-bit
-// elements each), rows in [F, ceil(F/128)*128) zeroed; every candidate list of row r restarts
-// empty at threshold tau_src[fail_list[r]] (or 0 = none); *m_out = F.
-__global__ void k_repair_setup(const uint16_t* __restrict__ Qp, int Cd, const int32_t* __restrict__ fail_list,
+// Repair set-up: rows r < F (F = *fail_count) of Qr <- rows fail_list[r] of Qp (row_u16 16-bit
+// words each; int8 rows are copied as pairs of codes) and, for the int8 scan, their C view scales;
+// rows in [F, ceil(F/128)*128) zeroed; every candidate list of row r restarts empty at threshold
+// tau_src[fail_list[r]] (or 0 = none); *m_out = F.
+__global__ void k_repair_setup(const uint16_t* __restrict__ Qp, int row_u16, const int32_t* __restrict__ fail_list,
                                const int32_t* __restrict__ fail_count, uint16_t* __restrict__ Qr,
                                const uint64_t* __restrict__ tau_src, uint64_t* tau, int32_t* cnt, int NS, int m_pad,
-                               int32_t* m_out) {
+                               int32_t* m_out, const float* __restrict__ qs_src, float* __restrict__ qs_dst, int C) {
   const int F = *fail_count;
   const int Fp = (F + 127) / 128 * 128;
   const int r = blockIdx.x;
@@ -541,7 +542,10 @@ __global__ void k_repair_setup(const uint16_t* __restrict__ Qp, int Cd, const in
   if (r == 0 && threadIdx.x == 0) *m_out = F;
   const bool v = r < F;
   const int q = v ? fail_list[r] : 0;
-  for (int e = threadIdx.x; e < Cd; e += blockDim.x) Qr[(size_t)r * Cd + e] = v ? Qp[(size_t)q * Cd + e] : (uint16_t)0;
+  for (int e = threadIdx.x; e < row_u16; e += blockDim.x)
+    Qr[(size_t)r * row_u16 + e] = v ? Qp[(size_t)q * row_u16 + e] : (uint16_t)0;
+  if (qs_src)
+    for (int c = threadIdx.x; c < C; c += blockDim.x) qs_dst[(size_t)r * C + c] = v ? qs_src[(size_t)q * C + c] : 1.f;
   const uint64_t t = (v && tau_src) ? tau_src[q] : 0ull;
   for (int sl = threadIdx.x; sl < NS; sl += blockDim.x) {
     tau[(size_t)sl * m_pad + r] = t;
@@ -549,12 +553,12 @@ __global__ void k_repair_setup(const uint16_t* __restrict__ Qp, int Cd, const in
   }
 }
 
-cudaError_t launch_repair_setup(const void* Qp, int Cd, const int32_t* fail_list, const int32_t* fail_count, void* Qr,
-                                const uint64_t* tau_src, uint64_t* tau, int32_t* cnt, int NS, int m_pad, int m_max,
-                                int32_t* m_out, cudaStream_t s) {
+cudaError_t launch_repair_setup(const void* Qp, int row_u16, const int32_t* fail_list, const int32_t* fail_count,
+                                void* Qr, const uint64_t* tau_src, uint64_t* tau, int32_t* cnt, int NS, int m_pad,
+                                int m_max, int32_t* m_out, const float* qs_src, float* qs_dst, int C, cudaStream_t s) {
   const int rows = (m_max + 127) / 128 * 128;
-  k_repair_setup<<<rows, 128, 0, s>>>((const uint16_t*)Qp, Cd, fail_list, fail_count, (uint16_t*)Qr, tau_src, tau,
-                                      cnt, NS, m_pad, m_out);
+  k_repair_setup<<<rows, 128, 0, s>>>((const uint16_t*)Qp, row_u16, fail_list, fail_count, (uint16_t*)Qr, tau_src, tau,
+                                      cnt, NS, m_pad, m_out, qs_src, qs_dst, C);
   return cudaGetLastError();
 }
 

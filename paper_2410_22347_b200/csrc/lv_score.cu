@@ -56,22 +56,30 @@ __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x
 // (d > 128): then A is single-buffered and rewritten after each unit (one short bubble per
 // unit, units are long at those sizes).
 constexpr int kTileN = 128;
-__host__ __device__ constexpr bool score_single_a(int d) { return (512 - d) / kTileN < 3; }
-__host__ __device__ constexpr int score_a_cols(int d) { return score_single_a(d) ? d / 2 : d; }
-__host__ __device__ constexpr int score_nacc(int d) {
-  return (512 - score_a_cols(d)) / kTileN > kMaxAcc ? kMaxAcc : (512 - score_a_cols(d)) / kTileN;
+// esz = bytes per reduced element (2: bf16/fp16, 1: int8); an A buffer takes d * esz / 4 columns
+__host__ __device__ constexpr bool score_single_a(int d, int esz = 2) { return (512 - d * esz / 2) / kTileN < 3; }
+__host__ __device__ constexpr int score_a_cols(int d, int esz = 2) {
+  return score_single_a(d, esz) ? d * esz / 4 : d * esz / 2;
+}
+__host__ __device__ constexpr int score_nacc(int d, int esz = 2) {
+  return (512 - score_a_cols(d, esz)) / kTileN > kMaxAcc ? kMaxAcc : (512 - score_a_cols(d, esz)) / kTileN;
 }
 __host__ __device__ constexpr int score_tile_n(int d) { return kTileN + 0 * d; }
+// bytes per row of one swizzled TMA box of X_low (the swizzle width): bf16/fp16 128 B when d % 64
+// == 0 else 64 B; int8 128 / 64 / 32 B by d's divisibility
+__host__ __device__ constexpr int score_box_bytes(int d, int esz) {
+  return esz == 2 ? ((d % 64 == 0) ? 128 : 64) : ((d % 128 == 0) ? 128 : ((d % 64 == 0) ? 64 : 32));
+}
 // Epilogue jobs: (128-column tile, column block) per TMEM lane quarter, taken in order by the
 // quarter's 4 warps.  A waiting warp checks the accumulator barrier by phase parity, which is
 // only unambiguous while the quarter's in-flight jobs (<= 4) span at most nacc tiles; hence
 // 64-column jobs (2 per tile, span <= 3 tiles) need nacc >= 3, else 32-column jobs (span <= 2).
-__host__ __device__ constexpr int job_cols(int d) { return score_nacc(d) >= 3 ? 64 : 32; }
+__host__ __device__ constexpr int job_cols(int d, int esz = 2) { return score_nacc(d, esz) >= 3 ? 64 : 32; }
 
-__host__ __device__ inline ScoreSmemLayout score_smem_layout(int d, int stages) {
+__host__ __device__ inline ScoreSmemLayout score_smem_layout(int d, int stages, int esz = 2) {
   ScoreSmemLayout L;
   L.b_off = 0;
-  L.epi_off = align_up((uint32_t)stages * (uint32_t)kTileN * (uint32_t)d * 2u, 1024);
+  L.epi_off = align_up((uint32_t)stages * (uint32_t)kTileN * (uint32_t)d * (uint32_t)esz, 1024);
   L.bar_off = align_up(L.epi_off + (uint32_t)sizeof(EpiShared), 16);
   // barriers: b_full[stages], b_empty[stages], acc_full[kMaxAcc], acc_empty[kMaxAcc], a_full[2], tmem ptr
   // + the unit queue: uq_full[kUQ], uq_empty[kUQ] and kUQ unit ids
@@ -129,6 +137,21 @@ __device__ __noinline__ uint64_t warp_compact(uint64_t* buf, int count, int R, i
 // Float threshold matching a key threshold: keys > thr  <=>  (for the max test) score >= ts.
 LV_DEVINL float thr_score(uint64_t thr) {
   return thr == 0ull ? -FLT_MAX : unord_f32((uint32_t)((thr + 1ull) >> 32));
+}
+
+// int8 scan (NEXT-4): a score is fl(s * float(acc)) with s > 0 the (query, view) scale and acc
+// the exact int32 dot product of the codes (|acc| <= 192 * 127 * 127 < 2^24, so float(acc) is
+// exact).  fl(s * x) is non-decreasing in x, so score >= ts  <=>  acc >= the smallest integer v
+// with fl(s * v) >= ts: the epilogue filters on integers and converts only hitting blocks.
+LV_DEVINL int i8_threshold(float ts, float s) {
+  if (!(ts > -FLT_MAX)) return INT_MIN + 1;   // no threshold: every unmasked score
+  const float t = ts / s;
+  if (t > 1.0e7f) return INT_MAX;             // above every reachable score (padded queries)
+  if (t < -1.0e7f) return INT_MIN + 1;
+  int v = (int)ceilf(t);
+  while (s * (float)(v - 1) >= ts) --v;
+  while (s * (float)v < ts) ++v;
+  return v;
 }
 
 // Approximate (16-bit prefix) radix compaction of lane L's buffer by the whole warp: finds the
@@ -218,24 +241,29 @@ __device__ __forceinline__ int warp_compact_fast(uint64_t* buf, int count, int R
 
 // kSample: the sample stage (block maxima only, no candidate lists; a.bmax != nullptr) is a
 // separate instantiation so the main stage's per-tile loop carries no mode checks.
-template <bool kBF16, int kD, bool kSample>
+// kFmt: 0 fp16, 1 bf16 (kind::f16, fp32 accumulators), 2 int8 (kind::i8, s32 accumulators,
+// scores fl(s * acc), NEXT-4).
+template <int kFmt, int kD, bool kSample>
 __global__ void __launch_bounds__(kThreads, 1)
     k_score_topr(const __grid_constant__ CUtensorMap tmap_xlow, const ScoreArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base (SWIZZLE_128B atoms) as an offset into the shared array, so that every
   // access through it stays in the shared address space (LDS/STS, not generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr bool kI8 = kFmt == 2;
+  constexpr int kEsz = kI8 ? 1 : 2;               // bytes per reduced element
   constexpr int d = kD;
-  constexpr int kCH = (kD % 64 == 0) ? 64 : 32;   // columns per swizzled TMA box (128 B or 64 B rows)
+  constexpr int kCHB = score_box_bytes(kD, kEsz); // bytes per swizzled TMA box row (the swizzle)
+  constexpr int kCH = kCHB / kEsz;                // elements per box row
   constexpr int kN = kTileN;
   constexpr int nch = d / kCH;
-  constexpr uint32_t box_bytes = (uint32_t)kN * kCH * 2u;
-  constexpr int nacc = score_nacc(kD);
-  constexpr int kJobCols = job_cols(kD);          // score columns per epilogue job
+  constexpr uint32_t box_bytes = (uint32_t)kN * kCHB;
+  constexpr int nacc = score_nacc(kD, kEsz);
+  constexpr int kJobCols = job_cols(kD, kEsz);    // score columns per epilogue job
   constexpr int kJV = kJobCols / 32;              // 32-column tcgen05.ld per job
   constexpr int kJobsPerTile = 128 / kJobCols;    // jobs per lane quarter and tile
   static_assert((3 + kJobsPerTile - 1) / kJobsPerTile + 1 <= nacc, "4 in-flight jobs must span <= nacc tiles");
-  const ScoreSmemLayout L = score_smem_layout(d, a.stages);
+  const ScoreSmemLayout L = score_smem_layout(d, a.stages, kEsz);
   uint8_t* sB = smem + L.b_off;
   EpiShared& S = *reinterpret_cast<EpiShared*>(smem + L.epi_off);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
@@ -283,8 +311,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr;
-  constexpr bool kSingleA = score_single_a(kD);
-  const uint32_t acc_col0 = (uint32_t)score_a_cols(kD);   // A buffer(s) occupy columns [0, acc_col0)
+  constexpr bool kSingleA = score_single_a(kD, kEsz);
+  constexpr uint32_t kACols = (uint32_t)(kD * kEsz / 4);   // TMEM columns of one A buffer
+  const uint32_t acc_col0 = (uint32_t)score_a_cols(kD, kEsz);   // A buffer(s) occupy columns [0, acc_col0)
   const uint32_t acc_full_u = tc::smem_u32(acc_full), acc_empty_u = tc::smem_u32(acc_empty);
   // Work units of this CTA in order: static (blockIdx.x + i * gridDim.x) or, with a.unit_ctr,
   // dynamic: the TMA thread takes units from the launch's global counter as it needs them (CTAs
@@ -351,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer (A from TMEM)
-    constexpr uint32_t idesc = tc::make_idesc_f16(128, kN, kBF16);
+    constexpr uint32_t idesc = kI8 ? tc::make_idesc_i8(128, kN) : tc::make_idesc_f16(128, kN, kFmt == 1);
     const uint32_t sB_addr = tc::smem_u32(sB);
     int stage = 0;
     uint32_t phase = 0;
@@ -369,21 +398,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (kSingleA) tc::mbar_wait_sleep(a_full, (uint32_t)i & 1u);
       else tc::mbar_wait_sleep(a_full + (i & 1), (uint32_t)(i >> 1) & 1u);
       tc::tc_fence_after();
-      const uint32_t at = tmem_base + (kSingleA ? 0u : (uint32_t)(i & 1) * (uint32_t)(d / 2));
+      const uint32_t at = tmem_base + (kSingleA ? 0u : (uint32_t)(i & 1) * kACols);
       for (int t = t0; t < t1; t += ts_) {
         tc::mbar_wait_sleep(acc_empty + acc, acc_phase ^ 1);
         tc::mbar_wait_sleep(b_full + stage, phase);
         tc::tc_fence_after();
         if (issuer) {
-          const uint64_t bd0 = tc::make_sdesc(sB_addr + (uint32_t)stage * nch * box_bytes, kCH * 2);
+          const uint64_t bd0 = tc::make_sdesc(sB_addr + (uint32_t)stage * nch * box_bytes, kCHB);
           const uint32_t dt = tmem_base + acc_col0 + (uint32_t)acc * kN;
-          const int nk = (a.flags & 64) ? 1 : d / 16;   // probe: one K step per tile (no tensor-pipe bound)
+          constexpr int kSteps = d * kEsz / 32;          // one MMA per 32 bytes of K (K16 f16, K32 i8)
+          const int nk = (a.flags & 64) ? 1 : kSteps;   // probe: one K step per tile (no tensor-pipe bound)
 #pragma unroll
-          for (int kk = 0; kk < d / 16; ++kk) {
+          for (int kk = 0; kk < kSteps; ++kk) {
             if (kk >= nk) break;
-            // K step kk: box kk*16/kCH, byte offset (kk*16 % kCH)*2 inside the swizzled row
-            const uint32_t off16 = (((uint32_t)((kk * 16) / kCH) * box_bytes) + (uint32_t)((kk * 16) % kCH) * 2u) >> 4;
-            tc::mma_f16_ts(dt, at + (uint32_t)kk * 8u, bd0 + off16, idesc, kk > 0 ? 1u : 0u);
+            // K step kk: box (32 kk) / kCHB, byte offset (32 kk) % kCHB inside the swizzled row;
+            // A: 32 bytes of K = 8 TMEM columns
+            const uint32_t off16 = (((uint32_t)((kk * 32) / kCHB) * box_bytes) + (uint32_t)((kk * 32) % kCHB)) >> 4;
+            if (kI8)
+              tc::mma_i8_ts(dt, at + (uint32_t)kk * 8u, bd0 + off16, idesc, kk > 0 ? 1u : 0u);
+            else
+              tc::mma_f16_ts(dt, at + (uint32_t)kk * 8u, bd0 + off16, idesc, kk > 0 ? 1u : 0u);
           }
           tc::mma_commit(b_empty + stage);
           tc::mma_commit(acc_full + acc);
@@ -408,40 +442,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     float (*srows)[32] = S.rows[warp];
     int* hist = S.hist[warp];
     // A operand of unit u (its cluster's view of the tile's 128 queries) -> TMEM buffer b; this
-    // warp writes K range [cq*d/4, (cq+1)*d/4) of its 32 rows (d/8 TMEM columns)
+    // warp writes K range [cq*d/4, (cq+1)*d/4) of its 32 rows (d*esz/16 TMEM columns), loaded as
+    // 8-byte words (the slice start is 8-byte aligned for every d and element size)
     auto write_A = [&](int u, int b) {
       const int c = u / QT, qt = u % QT;
       const int cl = a.chunk_info[kChunkInts * c + 2];
       const int qq = qt * 128 + row;
-      const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.Qp) +
-                                                       (size_t)qq * ldq + (size_t)cl * d + cq * (d / 4));
-      const uint32_t dst = tmem_base + lane_base + (uint32_t)b * (uint32_t)(d / 2) + (uint32_t)cq * (uint32_t)(d / 8);
-      constexpr int ncols = d / 8;   // 4..24, a multiple of 4
+      constexpr int ncols = d * kEsz / 16;   // 2..24, even
+      const uint2* src = reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(a.Qp) +
+                                                       ((size_t)qq * ldq + (size_t)cl * d + cq * (d / 4)) * kEsz);
+      const uint32_t dst = tmem_base + lane_base + (uint32_t)b * kACols + (uint32_t)cq * (uint32_t)ncols;
+      uint32_t r[ncols];
+#pragma unroll
+      for (int j = 0; j < ncols / 2; ++j) {
+        const uint2 w = __ldg(src + j);
+        r[2 * j] = w.x;
+        r[2 * j + 1] = w.y;
+      }
       int col = 0;
 #pragma unroll
       for (; col + 16 <= ncols; col += 16) {
-        uint32_t r[16];
+        uint32_t t[16];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint4 w = __ldg(src + col / 4 + j);
-          r[4 * j] = w.x; r[4 * j + 1] = w.y; r[4 * j + 2] = w.z; r[4 * j + 3] = w.w;
-        }
-        tc::tmem_st_32x32b_x16(dst + (uint32_t)col, r);
+        for (int j = 0; j < 16; ++j) t[j] = r[col + j];
+        tc::tmem_st_32x32b_x16(dst + (uint32_t)col, t);
       }
       if (col + 8 <= ncols) {
-        uint32_t r[8];
+        uint32_t t[8];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const uint4 w = __ldg(src + col / 4 + j);
-          r[4 * j] = w.x; r[4 * j + 1] = w.y; r[4 * j + 2] = w.z; r[4 * j + 3] = w.w;
-        }
-        tc::tmem_st_32x32b_x8(dst + (uint32_t)col, r);
+        for (int j = 0; j < 8; ++j) t[j] = r[col + j];
+        tc::tmem_st_32x32b_x8(dst + (uint32_t)col, t);
         col += 8;
       }
       if (col + 4 <= ncols) {
-        const uint4 w = __ldg(src + col / 4);
-        const uint32_t r[4] = {w.x, w.y, w.z, w.w};
-        tc::tmem_st_32x32b_x4(dst + (uint32_t)col, r);
+        const uint32_t t[4] = {r[col], r[col + 1], r[col + 2], r[col + 3]};
+        tc::tmem_st_32x32b_x4(dst + (uint32_t)col, t);
+        col += 4;
+      }
+      if (col + 2 <= ncols) {
+        const uint32_t t[2] = {r[col], r[col + 1]};
+        tc::tmem_st_32x32b_x2(dst + (uint32_t)col, t);
       }
       tc::tmem_wait_st();
       tc::tc_fence_before();
@@ -494,6 +534,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int cnt = lists ? a.cnt[si] : 0;
       uint64_t tk = lists ? a.tau[si] : 0ull;
       float ts = qvalid ? thr_score(tk) : FLT_MAX;   // padded queries never hit
+      // int8: this query's scale for the unit's cluster view, and the threshold on accumulators
+      const float qs = kI8 ? a.qscale[(size_t)q * a.C + ci[2]] : 1.f;
+      int ti = kI8 ? i8_threshold(ts, qs) : 0;
       uint64_t* const bp = a.cand + si * (size_t)a.Cap;
       const int n_t = (t1 - t0 + tstride - 1) / tstride;   // tiles of this unit
       const int jend = (tiles_before + n_t) * kJobsPerTile;   // job index bound of this unit
@@ -540,20 +583,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (tv < 32) {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
-                if (j >= tv) v[j] = -FLT_MAX;
+                if (j >= tv) v[j] = kI8 ? __int_as_float(INT_MIN) : -FLT_MAX;
             }
           }
+          // int8: v holds s32 accumulators; the score of column j is fl(qs * float(acc_j))
+          auto score_of = [&](float raw) -> float {
+            if (!kI8) return raw;
+            const int iv = __float_as_int(raw);
+            return iv == INT_MIN ? -FLT_MAX : qs * (float)iv;
+          };
           if (a.raw != nullptr) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + hpos + j] = v[j];
+            for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + hpos + j] = score_of(v[j]);
           }
-          float mx = v[0];
+          float mx;
+          bool hit;
+          if (kI8) {
+            int im = __float_as_int(v[0]);
 #pragma unroll
-          for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
+            for (int j = 1; j < 32; ++j) im = max(im, __float_as_int(v[j]));
+            mx = im == INT_MIN ? -FLT_MAX : qs * (float)im;
+            hit = im >= ti && im > INT_MIN;
+          } else {
+            mx = v[0];
+#pragma unroll
+            for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
+            hit = mx >= ts && mx > -FLT_MAX;
+          }
           if (kSample) {
             // sample stage: record block maxima (query q; blocks of 32 database rows when
             // a.flags & 8, else of the job's 64: fine blocks keep the threshold estimate of
-            // DESIGN.md §5 tight when top rows cluster); no top-R here
+            // DESIGN.md §6 tight when top rows cluster); no top-R here
             const int sblk = (sbase + (t - t0) / tstride) * kJobsPerTile + jh;
             if (fine_blocks) {
               a.bmax[(size_t)(sblk * kJV + h) * a.m_pad + q] = mx;
@@ -563,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             continue;
           }
-          const bool hit = mx >= ts && mx > -FLT_MAX;
+
           uint32_t hb = __ballot_sync(0xffffffffu, hit);
           if (hb == 0u) continue;
           if (count_stats && lane == 0) atomicAdd(a.stats + 0, 1ull);
@@ -575,7 +635,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (hit) {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-              reinterpret_cast<float4*>(srows[lane])[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              reinterpret_cast<float4*>(srows[lane])[j] =
+                  make_float4(score_of(v[4 * j]), score_of(v[4 * j + 1]), score_of(v[4 * j + 2]), score_of(v[4 * j + 3]));
           }
           __syncwarp();
           do {
@@ -598,6 +659,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (lane == Lz) {
                 tk = nthr;
                 ts = thr_score(nthr);
+                if (kI8) ti = i8_threshold(ts, qs);
               }
               if (count_stats && lane == 0) atomicAdd(a.stats + 2, 1ull);
               keep = keep && key > tkz;
@@ -635,9 +697,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kMmaWarp) tc::tmem_dealloc(tmem_base, 512);
 }
 
-size_t score_smem_bytes(int d, int stages) { return score_smem_layout(d, stages).total + 1024; }
+size_t score_smem_bytes(int d, int stages, int esz) { return score_smem_layout(d, stages, esz).total + 1024; }
 
-template <bool B, int D, bool S>
+template <int B, int D, bool S>
 static cudaError_t launch_t(const CUtensorMap* tx, const ScoreArgs& a, int grid, size_t smem, cudaStream_t s) {
   auto kern = k_score_topr<B, D, S>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -646,7 +708,7 @@ static cudaError_t launch_t(const CUtensorMap* tx, const ScoreArgs& a, int grid,
   return cudaGetLastError();
 }
 
-template <bool B, bool S>
+template <int B, bool S>
 static cudaError_t launch_d(const CUtensorMap* tx, const ScoreArgs& a, int grid, size_t smem, cudaStream_t s) {
   switch (a.d) {
     case 32: return launch_t<B, 32, S>(tx, a, grid, smem, s);
@@ -659,16 +721,21 @@ static cudaError_t launch_d(const CUtensorMap* tx, const ScoreArgs& a, int grid,
   }
 }
 
-cudaError_t launch_score(const CUtensorMap* tmap_xlow, const ScoreArgs& a, bool bf16, int grid, size_t smem,
+cudaError_t launch_score(const CUtensorMap* tmap_xlow, const ScoreArgs& a, int fmt, int grid, size_t smem,
                          cudaStream_t s) {
   const bool sample = a.bmax != nullptr;
-  if (sample) return bf16 ? launch_d<true, true>(tmap_xlow, a, grid, smem, s) : launch_d<false, true>(tmap_xlow, a, grid, smem, s);
-  return bf16 ? launch_d<true, false>(tmap_xlow, a, grid, smem, s) : launch_d<false, false>(tmap_xlow, a, grid, smem, s);
+  if (sample) {
+    if (fmt == 2) return launch_d<2, true>(tmap_xlow, a, grid, smem, s);
+    return fmt == 1 ? launch_d<1, true>(tmap_xlow, a, grid, smem, s) : launch_d<0, true>(tmap_xlow, a, grid, smem, s);
+  }
+  if (fmt == 2) return launch_d<2, false>(tmap_xlow, a, grid, smem, s);
+  return fmt == 1 ? launch_d<1, false>(tmap_xlow, a, grid, smem, s) : launch_d<0, false>(tmap_xlow, a, grid, smem, s);
 }
 
 int score_tile_rows(int d) { return score_tile_n(d); }
-int score_blocks_per_tile(int d, bool fine) {   // block maxima per sampled tile
-  return fine ? kTileN / 32 : kTileN / job_cols(d);
+int score_box_cols(int d, int esz) { return score_box_bytes(d, esz) / esz; }
+int score_blocks_per_tile(int d, bool fine, int esz) {   // block maxima per sampled tile
+  return fine ? kTileN / 32 : kTileN / job_cols(d, esz);
 }
 
 }  // namespace lv

@@ -78,9 +78,7 @@ lv_status flex_layout(lv_index* ix, cudaStream_t s) {
   LV_CUDA(cudaMemcpyAsync(ix->inv, ix->h_inv.data(), sizeof(int32_t) * ix->id_cap, cudaMemcpyHostToDevice, s));
   LV_CUDA(cudaStreamSynchronize(s));   // the host vectors are copy sources
   ix->offsets.assign({0, ix->n_pad});
-  lv_status st = make_tmap(&ix->tmap_xlow, ix->X_low, ix->n_pad, ix->d, (ix->d % 64 == 0) ? 64 : 32, ix->low == LV_BF16,
-                           lv::score_tile_rows(ix->d));
-  if (!st) st = make_search_tmap(ix);
+  lv_status st = make_xlow_tmap(ix);
   ix->plan.valid = false;
   return st;
 }

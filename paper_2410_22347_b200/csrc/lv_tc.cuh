@@ -166,6 +166,15 @@ LV_TC_INL void mma_f16_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::i8 (signed 8-bit inputs, K = 32 per instruction, s32
+// accumulate), A (M x K, 4 per 32-bit column) in TMEM.
+LV_TC_INL void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 LV_TC_INL void mma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t.reg .b32 rl;\n\telect.sync rl|e, 0xffffffff;\n\t"
@@ -192,6 +201,9 @@ LV_TC_INL void tmem_st_32x32b_x4(uint32_t taddr, const uint32_t (&r)[4]) {
                "r"(r[2]), "r"(r[3])
                : "memory");
 }
+LV_TC_INL void tmem_st_32x32b_x2(uint32_t taddr, const uint32_t (&r)[2]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(r[0]), "r"(r[1]) : "memory");
+}
 LV_TC_INL void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete.
@@ -210,11 +222,16 @@ __host__ __device__ constexpr uint32_t make_idesc_f16(int M, int N, bool bf16) {
          | ((uint32_t)(M >> 4) << 24);           // M >> 4
 }
 
+// Instruction descriptor, kind::i8: D s32 (fmt 2), A/B signed 8-bit (fmt 1), both K-major.
+__host__ __device__ constexpr uint32_t make_idesc_i8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
 // Shared-memory matrix descriptor for a K-major operand stored as rows of `row_bytes`
-// (64 B -> SWIZZLE_64B, 128 B -> SWIZZLE_128B) as written by TMA with the same swizzle.
-// Stride between 8-row core-matrix groups = 8 * row_bytes.
+// (32 B -> SWIZZLE_32B, 64 B -> SWIZZLE_64B, 128 B -> SWIZZLE_128B) as written by TMA with the
+// same swizzle.  Stride between 8-row core-matrix groups = 8 * row_bytes.
 LV_TC_INL uint64_t make_sdesc(uint32_t smem_addr, uint32_t row_bytes) {
-  const uint64_t layout = (row_bytes == 128) ? 2ull : 4ull;   // SWIZZLE_128B : SWIZZLE_64B
+  const uint64_t layout = (row_bytes == 128) ? 2ull : (row_bytes == 64 ? 4ull : 6ull);
   uint64_t d = 0;
   d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);                 // start address
   d |= (uint64_t)1u << 16;                                      // LBO (unused for swizzled K-major)

@@ -15,16 +15,17 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LV_LIB") or os.path.join(HERE, "liblv.so")   # LV_LIB: experiment builds
 
-LV_F32, LV_F16, LV_BF16 = 0, 1, 2
-_DT = {"fp32": LV_F32, "f32": LV_F32, "fp16": LV_F16, "f16": LV_F16, "bf16": LV_BF16}
-_TORCH_DT = {LV_F32: torch.float32, LV_F16: torch.float16, LV_BF16: torch.bfloat16}
+LV_F32, LV_F16, LV_BF16, LV_I8 = 0, 1, 2, 3
+_DT = {"fp32": LV_F32, "f32": LV_F32, "fp16": LV_F16, "f16": LV_F16, "bf16": LV_BF16, "i8": LV_I8, "int8": LV_I8}
+_TORCH_DT = {LV_F32: torch.float32, LV_F16: torch.float16, LV_BF16: torch.bfloat16, LV_I8: torch.int8}
 
 EXPORTS = ["lv_last_error", "lv_version", "lv_fit_stats", "lv_index_create", "lv_encode_database",
            "lv_project_queries", "lv_search", "lv_search_host", "lv_timing_collect", "lv_encode_timing", "lv_assign_tags",
            "lv_index_info", "lv_index_export", "lv_index_destroy", "lv_index_set_search_dim",
            "lv_index_get_search_dim", "lv_normalize_rows", "lv_kmeans_assign", "lv_kmeans_centre_sums",
            "lv_index_create_flex", "lv_stream_insert", "lv_stream_remove", "lv_stream_observe_queries",
-           "lv_stream_stats", "lv_stream_reproject", "lv_index_export_xprime"]
+           "lv_stream_stats", "lv_stream_reproject", "lv_index_export_xprime", "lv_project_queries_i8",
+           "lv_index_i8_scales"]
 
 
 class LVError(RuntimeError):
@@ -68,6 +69,8 @@ def lib():
             "lv_assign_tags": [vp, i32, i64, i32, vp, i32, vp, vp],
             "lv_normalize_rows": [vp, i32, i64, i32, vp, vp],
             "lv_index_create_flex": [ctypes.POINTER(vp), i32, i32, i32, vp, vp, i64],
+            "lv_project_queries_i8": [vp, vp, i64, vp, vp, vp],
+            "lv_index_i8_scales": [vp, vp],
             "lv_stream_insert": [vp, vp, i32, i64, vp, vp],
             "lv_stream_remove": [vp, vp, i64, vp],
             "lv_stream_observe_queries": [vp, vp, i64, vp],
@@ -271,6 +274,24 @@ def lv_project_queries(index: Index, Q: torch.Tensor) -> torch.Tensor:
                      device=Q.device)
     _check(lib().lv_project_queries(index.h, _ptr(Q), Q.shape[0], _ptr(Qp), _stream()), "lv_project_queries")
     return Qp
+
+
+def lv_project_queries_i8(index: Index, Q: torch.Tensor):
+    """int8 index: query codes int8 [m, C * d_search] and scales fp32 [m, C] (R21)."""
+    Q = _dev(Q, torch.float32)
+    ds = lv_index_get_search_dim(index)
+    codes = torch.empty((Q.shape[0], index.C * ds), dtype=torch.int8, device=Q.device)
+    scales = torch.empty((Q.shape[0], index.C), dtype=torch.float32, device=Q.device)
+    _check(lib().lv_project_queries_i8(index.h, _ptr(Q), Q.shape[0], _ptr(codes), _ptr(scales), _stream()),
+           "lv_project_queries_i8")
+    return codes, scales
+
+
+def lv_index_i8_scales(index: Index) -> np.ndarray:
+    """delta [C, d] fp32 of an encoded int8 index."""
+    out = np.zeros((index.C, index.d), dtype=np.float32)
+    _check(lib().lv_index_i8_scales(index.h, out.ctypes.data_as(ctypes.c_void_p)), "lv_index_i8_scales")
+    return out
 
 
 def lv_search(index: Index, Q: torch.Tensor, k: int, R: int, cand: bool = False, raw: bool = False,
