@@ -166,17 +166,27 @@ def build_index(cfg, rank=0, world=1, log=print, family=None):
             "fit_s": t_fit, "encode_ms": t_enc, "encode_kernels": enc_k, "n_pad": n_pad, "gaps": f.get("gaps")}
 
 
+def _peak_for(cfg):
+    """Tensor peak of the scan's dtype: the measured bf16 dense peak, x2 for int8 (the guide's
+    nominal ratio, 4.5 vs 2.25 dense P(FL)OP/s)."""
+    pk = _peaks()
+    f = 2.0 if cfg.low_dtype == "i8" else 1.0
+    return pk["bf16"] * f, (pk["bf16_sus"] * f if pk["bf16_sus"] else None), \
+        ("int8 dense = 2 x measured bf16 burst (nominal ratio)" if f > 1 else "bf16 dense burst")
+
+
 def roofline_scan(cfg, ms, m):
     """Dominant kernel: the main k_score_topr launch (every database row x every query, 2 d flop
     per score).  ms = its average launch time over the timed region (CUDA events)."""
     pk = _peaks()
+    peak, sus, what = _peak_for(cfg)
     flops = 2.0 * m * cfg.n * cfg.d
     ach = flops / (ms * 1e-3) / 1e12
-    return {"bound": "tensor", "achieved": round(ach, 1), "peak": pk["bf16"], "unit": "TFLOP/s",
-            "frac": round(ach / pk["bf16"], 4), "frac_of_sustained": round(ach / pk["bf16_sus"], 4) if pk["bf16_sus"] else None,
-            "peak_source": pk["src"] + ", bf16 dense burst (sustained alongside)",
+    return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s" if cfg.low_dtype != "i8" else "TOP/s",
+            "frac": round(ach / peak, 4), "frac_of_sustained": round(ach / sus, 4) if sus else None,
+            "peak_source": pk["src"] + ", " + what + " (sustained alongside)",
             "kernel": "k_score_topr main stage (K2/K3 fused scoring + top-R)", "launch_ms": round(ms, 4),
-            "algorithmic": f"2*m*n*d = {flops:.3e} flop per launch", "traffic": _ncu_traffic(cfg.cfg_id)}
+            "algorithmic": f"2*m*n*d = {flops:.3e} flop per launch", "traffic": _ncu_traffic(_tkey(cfg))}
 
 
 def roofline_rerank(cfg, ms, m):
@@ -192,7 +202,7 @@ def roofline_rerank(cfg, ms, m):
     traffic = None
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
-        traffic = json.load(open(p)).get(f"cfg{cfg.cfg_id}", {}).get("rerank_K5_dram_bytes_per_launch")
+        traffic = json.load(open(p)).get(f"cfg{cfg.cfg_id}", {}).get("rerank_K5_dram_bytes_per_launch")   # K5 is the same for every X_low dtype
     ach = traffic / (ms * 1e-3) / 1e9 if traffic else alg
     return {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s", "frac": round(ach / pk["hbm"], 4),
             "frac_basis": "ncu DRAM bytes per launch / CUDA-event time" if traffic else "algorithmic bytes (no ncu capture)",
@@ -203,11 +213,11 @@ def roofline_rerank(cfg, ms, m):
 def scan_phase(cfg, kms, m):
     """The whole scoring + top-R phase (sample stage + threshold select + main scan + K4 top-R
     select) against the bf16 tensor peak, 2 m n d flop (burst; sustained alongside)."""
-    pk = _peaks()
+    peak, sus, _ = _peak_for(cfg)
     ms = kms["sample_stage"] + kms["threshold_select"] + kms["main_scan"] + kms["select_K4"]
     tf = 2.0 * m * cfg.n * cfg.d / (ms * 1e-3) / 1e12
-    return {"ms": round(ms, 4), "frac_of_bf16_peak": round(tf / pk["bf16"], 4),
-            "frac_of_sustained": round(tf / pk["bf16_sus"], 4) if pk["bf16_sus"] else None,
+    return {"ms": round(ms, 4), "frac_of_tensor_peak": round(tf / peak, 4),
+            "frac_of_sustained": round(tf / sus, 4) if sus else None,
             "note": "sample stage + threshold select + main scan + K4 top-R select (the scoring + top-R phase)"}
 
 
@@ -226,13 +236,17 @@ def roofline_encode(cfg, k6_ms, n_pad, x_bytes):
             "algorithmic": f"{byts:.3e} B per launch (n D {x_bytes} + n_pad d 2 + n_pad 4)"}
 
 
-def _ncu_traffic(cfg_id):
+def _tkey(cfg):
+    return f"cfg{cfg.cfg_id}" + ("_i8" if cfg.low_dtype == "i8" else "")
+
+
+def _ncu_traffic(key):
     """dram__bytes_read.sum + dram__bytes_write.sum of the main scan launch, from the committed
     ncu capture summary (profiles/ncu_traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get(f"cfg{cfg_id}", {}).get("main_scan_dram_bytes_per_launch")
+            return json.load(open(p)).get(key, {}).get("main_scan_dram_bytes_per_launch")
         except Exception:
             return None
     return None
@@ -256,28 +270,52 @@ def reduce_max_ms(ms, world):
     return float(t.item())
 
 
+def oracle_database(cfg, X, B, assign):
+    """The oracle's stored reduced database (chunked encode so a 10M x 768 database is never
+    converted to fp64 at once): storage-rounded X_low, or for int8 the codes and delta."""
+    import oracle as O
+    ch = 1 << 19
+    chunks = [O.encode(X[lo:lo + ch], B, None if assign is None else assign[lo:lo + ch],
+                       store=None if cfg.low_dtype == "i8" else cfg.low_dtype) for lo in range(0, X.shape[0], ch)]
+    if cfg.low_dtype != "i8":
+        return {"X_low": np.concatenate(chunks)}
+    x32 = np.concatenate([c.astype(np.float32) for c in chunks])
+    del chunks
+    codes, delta = O.quantize_db_i8(x32, assign, cfg.C)
+    return {"codes": codes, "delta": delta}
+
+
+def oracle_search_sample(cfg, Qs, X, A, assign, db):
+    """The oracle's search of a query sample against the stored database (project, exhaustive
+    reduced top-R, fp64 re-rank, top-k)."""
+    import oracle as O
+    if cfg.low_dtype == "i8":
+        qc, qs = O.quantize_queries_i8(O.project(Qs, A), db["delta"])
+        Qeff = qs[:, :, None].astype(np.float64) * qc.astype(np.float64)
+        cand, _ = O.reduced_search(Qeff, db["codes"].astype(np.float64), assign, cfg.R, score_fp32=True)
+    else:
+        cand, _ = O.reduced_search(O.project(Qs, A, store=cfg.low_dtype), db["X_low"], assign, cfg.R)
+    ids, _ = O.rerank_topk(Qs, X, cand, cfg.k)
+    return ids
+
+
 def cpu_baseline(cfg, data, nq, log=print):
     """The fp64 oracle (as it stands) on a bounded sample of the same workload."""
-    import oracle as O
     ncores = len(os.sched_getaffinity(0))
     A, B = data["A"], data["B"]
     assign = None if data["assign"] is None else data["assign"].cpu().numpy()
     X = data["X"]
     t0 = time.time()
-    ch = 1 << 19   # chunked so a 10M x 768 database is never converted to fp64 at once
-    X_low = np.concatenate([O.encode(X[lo:lo + ch], B, None if assign is None else assign[lo:lo + ch],
-                                     store=cfg.low_dtype) for lo in range(0, X.shape[0], ch)])
+    db = oracle_database(cfg, X, B, assign)
     t_enc = time.time() - t0
     Qs = data["Q"][:nq]
     t0 = time.time()
-    Qp = O.project(Qs, A, store=cfg.low_dtype)
-    cand, _ = O.reduced_search(Qp, X_low, assign, cfg.R)
-    ids, _ = O.rerank_topk(Qs, X, cand, cfg.k)
+    ids = oracle_search_sample(cfg, Qs, X, A, assign, db)
     dt = time.time() - t0
     log(f"[bench] oracle: {nq} queries in {dt:.1f}s (encode {t_enc:.1f}s, untimed)")
     return {"value": round(nq / dt, 3), "unit": "queries/s", "cores": ncores, "kind": "oracle",
             "sample": f"{nq} of {cfg.m_test} queries, full n={cfg.n} database (project + exhaustive reduced top-R + "
-                      f"re-rank + top-k, fp64 numpy/OpenBLAS); X_low encode untimed"}, ids, X_low
+                      f"re-rank + top-k, fp64 numpy/OpenBLAS); X_low encode untimed"}, ids, db
 
 
 def main():
@@ -291,6 +329,8 @@ def main():
                     help="oracle sample (default 200 queries at 1M rows, 32 at 10M rows)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--family", default=None, help="query family (cfg 4: ood (default) or id; one fit + encode each)")
+    ap.add_argument("--low", default=None, choices=["bf16", "fp16", "i8"],
+                    help="storage of the reduced vectors (default: the config's; i8 = NEXT-4 8-bit scalar quantisation)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -301,10 +341,13 @@ def main():
 
     import lvgen
     cfg = lvgen.get_config(args.config)
+    if args.low:
+        cfg = cfg.replace(low_dtype=args.low)
     if args.oracle_queries is None:
         args.oracle_queries = 200 if cfg.n <= 2_000_000 else 32
     family = args.family or cfg.families[-1]
-    workload = f"cfg{cfg.cfg_id} {cfg.name}" + (f" [{family} queries]" if len(cfg.families) > 1 else "")
+    workload = f"cfg{cfg.cfg_id} {cfg.name}" + (f" [{family} queries]" if len(cfg.families) > 1 else "") + \
+        (f" [{cfg.low_dtype} reduced vectors]" if args.low else "")
     conf = {"workload": workload, "n": cfg.n, "D": cfg.D, "d": cfg.d, "C": cfg.C, "m": cfg.m_test, "R": cfg.R,
             "k": cfg.k, "low_dtype": cfg.low_dtype, "full_dtype": cfg.full_dtype,
             "l2": "no flush: X_low and X exceed the 126 MB L2 and are streamed every step"}
@@ -325,15 +368,12 @@ def main():
             A, B = g["A"], g["B"]
             assign = np.concatenate([O.assign_tags(X[lo:lo + (1 << 19)], g["centres"])
                                      for lo in range(0, X.shape[0], 1 << 19)])
-        X_low = np.concatenate([O.encode(X[lo:lo + (1 << 19)], B, None if assign is None else assign[lo:lo + (1 << 19)],
-                                         store=cfg.low_dtype) for lo in range(0, X.shape[0], 1 << 19)])
+        db = oracle_database(cfg, X, B, assign)
         per = max(1, args.oracle_queries // (4 if cfg.n <= 2_000_000 else 16))
         def step(i):
             lo = (i * per) % cfg.m_test
             Qs = Q[lo:lo + per]
-            Qp = O.project(Qs, A, store=cfg.low_dtype)
-            cand, _ = O.reduced_search(Qp, X_low, assign, cfg.R)
-            O.rerank_topk(Qs, X, cand, cfg.k)
+            oracle_search_sample(cfg, Qs, X, A, assign, db)
         for i in range(args.warmup):
             step(i)
         t0 = time.time()
