@@ -566,110 +566,150 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the job's 32-column halves in turn: load, (mask), max, compare, rare hit path; the
         // accumulator is released after the last half's load
         float bm = -FLT_MAX;   // sample stage: running block maximum of the job
-#pragma unroll
-        for (int h = 0; h < kJV; ++h) {
-          float v[32];
-          tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kN + (uint32_t)(jh * kJobCols + 32 * h), v);
-          tc::tmem_wait_ld();
-          if (h + 1 == kJV) {
-            tc::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
-          }
-          if (skip_topr) continue;
-          const int hpos = base_pos + 32 * h;
-          if (t == t_last) {   // a cluster segment's last tile may be partial
-            const int tv = a.tile_valid[t_last] - (jh * kJobCols + 32 * h);
-            if (tv < 32) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (j >= tv) v[j] = kI8 ? __int_as_float(INT_MIN) : -FLT_MAX;
-            }
-          }
-          // int8: v holds s32 accumulators; the score of column j is fl(qs * float(acc_j))
-          auto score_of = [&](float raw) -> float {
-            if (!kI8) return raw;
-            const int iv = __float_as_int(raw);
-            return iv == INT_MIN ? -FLT_MAX : qs * (float)iv;
-          };
-          if (a.raw != nullptr) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + hpos + j] = score_of(v[j]);
-          }
-          float mx;
-          bool hit;
-          if (kI8) {
-            int im = __float_as_int(v[0]);
-#pragma unroll
-            for (int j = 1; j < 32; ++j) im = max(im, __float_as_int(v[j]));
-            mx = im == INT_MIN ? -FLT_MAX : qs * (float)im;
-            hit = im >= ti && im > INT_MIN;
-          } else {
-            mx = v[0];
-#pragma unroll
-            for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
-            hit = mx >= ts && mx > -FLT_MAX;
-          }
-          if (kSample) {
-            // sample stage: record block maxima (query q; blocks of 32 database rows when
-            // a.flags & 8, else of the job's 64: fine blocks keep the threshold estimate of
-            // DESIGN.md §6 tight when top rows cluster); no top-R here
-            const int sblk = (sbase + (t - t0) / tstride) * kJobsPerTile + jh;
-            if (fine_blocks) {
-              a.bmax[(size_t)(sblk * kJV + h) * a.m_pad + q] = mx;
-            } else {
-              bm = fmaxf(bm, mx);
-              if (h + 1 == kJV) a.bmax[(size_t)sblk * a.m_pad + q] = bm;
-            }
-            continue;
-          }
-
-          uint32_t hb = __ballot_sync(0xffffffffu, hit);
-          if (hb == 0u) continue;
-          if (count_stats && lane == 0) atomicAdd(a.stats + 0, 1ull);
-          if (fast_only) continue;
-          // hit path (divergence-free): each hitting lane's 32 scores are broadcast through shared
-          // memory, lane j tests column j, survivors are appended to the hitting lane's sub-list
-          // with coalesced stores
-          const int32_t id_h = (a.perm ? my_id[h] : hpos + lane);
-          if (hit) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              reinterpret_cast<float4*>(srows[lane])[j] =
-                  make_float4(score_of(v[4 * j]), score_of(v[4 * j + 1]), score_of(v[4 * j + 2]), score_of(v[4 * j + 3]));
-          }
-          __syncwarp();
-          do {
-            const int Lz = __ffs(hb) - 1;
-            hb &= hb - 1u;
-            const float f = srows[Lz][lane];
-            const float tsz = __shfl_sync(0xffffffffu, ts, Lz);
-            uint64_t tkz = __shfl_sync(0xffffffffu, tk, Lz);
-            int cz = __shfl_sync(0xffffffffu, cnt, Lz);
-            const uint64_t key = make_key(f, id_h);
-            bool keep = f >= tsz && f > -FLT_MAX && key > tkz;
-            uint32_t kb = __ballot_sync(0xffffffffu, keep);
-            if (kb == 0u) continue;
-            uint64_t* bz = reinterpret_cast<uint64_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(bp), Lz));
-            if (cz + __popc(kb) > a.Cap) {
-              // full sub-list: compact it to its top-R (raises its threshold), then re-filter
-              uint64_t nthr;
-              cz = warp_compact_fast(bz, cz, a.R, a.Cap, lane, hist, &nthr);
-              tkz = nthr;
-              if (lane == Lz) {
-                tk = nthr;
-                ts = thr_score(nthr);
-                if (kI8) ti = i8_threshold(ts, qs);
+        // one 32-column half of the job: (mask), raw output, max, threshold test, rare hit path
+        auto half = [&](float (&v)[32], const int h) {
+            if (skip_topr) return;
+            const int hpos = base_pos + 32 * h;
+            if (t == t_last) {   // a cluster segment's last tile may be partial
+              const int tv = a.tile_valid[t_last] - (jh * kJobCols + 32 * h);
+              if (tv < 32) {
+  #pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (j >= tv) v[j] = kI8 ? __int_as_float(INT_MIN) : -FLT_MAX;
               }
-              if (count_stats && lane == 0) atomicAdd(a.stats + 2, 1ull);
-              keep = keep && key > tkz;
-              kb = __ballot_sync(0xffffffffu, keep);
             }
-            if (keep) bz[cz + __popc(kb & lt)] = key;
-            if (lane == Lz) cnt = cz + __popc(kb);
-            if (count_stats && lane == 0) atomicAdd(a.stats + 1, (unsigned long long)__popc(kb));
-          } while (hb != 0u);
+            // int8: v holds s32 accumulators; the score of column j is fl(qs * float(acc_j))
+            auto score_of = [&](float raw) -> float {
+              if (!kI8) return raw;
+              const int iv = __float_as_int(raw);
+              return iv == INT_MIN ? -FLT_MAX : qs * (float)iv;
+            };
+            if (a.raw != nullptr) {
+  #pragma unroll
+              for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + hpos + j] = score_of(v[j]);
+            }
+            float mx;
+            bool hit;
+            if (kI8) {
+              // tree of integer maxima (a 31-deep dependent chain would expose its latency)
+              int t16[16];
+  #pragma unroll
+              for (int j = 0; j < 16; ++j) t16[j] = max(__float_as_int(v[j]), __float_as_int(v[j + 16]));
+  #pragma unroll
+              for (int w = 8; w >= 1; w >>= 1)
+  #pragma unroll
+                for (int j = 0; j < w; ++j) t16[j] = max(t16[j], t16[j + w]);
+              const int im = t16[0];
+              mx = im == INT_MIN ? -FLT_MAX : qs * (float)im;
+              hit = im >= ti && im > INT_MIN;
+            } else {
+#if defined(LV_EPI_TREE)
+              float t16[16];
+  #pragma unroll
+              for (int j = 0; j < 16; ++j) t16[j] = fmaxf(v[j], v[j + 16]);
+  #pragma unroll
+              for (int w = 8; w >= 1; w >>= 1)
+  #pragma unroll
+                for (int j = 0; j < w; ++j) t16[j] = fmaxf(t16[j], t16[j + w]);
+              mx = t16[0];
+#else
+              mx = v[0];
+  #pragma unroll
+              for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
+#endif
+              hit = mx >= ts && mx > -FLT_MAX;
+            }
+            if (kSample) {
+              // sample stage: record block maxima (query q; blocks of 32 database rows when
+              // a.flags & 8, else of the job's 64: fine blocks keep the threshold estimate of
+              // DESIGN.md §6 tight when top rows cluster); no top-R here
+              const int sblk = (sbase + (t - t0) / tstride) * kJobsPerTile + jh;
+              if (fine_blocks) {
+                a.bmax[(size_t)(sblk * kJV + h) * a.m_pad + q] = mx;
+              } else {
+                bm = fmaxf(bm, mx);
+                if (h + 1 == kJV) a.bmax[(size_t)sblk * a.m_pad + q] = bm;
+              }
+              return;
+            }
+
+            uint32_t hb = __ballot_sync(0xffffffffu, hit);
+            if (hb == 0u) return;
+            if (count_stats && lane == 0) atomicAdd(a.stats + 0, 1ull);
+            if (fast_only) return;
+            // hit path (divergence-free): each hitting lane's 32 scores are broadcast through shared
+            // memory, lane j tests column j, survivors are appended to the hitting lane's sub-list
+            // with coalesced stores
+            const int32_t id_h = (a.perm ? my_id[h] : hpos + lane);
+            if (hit) {
+  #pragma unroll
+              for (int j = 0; j < 8; ++j)
+                reinterpret_cast<float4*>(srows[lane])[j] =
+                    make_float4(score_of(v[4 * j]), score_of(v[4 * j + 1]), score_of(v[4 * j + 2]), score_of(v[4 * j + 3]));
+            }
+            __syncwarp();
+            do {
+              const int Lz = __ffs(hb) - 1;
+              hb &= hb - 1u;
+              const float f = srows[Lz][lane];
+              const float tsz = __shfl_sync(0xffffffffu, ts, Lz);
+              uint64_t tkz = __shfl_sync(0xffffffffu, tk, Lz);
+              int cz = __shfl_sync(0xffffffffu, cnt, Lz);
+              const uint64_t key = make_key(f, id_h);
+              bool keep = f >= tsz && f > -FLT_MAX && key > tkz;
+              uint32_t kb = __ballot_sync(0xffffffffu, keep);
+              if (kb == 0u) return;
+              uint64_t* bz = reinterpret_cast<uint64_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(bp), Lz));
+              if (cz + __popc(kb) > a.Cap) {
+                // full sub-list: compact it to its top-R (raises its threshold), then re-filter
+                uint64_t nthr;
+                cz = warp_compact_fast(bz, cz, a.R, a.Cap, lane, hist, &nthr);
+                tkz = nthr;
+                if (lane == Lz) {
+                  tk = nthr;
+                  ts = thr_score(nthr);
+                  if (kI8) ti = i8_threshold(ts, qs);
+                }
+                if (count_stats && lane == 0) atomicAdd(a.stats + 2, 1ull);
+                keep = keep && key > tkz;
+                kb = __ballot_sync(0xffffffffu, keep);
+              }
+              if (keep) bz[cz + __popc(kb & lt)] = key;
+              if (lane == Lz) cnt = cz + __popc(kb);
+              if (count_stats && lane == 0) atomicAdd(a.stats + 1, (unsigned long long)__popc(kb));
+            } while (hb != 0u);
+            __syncwarp();
+        };
+#if defined(LV_EPI_DUAL)
+        if constexpr (kJV == 2) {
+          // both halves loaded before one wait (the second load's latency hides behind the first's)
+          float v0[32], v1[32];
+          tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kN + (uint32_t)(jh * kJobCols), v0);
+          tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kN + (uint32_t)(jh * kJobCols + 32), v1);
+          tc::tmem_wait_ld();
+          tc::tc_fence_before();
           __syncwarp();
+          if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
+          if (!skip_topr) {
+            half(v0, 0);
+            half(v1, 1);
+          }
+        } else
+#endif
+        {
+#pragma unroll
+          for (int h = 0; h < kJV; ++h) {
+            float v[32];
+            tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kN + (uint32_t)(jh * kJobCols + 32 * h), v);
+            tc::tmem_wait_ld();
+            if (h + 1 == kJV) {
+              tc::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
+            }
+            if (skip_topr) continue;
+            half(v, h);
+          }
         }
       }
       tiles_before += n_t;

@@ -66,15 +66,32 @@ def test_i8_codes_match_oracle(lv, cfg_id, d, C):
     c, X, Q, A32, B32, assign = _fitted(cfg_id, 8000, 300, d, C)
     ix = _index(lv, c, X, A32, B32, assign, C)
     xc, delta = _gpu_codes(lv, ix, c, C)
-    ref_c, ref_d = O.quantize_db_i8(O.encode(X, B32 if C > 1 else B32[0], assign), assign, C)
-    assert np.all(np.abs(delta.astype(np.float64) / ref_d.astype(np.float64) - 1) <= 2.0 ** -22)
+    B1 = B32 if C > 1 else B32[0]
+    x_ref = O.encode(X, B1, assign)
+    ref_c, ref_d = O.quantize_db_i8(x_ref, assign, C)
+    # delta = max|x| / 127 inherits the fp32-faithful product's error at the column's extreme
+    # (G1's accumulation bound D 2^-24 sum_k |b_k x_k|) plus one fp32 ulp of each division
+    absdot = O.encode(np.abs(X.astype(np.float64)), np.abs(B1), assign)
+    a = np.zeros(X.shape[0], np.int64) if assign is None else assign
+    for cc in range(C):
+        rows = np.nonzero(a == cc)[0]
+        if rows.size == 0:
+            continue
+        arg = rows[np.argmax(np.abs(x_ref[rows]), axis=0)]
+        bound = (c.D * 2.0 ** -24 * absdot[arg, np.arange(c.d)] / 127.0
+                 + 2.0 ** -22 * ref_d[cc].astype(np.float64))
+        assert np.all(np.abs(delta[cc].astype(np.float64) - ref_d[cc].astype(np.float64)) <= bound), cc
     diff = np.abs(xc.astype(int) - ref_c.astype(int))
     assert diff.max() <= 1 and (diff > 0).mean() < 5e-3, (diff > 0).mean()
     qc, qs = lv.lv_project_queries_i8(ix, torch.from_numpy(Q).cuda())
     rq, rs = O.quantize_queries_i8(O.project(Q, A32), delta)   # the GPU's delta: query parity alone
     qd = np.abs(qc.cpu().numpy().reshape(rq.shape).astype(int) - rq.astype(int))
     assert qd.max() <= 1 and (qd > 0).mean() < 5e-3
-    assert np.all(np.abs(qs.cpu().numpy().astype(np.float64) / rs.astype(np.float64) - 1) <= 2.0 ** -22)
+    # s = max|q' delta| / 127 with the same fp32-accumulation allowance on q' (K1's product)
+    qabs = O.project(np.abs(Q.astype(np.float64)), np.abs(A32))                  # [m, C, d]
+    sbound = (c.D * 2.0 ** -24 * (qabs * delta[None].astype(np.float64)).max(axis=2) / 127.0
+              + 2.0 ** -22 * rs.astype(np.float64))
+    assert np.all(np.abs(qs.cpu().numpy().astype(np.float64) - rs.astype(np.float64)) <= sbound)
 
 
 @pytest.mark.parametrize("d", [32, 64, 96, 128, 160, 192])
