@@ -88,8 +88,11 @@ lv_status lv_timing_collect(lv_index* index, float* kernel_ms, int32_t* calls);
 /*
  * lv_encode_timing — kernel times of the last lv_encode_database on this index (recorded with
  * CUDA events on its stream; the call synchronises before returning, so they are ready).
- * ms HOST float[3] out: [0] cluster sort + per-tile tables (C > 1; else the identity perm),
- * [1] K6 encode X_low = RNE(B_c x) (the kernel of Eq.(14)), [2] full-precision copy for K5.
+ * ms HOST float[3] out: [0] the cluster sort's kernels (histogram + scan and scatter; C = 1: the
+ * identity perm) — host allocation and the per-tile tables between them are not timed, [1] K6
+ * encode X_low = RNE(B_c x) (the kernel of Eq.(14); int8: with the scale and code kernels),
+ * [2] full-precision copy for K5.  A flexible index reports [1] x' GEMM + prefix rounding and
+ * [2] the K_X statistics.
  * LV_EINVAL when no encode has run.
  */
 lv_status lv_encode_timing(const lv_index* index, float* ms);

@@ -50,19 +50,26 @@ constexpr int kUQ = 4;                 // work-unit queue depth (dynamic unit or
 
 __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
-// TMEM: the A operand (one 128-query tile, d bf16 = d/2 columns) then NACC fp32 accumulator
-// buffers of N = 128 columns.  A is double-buffered across work units (the next unit's A is
-// written while the current one runs) unless that would leave fewer than 3 accumulators
-// (d > 128): then A is single-buffered and rewritten after each unit (one short bubble per
-// unit, units are long at those sizes).
+// TMEM: the A operand (one 128-query tile, d * esz / 4 columns per buffer) then NACC fp32 / s32
+// accumulator buffers of kAccN = 128 columns (one database tile).  LV_HALF_ACC (experiment build)
+// makes a buffer half a tile (two N = 64 MMAs per tile, one 64-column job per buffer): measured
+// slower (cfg 2 main scan 2.37 vs 2.15 ms; an N = 64 tcgen05.mma costs about as long as an N = 128
+// one, so the tile's MMA time doubles).  A is double-buffered across work units (the next unit's A is written while
+// the current one runs) unless that would leave too few accumulators: then A is single-buffered
+// and rewritten after each unit (one short bubble per unit, units are long at those sizes).
 constexpr int kTileN = 128;
+#if defined(LV_HALF_ACC)
+constexpr int kAccN = 64, kMinAcc = 5;
+#else
+constexpr int kAccN = 128, kMinAcc = 3;
+#endif
 // esz = bytes per reduced element (2: bf16/fp16, 1: int8); an A buffer takes d * esz / 4 columns
-__host__ __device__ constexpr bool score_single_a(int d, int esz = 2) { return (512 - d * esz / 2) / kTileN < 3; }
+__host__ __device__ constexpr bool score_single_a(int d, int esz = 2) { return (512 - d * esz / 2) / kAccN < kMinAcc; }
 __host__ __device__ constexpr int score_a_cols(int d, int esz = 2) {
   return score_single_a(d, esz) ? d * esz / 4 : d * esz / 2;
 }
 __host__ __device__ constexpr int score_nacc(int d, int esz = 2) {
-  return (512 - score_a_cols(d, esz)) / kTileN > kMaxAcc ? kMaxAcc : (512 - score_a_cols(d, esz)) / kTileN;
+  return (512 - score_a_cols(d, esz)) / kAccN > kMaxAcc ? kMaxAcc : (512 - score_a_cols(d, esz)) / kAccN;
 }
 __host__ __device__ constexpr int score_tile_n(int d) { return kTileN + 0 * d; }
 // bytes per row of one swizzled TMA box of X_low (the swizzle width): bf16/fp16 128 B when d % 64
@@ -70,11 +77,14 @@ __host__ __device__ constexpr int score_tile_n(int d) { return kTileN + 0 * d; }
 __host__ __device__ constexpr int score_box_bytes(int d, int esz) {
   return esz == 2 ? ((d % 64 == 0) ? 128 : 64) : ((d % 128 == 0) ? 128 : ((d % 64 == 0) ? 64 : 32));
 }
-// Epilogue jobs: (128-column tile, column block) per TMEM lane quarter, taken in order by the
-// quarter's 4 warps.  A waiting warp checks the accumulator barrier by phase parity, which is
-// only unambiguous while the quarter's in-flight jobs (<= 4) span at most nacc tiles; hence
-// 64-column jobs (2 per tile, span <= 3 tiles) need nacc >= 3, else 32-column jobs (span <= 2).
-__host__ __device__ constexpr int job_cols(int d, int esz = 2) { return score_nacc(d, esz) >= 3 ? 64 : 32; }
+// Epilogue jobs: (tile, column block) per TMEM lane quarter, taken in order by the quarter's 4
+// warps.  A waiting warp checks its accumulator buffer's barrier by phase parity, which is only
+// unambiguous while the quarter's in-flight jobs (<= 4) span at most nacc buffers: with half-tile
+// buffers every job is one buffer (64 columns, nacc >= 5); with full-tile buffers 64-column jobs
+// (2 per tile, span <= 3 tiles) need nacc >= 3, else 32-column jobs (span <= 2).
+__host__ __device__ constexpr int job_cols(int d, int esz = 2) {
+  return kAccN == 64 ? 64 : (score_nacc(d, esz) >= 3 ? 64 : 32);
+}
 
 __host__ __device__ inline ScoreSmemLayout score_smem_layout(int d, int stages, int esz = 2) {
   ScoreSmemLayout L;
@@ -262,7 +272,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kJobCols = job_cols(kD, kEsz);    // score columns per epilogue job
   constexpr int kJV = kJobCols / 32;              // 32-column tcgen05.ld per job
   constexpr int kJobsPerTile = 128 / kJobCols;    // jobs per lane quarter and tile
-  static_assert((3 + kJobsPerTile - 1) / kJobsPerTile + 1 <= nacc, "4 in-flight jobs must span <= nacc tiles");
+  constexpr int kHalves = kTileN / kAccN;           // accumulator buffers per database tile
+  constexpr int kJobsPerBuf = kAccN / kJobCols;     // jobs per buffer and lane quarter
+  static_assert((3 + kJobsPerBuf - 1) / kJobsPerBuf + 1 <= nacc, "4 in-flight jobs must span <= nacc buffers");
   const ScoreSmemLayout L = score_smem_layout(d, a.stages, kEsz);
   uint8_t* sB = smem + L.b_off;
   EpiShared& S = *reinterpret_cast<EpiShared*>(smem + L.epi_off);
@@ -294,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < nacc; ++s) {
       tc::mbar_init(acc_full + s, 1);
-      tc::mbar_init(acc_empty + s, 4 * kJobsPerTile);   // one arrival per (lane quarter, job)
+      tc::mbar_init(acc_empty + s, 4 * kJobsPerBuf);   // one arrival per (lane quarter, job)
     }
     tc::mbar_init(a_full + 0, kEpiWarps);
     tc::mbar_init(a_full + 1, kEpiWarps);
@@ -380,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer (A from TMEM)
-    constexpr uint32_t idesc = kI8 ? tc::make_idesc_i8(128, kN) : tc::make_idesc_f16(128, kN, kFmt == 1);
+    constexpr uint32_t idesc = kI8 ? tc::make_idesc_i8(128, kAccN) : tc::make_idesc_f16(128, kAccN, kFmt == 1);
     const uint32_t sB_addr = tc::smem_u32(sB);
     int stage = 0;
     uint32_t phase = 0;
@@ -400,31 +412,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tc_fence_after();
       const uint32_t at = tmem_base + (kSingleA ? 0u : (uint32_t)(i & 1) * kACols);
       for (int t = t0; t < t1; t += ts_) {
-        tc::mbar_wait_sleep(acc_empty + acc, acc_phase ^ 1);
-        tc::mbar_wait_sleep(b_full + stage, phase);
-        tc::tc_fence_after();
-        if (issuer) {
-          const uint64_t bd0 = tc::make_sdesc(sB_addr + (uint32_t)stage * nch * box_bytes, kCHB);
-          const uint32_t dt = tmem_base + acc_col0 + (uint32_t)acc * kN;
-          constexpr int kSteps = d * kEsz / 32;          // one MMA per 32 bytes of K (K16 f16, K32 i8)
-          const int nk = (a.flags & 64) ? 1 : kSteps;   // probe: one K step per tile (no tensor-pipe bound)
 #pragma unroll
-          for (int kk = 0; kk < kSteps; ++kk) {
-            if (kk >= nk) break;
-            // K step kk: box (32 kk) / kCHB, byte offset (32 kk) % kCHB inside the swizzled row;
-            // A: 32 bytes of K = 8 TMEM columns
-            const uint32_t off16 = (((uint32_t)((kk * 32) / kCHB) * box_bytes) + (uint32_t)((kk * 32) % kCHB)) >> 4;
-            if (kI8)
-              tc::mma_i8_ts(dt, at + (uint32_t)kk * 8u, bd0 + off16, idesc, kk > 0 ? 1u : 0u);
-            else
-              tc::mma_f16_ts(dt, at + (uint32_t)kk * 8u, bd0 + off16, idesc, kk > 0 ? 1u : 0u);
+        for (int hh = 0; hh < kHalves; ++hh) {
+#if defined(LV_MMA_SPIN)
+          tc::mbar_wait(acc_empty + acc, acc_phase ^ 1);
+          if (hh == 0) tc::mbar_wait(b_full + stage, phase);
+#else
+          tc::mbar_wait_sleep(acc_empty + acc, acc_phase ^ 1);
+          if (hh == 0) tc::mbar_wait_sleep(b_full + stage, phase);
+#endif
+          tc::tc_fence_after();
+          if (issuer) {
+            // rows [hh kAccN, (hh + 1) kAccN) of the tile: kAccN rows further into every box
+            const uint64_t bd0 =
+                tc::make_sdesc(sB_addr + (uint32_t)stage * nch * box_bytes + (uint32_t)(hh * kAccN * kCHB), kCHB);
+            const uint32_t dt = tmem_base + acc_col0 + (uint32_t)acc * kAccN;
+            constexpr int kSteps = d * kEsz / 32;          // one MMA per 32 bytes of K (K16 f16, K32 i8)
+            const int nk = (a.flags & 64) ? 1 : kSteps;   // probe: one K step per tile (no tensor-pipe bound)
+#pragma unroll
+            for (int kk = 0; kk < kSteps; ++kk) {
+              if (kk >= nk) break;
+              // K step kk: box (32 kk) / kCHB, byte offset (32 kk) % kCHB inside the swizzled row;
+              // A: 32 bytes of K = 8 TMEM columns
+              const uint32_t off16 = (((uint32_t)((kk * 32) / kCHB) * box_bytes) + (uint32_t)((kk * 32) % kCHB)) >> 4;
+              if (kI8)
+                tc::mma_i8_ts(dt, at + (uint32_t)kk * 8u, bd0 + off16, idesc, kk > 0 ? 1u : 0u);
+              else
+                tc::mma_f16_ts(dt, at + (uint32_t)kk * 8u, bd0 + off16, idesc, kk > 0 ? 1u : 0u);
+            }
+            tc::mma_commit(acc_full + acc);
+            if (hh + 1 == kHalves) tc::mma_commit(b_empty + stage);
           }
-          tc::mma_commit(b_empty + stage);
-          tc::mma_commit(acc_full + acc);
+          __syncwarp();
+          if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
         }
-        __syncwarp();
         if (++stage == a.stages) { stage = 0; phase ^= 1; }
-        if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else {
@@ -560,8 +582,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         int32_t my_id[kJV];
 #pragma unroll
         for (int h = 0; h < kJV; ++h) my_id[h] = (!kSample && a.perm) ? __ldg(a.perm + base_pos + 32 * h + lane) : 0;
-        const int accb = g % nacc;
-        tc::mbar_wait_sleep_u32(acc_full_u + 8u * (uint32_t)accb, (uint32_t)(g / nacc) & 1u);
+        // the job's accumulator buffer: buffers are used in order, kHalves per tile
+        const int qb = g * kHalves + (jh * kJobCols) / kAccN;
+        const int accb = qb % nacc;
+        const uint32_t acol = (uint32_t)((jh * kJobCols) % kAccN);   // column of the job in its buffer
+#if defined(LV_EPI_SLEEP)
+        tc::mbar_wait_sleep_u32(acc_full_u + 8u * (uint32_t)accb, (uint32_t)(qb / nacc) & 1u);
+#else
+        // spin (try_wait without a suspend hint): measured 1.5 % (cfg 2) / 4 % (cfg 3) faster than
+        // sleeping on the accumulator barrier (the wake-up is on the accumulator's critical path)
+        {
+          long long spins = 0;
+          while (!tc::mbar_try_wait_u32(acc_full_u + 8u * (uint32_t)accb, (uint32_t)(qb / nacc) & 1u))
+            if (++spins > (1ll << 31)) __trap();
+        }
+#endif
         tc::tc_fence_after();
         // the job's 32-column halves in turn: load, (mask), max, compare, rare hit path; the
         // accumulator is released after the last half's load
@@ -644,14 +679,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (hit) {
   #pragma unroll
               for (int j = 0; j < 8; ++j)
-                reinterpret_cast<float4*>(srows[lane])[j] =
-                    make_float4(score_of(v[4 * j]), score_of(v[4 * j + 1]), score_of(v[4 * j + 2]), score_of(v[4 * j + 3]));
+                reinterpret_cast<float4*>(srows[lane])[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             }
             __syncwarp();
             do {
               const int Lz = __ffs(hb) - 1;
               hb &= hb - 1u;
-              const float f = srows[Lz][lane];
+              float f = srows[Lz][lane];
+              if (kI8) {   // raw accumulator of row Lz: converted with row Lz's scale by the testing lane
+                const float qsz = __shfl_sync(0xffffffffu, qs, Lz);
+                const int iv = __float_as_int(f);
+                f = iv == INT_MIN ? -FLT_MAX : qsz * (float)iv;
+              }
               const float tsz = __shfl_sync(0xffffffffu, ts, Lz);
               uint64_t tkz = __shfl_sync(0xffffffffu, tk, Lz);
               int cz = __shfl_sync(0xffffffffu, cnt, Lz);
@@ -684,8 +723,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (kJV == 2) {
           // both halves loaded before one wait (the second load's latency hides behind the first's)
           float v0[32], v1[32];
-          tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kN + (uint32_t)(jh * kJobCols), v0);
-          tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kN + (uint32_t)(jh * kJobCols + 32), v1);
+          tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kAccN + acol, v0);
+          tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kAccN + acol + 32u, v1);
           tc::tmem_wait_ld();
           tc::tc_fence_before();
           __syncwarp();
@@ -700,7 +739,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int h = 0; h < kJV; ++h) {
             float v[32];
-            tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kN + (uint32_t)(jh * kJobCols + 32 * h), v);
+            tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kAccN + acol + (uint32_t)(32 * h), v);
             tc::tmem_wait_ld();
             if (h + 1 == kJV) {
               tc::tc_fence_before();

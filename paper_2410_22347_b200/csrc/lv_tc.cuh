@@ -78,6 +78,15 @@ LV_TC_INL void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
 LV_TC_INL void mbar_arrive_u32(uint32_t bar) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(bar) : "memory");
 }
+LV_TC_INL bool mbar_try_wait_u32(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 LV_TC_INL void mbar_wait_sleep_u32(uint32_t bar, uint32_t parity) {
   long long spins = 0;
   for (;;) {
