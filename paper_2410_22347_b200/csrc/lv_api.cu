@@ -989,7 +989,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
   }
   unsigned long long*& dstats = ix->dbg_stats;   // debug counters (LV_DEBUG_SCAN_FLAGS & 2), owned by the index
   sa.stats = nullptr;
-  if (sa.flags & 2) {
+  if (sa.flags & (2 | 128)) {
     if (!dstats) LV_CUDA(cudaMalloc(&dstats, 8 * sizeof(unsigned long long)));
     sa.stats = dstats;
   }
@@ -1015,8 +1015,16 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
         const int32_t* ci = host_chunks.data() + lv::kChunkInts * c;
         tiles += (ci[1] - ci[0] + ci[3] - 1) / ci[3];
       }
-      fprintf(stderr, "[lv] %s: P=%d tiles=%lld grid=%d hit_warp_tiles=%llu appends=%llu compactions=%llu wait_spins=%llu\n",
-              what, sa.P, (long long)tiles, grid, h[0], h[1], h[2], h[3]);
+      if (sa.flags & 128)
+        fprintf(stderr,
+                "[lv] %s: P=%d tiles=%lld grid=%d per MMA-tile cycles: wait acc_empty+b_full %.1f, issue->next %.1f "
+                "(tiles %llu); per epilogue job: wait acc_full %.1f, total %.1f (jobs %llu); hit paths %llu "
+                "(%.3f per job) of %.1f cycles each\n",
+                what, sa.P, (long long)tiles, grid, (double)h[0] / h[5], (double)h[4] / h[5], h[5],
+                (double)h[2] / h[6], (double)h[7] / h[6], h[6], h[1], (double)h[1] / h[6], (double)h[3] / (h[1] ? h[1] : 1));
+      else
+        fprintf(stderr, "[lv] %s: P=%d tiles=%lld grid=%d hit_warp_tiles=%llu appends=%llu compactions=%llu wait_spins=%llu\n",
+                what, sa.P, (long long)tiles, grid, h[0], h[1], h[2], h[3]);
     }
     return LV_OK;
   };

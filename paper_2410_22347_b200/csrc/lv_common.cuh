@@ -9,6 +9,25 @@
 
 #define LV_DEVINL __device__ __forceinline__
 
+// Device-side bounds checks of the debug build (-DLV_CHECKS, tools/checks_build.sh): a failed check
+// prints its site and traps.  compute-sanitizer is closed on the GPU pool, so these asserts are the
+// memory-safety evidence.  Compiled out otherwise.
+#if defined(LV_CHECKS)
+#include <cstdio>
+#define LV_CHECK(cond)                                                                              \
+  do {                                                                                              \
+    if (!(cond)) {                                                                                  \
+      printf("LV_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__,      \
+             (int)blockIdx.x, (int)threadIdx.x);                                                    \
+      __trap();                                                                                     \
+    }                                                                                               \
+  } while (0)
+#else
+#define LV_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 namespace lv {
 
 // Storage conversions: RNE from fp32 (cuda_bf16/cuda_fp16 intrinsics are round-to-nearest-even).

@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(kSelW * 32) k_select_topr(const RerankArgs a) 
   const int total = tot0 + __shfl_sync(0xffffffffu, e1, 31);
   e0 -= c0;                  // exclusive offsets
   e1 = tot0 + e1 - c1;
+  LV_CHECK(c0 >= 0 && c0 <= a.Cap && c1 >= 0 && c1 <= a.Cap && r < a.m_pad);
   if (a.checked && total < a.R) {
     if (lane == 0) {
       a.fail_list[atomicAdd(a.fail_count, 1)] = q;
@@ -352,7 +353,9 @@ __global__ void __launch_bounds__(128) k_rerank_topk(const RerankArgs a) {
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         id[g] = i0 + g < R ? ids[i0 + g] : ids[i0];
+        LV_CHECK(id[g] >= 0);
         const int64_t xrow = a.row_of_id ? __ldg(a.row_of_id + id[g]) : id[g];
+        LV_CHECK(xrow >= 0);
         const uint4* row = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(a.X) + (size_t)xrow * rowbytes);
 #pragma unroll
         for (int j = 0; j < kVPL; ++j) {

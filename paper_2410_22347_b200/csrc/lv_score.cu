@@ -51,18 +51,14 @@ constexpr int kUQ = 4;                 // work-unit queue depth (dynamic unit or
 __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
 // TMEM: the A operand (one 128-query tile, d * esz / 4 columns per buffer) then NACC fp32 / s32
-// accumulator buffers of kAccN = 128 columns (one database tile).  LV_HALF_ACC (experiment build)
-// makes a buffer half a tile (two N = 64 MMAs per tile, one 64-column job per buffer): measured
-// slower (cfg 2 main scan 2.37 vs 2.15 ms; an N = 64 tcgen05.mma costs about as long as an N = 128
-// one, so the tile's MMA time doubles).  A is double-buffered across work units (the next unit's A is written while
+// accumulator buffers of kAccN = 128 columns (one database tile).  Half-tile buffers (two N = 64
+// MMAs per tile, one 64-column job per buffer) were measured slower (cfg 2 main scan 2.37 vs
+// 2.15 ms: an N = 64 tcgen05.mma costs about as long as an N = 128 one); the buffer arithmetic
+// below keeps kAccN general.  A is double-buffered across work units (the next unit's A is written while
 // the current one runs) unless that would leave too few accumulators: then A is single-buffered
 // and rewritten after each unit (one short bubble per unit, units are long at those sizes).
 constexpr int kTileN = 128;
-#if defined(LV_HALF_ACC)
-constexpr int kAccN = 64, kMinAcc = 5;
-#else
-constexpr int kAccN = 128, kMinAcc = 3;
-#endif
+constexpr int kAccN = 128, kMinAcc = 3;   // accumulator buffer = one tile (see above)
 // esz = bytes per reduced element (2: bf16/fp16, 1: int8); an A buffer takes d * esz / 4 columns
 __host__ __device__ constexpr bool score_single_a(int d, int esz = 2) { return (512 - d * esz / 2) / kAccN < kMinAcc; }
 __host__ __device__ constexpr int score_a_cols(int d, int esz = 2) {
@@ -296,6 +292,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nunits = a.P * QT;
   const bool skip_topr = (a.flags & 1) != 0;
   const bool count_stats = (a.flags & 2) != 0 && a.stats != nullptr;
+  // probe (flag 128, with stats): clock64 cycle attribution per warp role
+#if defined(LV_CLK_STATS)
+  const bool clk_stats = (a.flags & 128) != 0 && a.stats != nullptr;
+#else
+  constexpr bool clk_stats = false;   // the probe is an experiment build (-DLV_CLK_STATS)
+#endif
   const bool fast_only = (a.flags & 4) != 0;   // debug: detect hits but drop them (fast-path cost probe)
   const bool fine_blocks = (a.flags & 8) != 0;  // sample stage: 32-row block maxima
 
@@ -400,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     int i = 0;
     const bool issuer = tc::elect_one();   // the single lane that issues tcgen05.mma / commit
+    unsigned long long ck[3] = {0ull, 0ull, 0ull}, ntiles_ck = 0ull;   // clock probe (LV_CLK_STATS)
     for (;; ++i) {
       const int u = unit_at(i);
       unit_release(i);
@@ -412,15 +415,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tc_fence_after();
       const uint32_t at = tmem_base + (kSingleA ? 0u : (uint32_t)(i & 1) * kACols);
       for (int t = t0; t < t1; t += ts_) {
+        long long c0 = clk_stats ? clock64() : 0;
 #pragma unroll
         for (int hh = 0; hh < kHalves; ++hh) {
-#if defined(LV_MMA_SPIN)
-          tc::mbar_wait(acc_empty + acc, acc_phase ^ 1);
-          if (hh == 0) tc::mbar_wait(b_full + stage, phase);
-#else
           tc::mbar_wait_sleep(acc_empty + acc, acc_phase ^ 1);
+          long long c1 = clk_stats ? clock64() : 0;
           if (hh == 0) tc::mbar_wait_sleep(b_full + stage, phase);
-#endif
+          if (clk_stats) {
+            const long long c2 = clock64();
+            ck[0] += (unsigned long long)(c1 - c0);
+            ck[1] += (unsigned long long)(c2 - c1);
+            c0 = c2;
+          }
+
           tc::tc_fence_after();
           if (issuer) {
             // rows [hh kAccN, (hh + 1) kAccN) of the tile: kAccN rows further into every box
@@ -444,10 +451,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (hh + 1 == kHalves) tc::mma_commit(b_empty + stage);
           }
           __syncwarp();
+          if (clk_stats) {
+            ck[2] += (unsigned long long)(clock64() - c0);
+            ++ntiles_ck;
+          }
           if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
         }
         if (++stage == a.stages) { stage = 0; phase ^= 1; }
       }
+    }
+    if (clk_stats && lane == 0) {
+      atomicAdd(a.stats + 0, ck[0]);
+      atomicAdd(a.stats + 4, ck[2]);
+      atomicAdd(a.stats + 5, ntiles_ck);
     }
   } else {
     // ------------------------------------------------------------ epilogue: 16 warps
@@ -510,6 +526,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(a_full + b);
     };
+    unsigned long long ek[3] = {0ull, 0ull, 0ull}, njobs_ck = 0ull;   // clock probe (LV_CLK_STATS)
+    unsigned long long ek_hit = 0ull, n_hit = 0ull;
     int u_next = unit_at(0);   // the unit after the current one (its A operand goes in early)
     if (u_next < nunits) write_A(u_next, 0);
     const uint32_t tm_lane = tmem_base + lane_base + acc_col0;
@@ -553,7 +571,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lists) tc::named_bar_sync(1, kEpiThreads);
       const int my_slot = lists ? S.slot : 0;
       const size_t si = (size_t)(my_slot * 4 + cq) * a.m_pad + q;   // this thread's sub-list
+      LV_CHECK(!lists || (my_slot >= 0 && my_slot < a.NS && q < a.m_pad));
       int cnt = lists ? a.cnt[si] : 0;
+      LV_CHECK(cnt >= 0 && cnt <= a.Cap);
       uint64_t tk = lists ? a.tau[si] : 0ull;
       float ts = qvalid ? thr_score(tk) : FLT_MAX;   // padded queries never hit
       // int8: this query's scale for the unit's cluster view, and the threshold on accumulators
@@ -582,21 +602,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         int32_t my_id[kJV];
 #pragma unroll
         for (int h = 0; h < kJV; ++h) my_id[h] = (!kSample && a.perm) ? __ldg(a.perm + base_pos + 32 * h + lane) : 0;
+        LV_CHECK(t >= t0 && t < t1 && (int64_t)(base_pos + kJobCols) <= a.n_pad);
         // the job's accumulator buffer: buffers are used in order, kHalves per tile
         const int qb = g * kHalves + (jh * kJobCols) / kAccN;
         const int accb = qb % nacc;
         const uint32_t acol = (uint32_t)((jh * kJobCols) % kAccN);   // column of the job in its buffer
+        const long long e0 = clk_stats ? clock64() : 0;
 #if defined(LV_EPI_SLEEP)
         tc::mbar_wait_sleep_u32(acc_full_u + 8u * (uint32_t)accb, (uint32_t)(qb / nacc) & 1u);
 #else
         // spin (try_wait without a suspend hint): measured 1.5 % (cfg 2) / 4 % (cfg 3) faster than
         // sleeping on the accumulator barrier (the wake-up is on the accumulator's critical path)
         {
-          long long spins = 0;
+          uint32_t spins = 0;   // try_wait blocks for a bounded time per call; 2^30 calls = a lost arrive
           while (!tc::mbar_try_wait_u32(acc_full_u + 8u * (uint32_t)accb, (uint32_t)(qb / nacc) & 1u))
-            if (++spins > (1ll << 31)) __trap();
+            if (++spins > (1u << 30)) __trap();
         }
 #endif
+        const long long e1 = clk_stats ? clock64() : 0;
         tc::tc_fence_after();
         // the job's 32-column halves in turn: load, (mask), max, compare, rare hit path; the
         // accumulator is released after the last half's load
@@ -622,6 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (a.raw != nullptr) {
   #pragma unroll
               for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + hpos + j] = score_of(v[j]);
+              LV_CHECK(q < a.m_pad && (int64_t)(hpos + 32) <= a.n_pad);
             }
             float mx;
             bool hit;
@@ -638,20 +662,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               mx = im == INT_MIN ? -FLT_MAX : qs * (float)im;
               hit = im >= ti && im > INT_MIN;
             } else {
-#if defined(LV_EPI_TREE)
-              float t16[16];
-  #pragma unroll
-              for (int j = 0; j < 16; ++j) t16[j] = fmaxf(v[j], v[j + 16]);
-  #pragma unroll
-              for (int w = 8; w >= 1; w >>= 1)
-  #pragma unroll
-                for (int j = 0; j < w; ++j) t16[j] = fmaxf(t16[j], t16[j + w]);
-              mx = t16[0];
-#else
               mx = v[0];
   #pragma unroll
               for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
-#endif
+
               hit = mx >= ts && mx > -FLT_MAX;
             }
             if (kSample) {
@@ -675,7 +689,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             // hit path (divergence-free): each hitting lane's 32 scores are broadcast through shared
             // memory, lane j tests column j, survivors are appended to the hitting lane's sub-list
             // with coalesced stores
+            const long long hc0 = clk_stats ? clock64() : 0;
             const int32_t id_h = (a.perm ? my_id[h] : hpos + lane);
+
             if (hit) {
   #pragma unroll
               for (int j = 0; j < 8; ++j)
@@ -713,34 +729,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 keep = keep && key > tkz;
                 kb = __ballot_sync(0xffffffffu, keep);
               }
+              LV_CHECK(cz + __popc(kb) <= a.Cap);
               if (keep) bz[cz + __popc(kb & lt)] = key;
               if (lane == Lz) cnt = cz + __popc(kb);
               if (count_stats && lane == 0) atomicAdd(a.stats + 1, (unsigned long long)__popc(kb));
             } while (hb != 0u);
             __syncwarp();
+            if (clk_stats) {
+              ek_hit += (unsigned long long)(clock64() - hc0);
+              ++n_hit;
+            }
         };
-#if defined(LV_EPI_DUAL)
-        if constexpr (kJV == 2) {
-          // both halves loaded before one wait (the second load's latency hides behind the first's)
-          float v0[32], v1[32];
-          tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kAccN + acol, v0);
-          tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kAccN + acol + 32u, v1);
-          tc::tmem_wait_ld();
-          tc::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
-          if (!skip_topr) {
-            half(v0, 0);
-            half(v1, 1);
-          }
-        } else
-#endif
         {
+          long long eld = 0;
 #pragma unroll
           for (int h = 0; h < kJV; ++h) {
             float v[32];
+            const long long l0 = clk_stats ? clock64() : 0;
             tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kAccN + acol + (uint32_t)(32 * h), v);
             tc::tmem_wait_ld();
+            if (clk_stats) eld += clock64() - l0;
             if (h + 1 == kJV) {
               tc::tc_fence_before();
               __syncwarp();
@@ -749,6 +757,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (skip_topr) continue;
             half(v, h);
           }
+          if (clk_stats) {
+            ek[0] += (unsigned long long)(e1 - e0);
+            ek[1] += (unsigned long long)eld;
+            ek[2] += (unsigned long long)(clock64() - e0);
+            ++njobs_ck;
+          }
         }
       }
       tiles_before += n_t;
@@ -756,6 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // this unit's A buffer before any warp overwrites it (write_A of unit u + 2 at the next
       // iteration); in the main stage the sub-list states go back to the slot, which is released
       if (lists && qvalid) {
+        LV_CHECK(cnt >= 0 && cnt <= a.Cap);
         a.cnt[si] = cnt;
         a.tau[si] = tk;
       }
@@ -769,6 +784,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       // single-buffered A: every job of this unit saw its tile committed, so the MMAs of this unit
       // are complete and its A buffer can take the next unit's operand
       if (kSingleA && u_next < nunits) write_A(u_next, 0);
+    }
+    if (clk_stats && lane == 0) {
+      atomicAdd(a.stats + 2, ek[0]);
+      atomicAdd(a.stats + 3, ek_hit);
+      atomicAdd(a.stats + 1, n_hit);
+      atomicAdd(a.stats + 6, njobs_ck);
+      atomicAdd(a.stats + 7, ek[2]);
     }
   }
   tc::tc_fence_before();
