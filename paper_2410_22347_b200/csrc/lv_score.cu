@@ -625,13 +625,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // accumulator is released after the last half's load
         float bm = -FLT_MAX;   // sample stage: running block maximum of the job
         // one 32-column half of the job: (mask), raw output, max, threshold test, rare hit path
-        // one 32-column half of the job, in two parts.  detect: (mask), raw output, max, threshold
-        // test, ballot; with `stage` the hitting lanes also copy their 32 scores to the warp's
-        // shared-memory rows.  process: the hit path on the staged rows (lane j tests column j of
-        // each hitting row; survivors appended to that row's sub-list with coalesced stores).
-        auto detect = [&](float (&v)[32], const int h, const bool stage, bool& hit) -> uint32_t {
-            hit = false;
-            if (skip_topr) return 0u;
+        auto half = [&](float (&v)[32], const int h) {
+            if (skip_topr) return;
             const int hpos = base_pos + 32 * h;
             if (t == t_last) {   // a cluster segment's last tile may be partial
               const int tv = a.tile_valid[t_last] - (jh * kJobCols + 32 * h);
@@ -641,19 +636,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                   if (j >= tv) v[j] = kI8 ? __int_as_float(INT_MIN) : -FLT_MAX;
               }
             }
+            // int8: v holds s32 accumulators; the score of column j is fl(qs * float(acc_j))
+            auto score_of = [&](float raw) -> float {
+              if (!kI8) return raw;
+              const int iv = __float_as_int(raw);
+              return iv == INT_MIN ? -FLT_MAX : qs * (float)iv;
+            };
             if (a.raw != nullptr) {
   #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                float f = v[j];
-                if (kI8) {   // int8: v holds s32 accumulators; the score is fl(qs * float(acc))
-                  const int iv = __float_as_int(f);
-                  f = iv == INT_MIN ? -FLT_MAX : qs * (float)iv;
-                }
-                a.raw[(size_t)q * a.n_pad + hpos + j] = f;
-              }
+              for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + hpos + j] = score_of(v[j]);
               LV_CHECK(q < a.m_pad && (int64_t)(hpos + 32) <= a.n_pad);
             }
             float mx;
+            bool hit;
             if (kI8) {
               // tree of integer maxima (a 31-deep dependent chain would expose its latency)
               int t16[16];
@@ -670,6 +665,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               mx = v[0];
   #pragma unroll
               for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
+
               hit = mx >= ts && mx > -FLT_MAX;
             }
             if (kSample) {
@@ -683,30 +679,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bm = fmaxf(bm, mx);
                 if (h + 1 == kJV) a.bmax[(size_t)sblk * a.m_pad + q] = bm;
               }
-              hit = false;
-              return 0u;
+              return;
             }
-            const uint32_t hb = __ballot_sync(0xffffffffu, hit);
-            if (hb == 0u) return 0u;
+
+            uint32_t hb = __ballot_sync(0xffffffffu, hit);
+            if (hb == 0u) return;
             if (count_stats && lane == 0) atomicAdd(a.stats + 0, 1ull);
-            if (fast_only) return 0u;
-            if (stage && hit) {
-  #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                reinterpret_cast<float4*>(srows[lane])[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            }
-            return hb;
-        };
-        auto stage_rows = [&](const float (&v)[32], const bool hit) {
+            if (fast_only) return;
+            // hit path (divergence-free): each hitting lane's 32 scores are broadcast through shared
+            // memory, lane j tests column j, survivors are appended to the hitting lane's sub-list
+            // with coalesced stores
+            const long long hc0 = clk_stats ? clock64() : 0;
+            const int32_t id_h = (a.perm ? my_id[h] : hpos + lane);
+
             if (hit) {
   #pragma unroll
               for (int j = 0; j < 8; ++j)
                 reinterpret_cast<float4*>(srows[lane])[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             }
-        };
-        auto process = [&](uint32_t hb, const int h) {
-            const long long hc0 = clk_stats ? clock64() : 0;
-            const int32_t id_h = (a.perm ? my_id[h] : base_pos + 32 * h + lane);
             __syncwarp();
             do {
               const int Lz = __ffs(hb) - 1;
@@ -752,50 +742,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         {
           long long eld = 0;
-#if defined(LV_EPI_SPLIT)
-          constexpr bool kSplit = kJV == 2;
-#else
-          constexpr bool kSplit = false;
-#endif
-          if constexpr (kSplit) {
-            // half 0 is detected (its hitting rows staged) before half 1 is loaded, and the
-            // accumulator is released right after half 1's load: both halves' hit paths run after
-            // the release, off the MMA's critical path
+#pragma unroll
+          for (int h = 0; h < kJV; ++h) {
             float v[32];
-            bool hit0, hit1;
             const long long l0 = clk_stats ? clock64() : 0;
-            tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kAccN + acol, v);
-            tc::tmem_wait_ld();
-            const uint32_t hb0 = detect(v, 0, true, hit0);
-            tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kAccN + acol + 32u, v);
+            tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kAccN + acol + (uint32_t)(32 * h), v);
             tc::tmem_wait_ld();
             if (clk_stats) eld += clock64() - l0;
-            tc::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
-            const uint32_t hb1 = detect(v, 1, false, hit1);
-            if (hb0) process(hb0, 0);
-            if (hb1) {
-              stage_rows(v, hit1);
-              process(hb1, 1);
+            if (h + 1 == kJV) {
+              tc::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
             }
-          } else {
-#pragma unroll
-            for (int h = 0; h < kJV; ++h) {
-              float v[32];
-              bool hit;
-              const long long l0 = clk_stats ? clock64() : 0;
-              tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kAccN + acol + (uint32_t)(32 * h), v);
-              tc::tmem_wait_ld();
-              if (clk_stats) eld += clock64() - l0;
-              if (h + 1 == kJV) {
-                tc::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
-              }
-              const uint32_t hb = detect(v, h, true, hit);
-              if (hb) process(hb, h);
-            }
+            if (skip_topr) continue;
+            half(v, h);
           }
           if (clk_stats) {
             ek[0] += (unsigned long long)(e1 - e0);

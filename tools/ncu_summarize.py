@@ -93,6 +93,7 @@ def main():
     ap.add_argument("--rep")
     ap.add_argument("--launches")
     ap.add_argument("--tag", default="r01")
+    ap.add_argument("--key", default=None, help="ncu_traffic.json key (default cfg<cfg>; e.g. cfg2_i8)")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles"), help="output directory (on a GPU box: under gpurun_out/)")
     a = ap.parse_args()
     prof = a.out
@@ -100,10 +101,11 @@ def main():
     traffic_path = os.path.join(prof, "ncu_traffic.json")
     seed = traffic_path if os.path.exists(traffic_path) else os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(seed)) if os.path.exists(seed) else {}
-    t = traffic.setdefault(f"cfg{a.cfg}", {})
+    key = a.key or f"cfg{a.cfg}"
+    t = traffic.setdefault(key, {})
     if a.rep:
         ks = summarize_rep(a.rep)
-        json.dump({"source": os.path.basename(a.rep), "kernels": ks}, open(os.path.join(prof, f"{a.tag}_ncu_cfg{a.cfg}.json"), "w"), indent=1)
+        json.dump({"source": os.path.basename(a.rep), "kernels": ks}, open(os.path.join(prof, f"{a.tag}_ncu_{key}.json"), "w"), indent=1)
         scans = [k for k in ks if k["kernel"].startswith("k_score_topr")]
         if scans:
             main_scan = max(scans, key=lambda k: k.get("duration_ms", 0))
@@ -116,7 +118,7 @@ def main():
             print(k)
     if a.launches:
         s = summarize_launches(a.launches)
-        json.dump(s, open(os.path.join(prof, f"{a.tag}_launches_cfg{a.cfg}.json"), "w"), indent=1)
+        json.dump(s, open(os.path.join(prof, f"{a.tag}_launches_{key}.json"), "w"), indent=1)
         for x in s["launches"]:
             print(x)
     json.dump(traffic, open(traffic_path, "w"), indent=1)
