@@ -178,3 +178,53 @@ def test_i8_search_parity(lv, cfg_id, n, m, d, C, R):
     dbg = check_i8_search(lv, ix, c, X, Q, A32, B32, assign, C, R, 10)
     if n >= 200_000:
         assert dbg["path"] == 1
+
+
+@pytest.mark.slow
+def test_i8_fullsize_cfg2_sampled(lv):
+    """The int8 scan at configuration 2's full size (1M x 512, d = 128, R = 100, m = 10 000 searched
+    in one call, as bench.py --config 2 --low i8 times it); gates on 256 evenly spaced queries:
+    strict G2 against the GPU's own codes, G3 / G5 against the oracle's int8 search of the full
+    database with code-flip bands, G4 and G6."""
+    c = lvgen.get_config(2)
+    X = lvgen.database(c)
+    Q = lvgen.queries(c, "test")
+    Ql = lvgen.queries(c, "learn")
+    f = O.sphering_fit(Ql, X[lvgen.learn_rows(c)].astype(np.float64), c.d)
+    A32, B32 = f["A"][None].astype(np.float32), f["B"][None].astype(np.float32)
+    ix = _index(lv, c, X, A32, B32, None, 1)
+    Qt = torch.from_numpy(Q).cuda()
+    ids, sc, dbg = lv.lv_search(ix, Qt, c.k, c.R, cand=True)
+    assert dbg["path"] == 1
+    sel = np.linspace(0, Q.shape[0] - 1, 256).astype(np.int64)
+    ids = ids.cpu().numpy()[sel].astype(np.int64)
+    sc = sc.cpu().numpy()[sel].astype(np.float64)
+    cid = dbg["cand_ids"].cpu().numpy()[sel].astype(np.int64)
+    csc = dbg["cand_scores"].cpu().numpy()[sel]
+    Qs = Q[sel]
+    xc, delta = _gpu_codes(lv, ix, c, 1)
+    qc, qs = lv.lv_project_queries_i8(ix, torch.from_numpy(Qs).cuda())
+    qc = qc.cpu().numpy().astype(np.int64)
+    qs = qs.cpu().numpy()[:, 0]
+    for j in range(len(sel)):
+        dots = xc[cid[j]].astype(np.int64) @ qc[j]
+        assert np.array_equal(csc[j], (qs[j] * dots.astype(np.float32)).astype(np.float32)), j
+    ref = O.search_i8(Qs, X, A32[0], B32[0], None, c.R, c.k)
+    S = O.reduced_scores(ref["Qeff"], ref["x_codes"].astype(np.float64)).astype(np.float32).astype(np.float64)
+    for j in range(len(sel)):
+        thr = ref["cand_scores"][j, -1]
+        band = TOL_RED * max(abs(thr), 1e-2) + 4 * 127 * float(ref["q_scales"][j].max())
+        for i in set(cid[j].tolist()) ^ set(ref["cand"][j].tolist()):
+            assert abs(S[j, i] - thr) <= band, (j, i)
+    check_topk_order(ids, sc)
+    ex = np.einsum("md,mkd->mk", Qs.astype(np.float64), X[ids].astype(np.float64))
+    assert (np.abs(sc - ex) <= TOL_RR * np.maximum(np.abs(ex), 1e-2)).all()
+    for j in range(len(sel)):
+        if not np.array_equal(ids[j], ref["ids"][j]):
+            kth, thr = ref["scores"][j, -1], ref["cand_scores"][j, -1]
+            band = TOL_RED * max(abs(thr), 1e-2) + 4 * 127 * float(ref["q_scales"][j].max())
+            for i in set(ids[j].tolist()) ^ set(ref["ids"][j].tolist()):
+                rr = float(Qs[j].astype(np.float64) @ X[i].astype(np.float64))
+                assert abs(rr - kth) <= TOL_RR * max(abs(kth), 1e-2) or abs(S[j, i] - thr) <= band, (j, i)
+    gt, _ = O.exact_topk(Qs, X, 10)
+    assert abs(O.recall_at_k(ids, gt, 10) - O.recall_at_k(ref["ids"], gt, 10)) <= 1e-3 + 1e-12
