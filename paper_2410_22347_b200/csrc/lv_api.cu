@@ -860,7 +860,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
     const size_t mp = pl.m_pad;
     size_t need = (mp * Cd * 2 + 256) + ((size_t)3 * mp * ix->Kp * 2 + 256) + ((size_t)NS2 * mp * pl.Cap * 8 + 256) +
                   ((size_t)NS2 * mp * 4 + 256) +
-                  ((size_t)NS2 * mp * 8 + 256) + ((size_t)pl.QP * 4 + 256) + (16 * 4 + 256) + (kMaxScans * 4 + 256) +
+                  ((size_t)NS2 * mp * 8 + 256) + ((size_t)pl.QP * 16 + 256) + (16 * 4 + 256) + (kMaxScans * 4 + 256) +
                   (mp * (size_t)R * 4 + 256) + (mp * 4 + 256) +
                   (nchunk_ints * 4 + 256 * (pl.chunks.size() + 2));
     if (pl.sampled)
@@ -884,7 +884,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
     pc.zero_lo = p;
     pc.cnt = carve<int32_t>(p, (size_t)NS2 * mp);
     pc.tau = carve<uint64_t>(p, (size_t)NS2 * mp);
-    pc.slot_busy = carve<int32_t>(p, (size_t)pl.QP);
+    pc.slot_busy = carve<int32_t>(p, (size_t)pl.QP * 4);   // [QP][2] 64-bit sub-list masks (one per query half)
     pc.sel_ids = carve<int32_t>(p, mp * (size_t)R);
     pc.sel_n = carve<int32_t>(p, mp);
     pc.fail = carve<int32_t>(p, 16);
@@ -969,7 +969,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
   sa.QP = pl.QP;
   sa.d = ix->ds;
   sa.R = R;
-  sa.NS = pl.NS;
+  sa.NS = NS2;   // the scan claims single sub-lists (64-bit masks per query tile and half)
   sa.Cap = pl.Cap;
   sa.stages = pl.stages;
   sa.tile_valid = ix->tile_valid;
@@ -990,7 +990,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
   unsigned long long*& dstats = ix->dbg_stats;   // debug counters (LV_DEBUG_SCAN_FLAGS & 2), owned by the index
   sa.stats = nullptr;
   if (sa.flags & (2 | 128)) {
-    if (!dstats) LV_CUDA(cudaMalloc(&dstats, 8 * sizeof(unsigned long long)));
+    if (!dstats) LV_CUDA(cudaMalloc(&dstats, 16 * sizeof(unsigned long long)));
     sa.stats = dstats;
   }
   int nscan = 0;
@@ -1003,11 +1003,11 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
     // dynamic unit order (LV_DYN_UNITS, default on): a fresh zeroed counter per launch
     sa.unit_ctr = (dyn_units && nscan < kMaxScans) ? pc.unit_ctr + nscan : nullptr;
     ++nscan;
-    if (sa.stats) LV_CUDA(cudaMemsetAsync(sa.stats, 0, 8 * sizeof(unsigned long long), s));
+    if (sa.stats) LV_CUDA(cudaMemsetAsync(sa.stats, 0, 16 * sizeof(unsigned long long), s));
     LV_CUDA(lv::launch_score(&ix->tmap_xlow_s, sa, ix->fmt(), grid, pl.smem, s));
     ++launches;
     if (sa.stats) {
-      unsigned long long h[8];
+      unsigned long long h[16];
       LV_CUDA(cudaMemcpyAsync(h, sa.stats, sizeof h, cudaMemcpyDeviceToHost, s));
       LV_CUDA(cudaStreamSynchronize(s));
       int64_t tiles = 0;
@@ -1018,10 +1018,16 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
       if (sa.flags & 128)
         fprintf(stderr,
                 "[lv] %s: P=%d tiles=%lld grid=%d per MMA-tile cycles: wait acc_empty+b_full %.1f, issue->next %.1f "
-                "(tiles %llu); per epilogue job: wait acc_full %.1f, total %.1f (jobs %llu); hit paths %llu "
+                "(tiles %llu); per epilogue job: wait acc_full %.1f, total %.1f (jobs %llu); append entries %llu "
                 "(%.3f per job) of %.1f cycles each\n",
                 what, sa.P, (long long)tiles, grid, (double)h[0] / h[5], (double)h[4] / h[5], h[5],
                 (double)h[2] / h[6], (double)h[7] / h[6], h[6], h[1], (double)h[1] / h[6], (double)h[3] / (h[1] ? h[1] : 1));
+      if (sa.flags & 128)
+        fprintf(stderr,
+                "[lv] %s: append batches %llu, per batch: read %.1f, process %.1f cycles; pushes %llu of %.1f cycles "
+                "(room waits %.1f)\n",
+                what, h[8], (double)h[9] / (h[8] ? h[8] : 1), (double)h[10] / (h[8] ? h[8] : 1), h[11],
+                (double)h[12] / (h[11] ? h[11] : 1), (double)h[13] / (h[11] ? h[11] : 1));
       else
         fprintf(stderr, "[lv] %s: P=%d tiles=%lld grid=%d hit_warp_tiles=%llu appends=%llu compactions=%llu wait_spins=%llu\n",
                 what, sa.P, (long long)tiles, grid, h[0], h[1], h[2], h[3]);

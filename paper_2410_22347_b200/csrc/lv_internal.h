@@ -34,7 +34,7 @@ struct ScoreArgs {
   uint64_t* cand;              // [NS][m_pad][Cap]
   int32_t* cnt;                // [NS][m_pad]
   uint64_t* tau;               // [NS][m_pad]
-  int32_t* slot_busy;          // [QP] bitmask of claimed slots per query tile (zero between launches)
+  int32_t* slot_busy;          // [QP][2] 64-bit masks of claimed sub-lists per query tile and half (zero between launches)
   float* raw;                  // [m_pad][n_pad] or nullptr
   float* bmax;                 // sample stage: [n_sample_tiles * blocks_per_tile][m_pad] block maxima, else nullptr
   const int32_t* m_dev;        // device query count (repair passes; overrides m and QP), or nullptr

@@ -314,18 +314,23 @@ __global__ void __launch_bounds__(kSelW * 32) k_select_topr(const RerankArgs a) 
 }
 
 // K5: r_ji = <q_j, x_i> in fp32 for the R candidates of list row r (Alg. 1 line 3) and the
-// top-k by (r desc, id asc).  One warp per row; lane l holds the 16-byte vectors l, l + 32, ... of
-// q and of each database row; G rows are loaded before their FMAs (G * kVPL 16-byte loads in flight
-// per lane); candidate i's key lands in lane i % 32, slot i / 32; top-k by k warp-wide maxima.
+// top-k by (r desc, id asc).  One CTA of kRrWarps warps per row: warp w takes the groups of G
+// candidates g = w, w + kRrWarps, ...; lane l holds the 16-byte vectors l, l + 32, ... of q and of
+// each database row, the G rows of a group are loaded before their FMAs (G * kVPL 16-byte loads
+// in flight per lane).  Candidate i's key goes to shared memory; warp 0 then takes the top-k by k
+// warp-wide maxima.  A CTA per row (instead of a warp per row) keeps the grid ~17 waves deep at
+// m = 10^4, so the last wave's idle SMs cost little of this HBM-bound gather.
+constexpr int kRrWarps = 4;
 template <bool kF16, int kVPL>
-__global__ void __launch_bounds__(128) k_rerank_topk(const RerankArgs a) {
+__global__ void __launch_bounds__(kRrWarps * 32) k_rerank_topk(const RerankArgs a) {
   constexpr int vec = kF16 ? 8 : 4;
   // rows in flight per warp (G * kVPL 16-byte loads per lane): 4 for up to 4 vectors per lane
   // (cfg 5's fp16 rows: select + re-rank phase 0.93 -> 0.85 ms against 2 rows), else 2
   constexpr int G = kVPL <= 4 ? 4 : 2;
   constexpr int kSlots = kMaxR / 32 > 8 ? 8 : kMaxR / 32;   // R <= 256
+  __shared__ uint64_t s_key[kSlots * 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * 4 + warp;
+  const int r = blockIdx.x;
   const int mrows = a.m_dev ? *a.m_dev : a.m;
   if (r >= mrows) return;
   const int R = a.sel_n[r];
@@ -341,57 +346,56 @@ __global__ void __launch_bounds__(128) k_rerank_topk(const RerankArgs a) {
   }
   const int32_t* ids = a.sel_ids + (size_t)r * a.R;
   const size_t rowbytes = (size_t)a.D * (kF16 ? 2 : 4);
-  uint64_t kk[kSlots];
-#pragma unroll
-  for (int sl = 0; sl < kSlots; ++sl) {
-    kk[sl] = 0ull;
-    if (sl * 32 >= R) continue;
 #pragma unroll 1
-    for (int i0 = sl * 32; i0 < min(R, sl * 32 + 32); i0 += G) {
-      int32_t id[G];
-      uint4 u[G][kVPL];
+  for (int i0 = warp * G; i0 < R; i0 += kRrWarps * G) {
+    int32_t id[G];
+    uint4 u[G][kVPL];
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        id[g] = i0 + g < R ? ids[i0 + g] : ids[i0];
-        LV_CHECK(id[g] >= 0);
-        const int64_t xrow = a.row_of_id ? __ldg(a.row_of_id + id[g]) : id[g];
-        LV_CHECK(xrow >= 0);
-        const uint4* row = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(a.X) + (size_t)xrow * rowbytes);
+    for (int g = 0; g < G; ++g) {
+      id[g] = i0 + g < R ? ids[i0 + g] : ids[i0];
+      LV_CHECK(id[g] >= 0);
+      const int64_t xrow = a.row_of_id ? __ldg(a.row_of_id + id[g]) : id[g];
+      LV_CHECK(xrow >= 0);
+      const uint4* row = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(a.X) + (size_t)xrow * rowbytes);
 #pragma unroll
-        for (int j = 0; j < kVPL; ++j) {
-          const int v = lane + 32 * j;
-          u[g][j] = v < nvec ? __ldg(row + v) : make_uint4(0u, 0u, 0u, 0u);
-        }
-      }
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        float acc = 0.f;
-#pragma unroll
-        for (int j = 0; j < kVPL; ++j) {
-          if (kF16) {
-            const __half2* h = reinterpret_cast<const __half2*>(&u[g][j]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __half22float2(h[e]);
-              acc = fmaf(f.x, qv[j * 8 + 2 * e], acc);
-              acc = fmaf(f.y, qv[j * 8 + 2 * e + 1], acc);
-            }
-          } else {
-            const float4 f = *reinterpret_cast<const float4*>(&u[g][j]);
-            acc = fmaf(f.x, qv[j * 4 + 0], acc);
-            acc = fmaf(f.y, qv[j * 4 + 1], acc);
-            acc = fmaf(f.z, qv[j * 4 + 2], acc);
-            acc = fmaf(f.w, qv[j * 4 + 3], acc);
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        const int i = i0 + g;
-        if (i < R && lane == (i & 31)) kk[sl] = make_key(acc, id[g]);
+      for (int j = 0; j < kVPL; ++j) {
+        const int v = lane + 32 * j;
+        u[g][j] = v < nvec ? __ldg(row + v) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < kVPL; ++j) {
+        if (kF16) {
+          const __half2* h = reinterpret_cast<const __half2*>(&u[g][j]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __half22float2(h[e]);
+            acc = fmaf(f.x, qv[j * 8 + 2 * e], acc);
+            acc = fmaf(f.y, qv[j * 8 + 2 * e + 1], acc);
+          }
+        } else {
+          const float4 f = *reinterpret_cast<const float4*>(&u[g][j]);
+          acc = fmaf(f.x, qv[j * 4 + 0], acc);
+          acc = fmaf(f.y, qv[j * 4 + 1], acc);
+          acc = fmaf(f.z, qv[j * 4 + 2], acc);
+          acc = fmaf(f.w, qv[j * 4 + 3], acc);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      const int i = i0 + g;
+      if (i < R && lane == g) s_key[i] = make_key(acc, id[g]);
+    }
   }
-  // top-k: k rounds of a warp-wide maximum of the lanes' best keys
+  __syncthreads();
+  if (warp != 0) return;
+  // top-k: k rounds of a warp-wide maximum of the lanes' best keys (candidate i at lane i % 32)
+  uint64_t kk[kSlots];
+#pragma unroll
+  for (int sl = 0; sl < kSlots; ++sl) kk[sl] = sl * 32 + lane < R ? s_key[sl * 32 + lane] : 0ull;
   for (int t = 0; t < a.k; ++t) {
     uint64_t best = 0ull;
     int bs = -1;
@@ -429,8 +433,8 @@ cudaError_t launch_rerank_topk(const RerankArgs& a, cudaStream_t s) {
   const int vec = a.full_f16 ? 8 : 4;
   const int vpl = (a.D / vec + 31) / 32;
   if (a.R > 256 || vpl > 6 || a.D % vec) return cudaErrorInvalidValue;
-  const dim3 grid((unsigned)((a.m + 3) / 4));
-#define LV_RR(F, V) k_rerank_topk<F, V><<<grid, 128, 0, s>>>(a)
+  const dim3 grid((unsigned)a.m);
+#define LV_RR(F, V) k_rerank_topk<F, V><<<grid, kRrWarps * 32, 0, s>>>(a)
   if (a.full_f16) {
     if (vpl <= 1) LV_RR(true, 1); else if (vpl <= 2) LV_RR(true, 2); else if (vpl <= 3) LV_RR(true, 3);
     else if (vpl <= 4) LV_RR(true, 4); else LV_RR(true, 6);

@@ -24,22 +24,34 @@
 
 namespace lv {
 
-constexpr int kEpiWarps = 16;          // 4 per SM sub-partition (latency hiding of the hit path)
-// the producer warps get the highest ids: the warp scheduler favours high ids, so the
-// single-thread TMA/MMA issue loops are never starved by the epilogue warps
+constexpr int kEpiWarps = 16;          // 4 per SM sub-partition (one TMEM lane quarter each)
+// the producer warps get the next ids (SM sub-partitions 0 and 1), the two append warps the last
+// two (sub-partitions 2 and 3): 5 warps per sub-partition, the same 96-register budget as 18 warps
 constexpr int kTmaWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
-constexpr int kThreads = 32 * (kEpiWarps + 2);
+constexpr int kAppWarps = 2, kAppWarp0 = kEpiWarps + 2;
+constexpr int kThreads = 32 * (kEpiWarps + 2 + kAppWarps);
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kMaxKeysPerLane = 12;    // Cap <= 384
+constexpr int kRing = 64;              // entries per append ring (power of two, >= 32 + 1)
 
-
-// Shared-memory epilogue state.
+// Shared-memory epilogue state.  The fast-path warps (16) only filter: a 32 x 32 block of
+// (query, column) scores with a hitting query row is pushed, one entry per hitting row, into the
+// append ring of its query half (lane quarters 0, 2 -> ring 0; 1, 3 -> ring 1); the append warp
+// of the ring owns the candidate sub-lists of those 64 queries for the unit and appends the
+// survivors.  So the hit path never holds a fast-path warp.
 struct EpiShared {
-  float rows[kEpiWarps][32][32];       // hitting lanes' 32 scores (row = lane), read column-wise
-  int hist[kEpiWarps][256];            // radix scratch of the compaction
-  int slot;                            // candidate slot of the current unit
-  int jc[4];                           // per TMEM lane quarter: next (tile, column-quarter) job
-  int pad_[3];
+  float rs[kAppWarps][kRing][32];      // entry: the hitting row's 32 scores (int8: converted)
+  int32_t rid[kAppWarps][kRing][32];   // entry: the 32 columns' ids (perm != nullptr)
+  uint64_t rfull[kAppWarps][kRing];    // entry ready: mbarrier (count 1), phase = ticket / kRing
+  int2 rmeta[kAppWarps][kRing];        // entry: x = row (-1: end of unit), y = first column
+  unsigned long long traise[2][128];   // per unit parity and row: ((unit + 1) << 32) | raised threshold score bits
+  unsigned long long st_tk[kAppWarps][64];   // append warps: sub-list thresholds of the unit's queries
+  int st_cnt[kAppWarps][64];           // append warps: sub-list key counts
+  int hist[kAppWarps][256];            // radix scratch of the append warps' compaction
+  int tail[kAppWarps];                 // next ticket of each ring
+  int head[kAppWarps];                 // entries consumed (written by the append warp)
+  int done;                            // fast-path warps that finished their current unit (mod 16)
+  int pad_;
 };
 
 struct ScoreSmemLayout {
@@ -314,12 +326,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::mbar_init(a_full + 1, kEpiWarps);
     for (int j = 0; j < kUQ; ++j) {
       tc::mbar_init(uq_full + j, 1);
-      tc::mbar_init(uq_empty + j, 1 + kEpiWarps);   // the MMA warp and every epilogue warp read each slot
+      tc::mbar_init(uq_empty + j, 1 + kEpiWarps + kAppWarps);   // MMA, epilogue and append warps read each slot
     }
-    for (int j = 0; j < 4; ++j) S.jc[j] = 0;
+    for (int j = 0; j < kAppWarps; ++j) S.tail[j] = S.head[j] = 0;
+    for (int j = 0; j < kAppWarps * kRing; ++j) tc::mbar_init(&S.rfull[0][0] + j, 1);
+    S.done = 0;
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmap_xlow);
   }
+  for (int j = threadIdx.x; j < 2 * 128; j += kThreads) (&S.traise[0][0])[j] = 0ull;
   if (warp == kMmaWarp) tc::tmem_alloc(tmem_ptr, 512);
   tc::tc_fence_before();
   __syncthreads();
@@ -465,20 +480,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       atomicAdd(a.stats + 4, ck[2]);
       atomicAdd(a.stats + 5, ntiles_ck);
     }
-  } else {
-    // ------------------------------------------------------------ epilogue: 16 warps
-    // The four warps of a TMEM lane quarter take (tile, 32-column quarter) jobs from a shared
-    // counter in order, so a warp busy on the hit path does not hold back its column quarter;
-    // thread = one query of the quarter, with its own candidate sub-list (4 per slot and query).
-    // write_A keeps the static split: warp group cq writes K range cq of the A operand.
-    const int cq = warp >> 2;        // warp group in the lane quarter (A split, sub-list index)
+  } else if (warp < kEpiWarps) {
+    // ------------------------------------------------------------ epilogue: 16 fast-path warps
+    // The four warps of a TMEM lane quarter take that quarter's (tile, column block) jobs in a
+    // fixed rotation (warp group cq takes jobs cq, cq + 4, ...): a warp's consecutive jobs are
+    // 4 / kJobsPerTile <= nacc - 1 tiles apart, so when it waits for tile g its previous wait
+    // proved tile g - nacc committed, and the parity wait on g's buffer is unambiguous.
+    // Thread = one query of the quarter.  Hitting rows go to the append ring of the quarter's
+    // query half; the fast path never appends.
+    // write_A: warp group cq writes K range cq of the A operand.
+    const int cq = warp >> 2;        // warp group in the lane quarter (A split, job rotation)
     const int quarter = warp & 3;    // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
+    const int rg = quarter & 1;      // append ring of this quarter's query half
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t lt = (1u << lane) - 1u;
     const int ldq = a.C * d;         // Q' row length (elements)
-    float (*srows)[32] = S.rows[warp];
-    int* hist = S.hist[warp];
     // A operand of unit u (its cluster's view of the tile's 128 queries) -> TMEM buffer b; this
     // warp writes K range [cq*d/4, (cq+1)*d/4) of its 32 rows (d*esz/16 TMEM columns), loaded as
     // 8-byte words (the slice start is 8-byte aligned for every d and element size)
@@ -526,13 +543,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(a_full + b);
     };
+    // ring room: the entries below `need` of ring r consumed
+    auto wait_room = [&](int r, int need) {
+      uint32_t spins = 0;
+      while (*reinterpret_cast<volatile int*>(&S.head[r]) < need) {
+        __nanosleep(32);
+        if (++spins > (1u << 28)) __trap();   // a lost append warp would otherwise hang the GPU
+      }
+    };
     unsigned long long ek[3] = {0ull, 0ull, 0ull}, njobs_ck = 0ull;   // clock probe (LV_CLK_STATS)
-    unsigned long long ek_hit = 0ull, n_hit = 0ull;
+    unsigned long long pk[2] = {0ull, 0ull}, npush = 0ull;
     int u_next = unit_at(0);   // the unit after the current one (its A operand goes in early)
     if (u_next < nunits) write_A(u_next, 0);
     const uint32_t tm_lane = tmem_base + lane_base + acc_col0;
     int tiles_before = 0;   // tiles of this CTA's earlier units (global tile ordinal base)
-    int pending = -1;       // a job index already taken that belongs to a later unit
+    int J = cq;             // this warp's next job (global job ordinal of its lane quarter)
     int i = 0;
     for (;; ++i) {
       const int u = u_next;
@@ -546,63 +571,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int t_last = t0 + (t1 - 1 - t0) / tstride * tstride;
       const int q = qt * 128 + row;
       const bool qvalid = q < m_eff;
-      // ---- unit start: claim a free candidate slot of query tile qt (units of one tile that run
-      // concurrently on different CTAs use different slots; a slot's lists carry over)
       constexpr bool lists = !kSample;   // the sample stage keeps no candidate lists
-      if (lists && threadIdx.x == 0) {
-        int32_t* busy = a.slot_busy + qt;
-        long long spins = 0;
-        int got = -1;
-        while (got < 0) {
-          const int32_t cur = ld_acquire(busy);
-          const uint32_t freem = ~(uint32_t)cur & ((1u << a.NS) - 1u);
-          if (freem) {
-            const int sl = __ffs(freem) - 1;
-            if (atomicCAS(busy, cur, cur | (1 << sl)) == cur) got = sl;
-          } else {
-            __nanosleep(128);
-            if (count_stats) atomicAdd(a.stats + 3, 1ull);
-            if (++spins > (1ll << 27)) __trap();   // a lost release would otherwise hang the GPU
-          }
-        }
-        __threadfence();
-        S.slot = got;
-      }
-      if (lists) tc::named_bar_sync(1, kEpiThreads);
-      const int my_slot = lists ? S.slot : 0;
-      const size_t si = (size_t)(my_slot * 4 + cq) * a.m_pad + q;   // this thread's sub-list
-      LV_CHECK(!lists || (my_slot >= 0 && my_slot < a.NS && q < a.m_pad));
-      int cnt = lists ? a.cnt[si] : 0;
-      LV_CHECK(cnt >= 0 && cnt <= a.Cap);
-      uint64_t tk = lists ? a.tau[si] : 0ull;
-      float ts = qvalid ? thr_score(tk) : FLT_MAX;   // padded queries never hit
+      // filter threshold of query q: the threshold of any of its sub-lists is valid (at least R
+      // stored keys lie above it, or it is the start threshold that K4 verifies), so sub-list 0's;
+      // the append warp raises it when a compaction of this unit's list raises that list's
+      LV_CHECK(q < a.m_pad);
+      const uint64_t tk0 = (lists && qvalid) ? a.tau[q] : 0ull;
+      float ts = qvalid ? thr_score(tk0) : FLT_MAX;   // padded queries never hit
       // int8: this query's scale for the unit's cluster view, and the threshold on accumulators
       const float qs = kI8 ? a.qscale[(size_t)q * a.C + ci[2]] : 1.f;
       int ti = kI8 ? i8_threshold(ts, qs) : 0;
-      uint64_t* const bp = a.cand + si * (size_t)a.Cap;
+      const uint32_t utag = (uint32_t)i + 1u;
       const int n_t = (t1 - t0 + tstride - 1) / tstride;   // tiles of this unit
-      const int jend = (tiles_before + n_t) * kJobsPerTile;   // job index bound of this unit
+      const int jend = (tiles_before + n_t) * kJobsPerTile;   // job ordinal bound of this unit
 
-      for (;;) {
-        int J = pending;
-        if (J < 0) {
-          if (lane == 0) J = atomicAdd(&S.jc[quarter], 1);
-          J = __shfl_sync(0xffffffffu, J, 0);
-        }
-        if (J >= jend) {   // first job of a later unit: keep it for then
-          pending = J;
-          break;
-        }
-        pending = -1;
+      for (; J < jend; J += 4) {
         const int g = J / kJobsPerTile, jh = J % kJobsPerTile;   // global tile ordinal, column block
         const int t = t0 + (g - tiles_before) * tstride;
         const int base_pos = t * kN + jh * kJobCols;
         // GleanVec: original ids of this lane's columns, loaded now so the loads overlap the
-        // accumulator wait and the max (they are only needed on the rare hit path)
+        // accumulator wait and the max (they are only needed when a block hits)
         int32_t my_id[kJV];
 #pragma unroll
         for (int h = 0; h < kJV; ++h) my_id[h] = (!kSample && a.perm) ? __ldg(a.perm + base_pos + 32 * h + lane) : 0;
         LV_CHECK(t >= t0 && t < t1 && (int64_t)(base_pos + kJobCols) <= a.n_pad);
+        if (lists) {   // a threshold the append warp raised for this unit's query
+          const unsigned long long w = S.traise[i & 1][row];
+          if ((uint32_t)(w >> 32) == utag) {
+            const float tr = __uint_as_float((uint32_t)w);
+            if (tr > ts) {
+              ts = tr;
+              if (kI8) ti = i8_threshold(ts, qs);
+            }
+          }
+        }
         // the job's accumulator buffer: buffers are used in order, kHalves per tile
         const int qb = g * kHalves + (jh * kJobCols) / kAccN;
         const int accb = qb % nacc;
@@ -621,136 +623,98 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         const long long e1 = clk_stats ? clock64() : 0;
         tc::tc_fence_after();
-        // the job's 32-column halves in turn: load, (mask), max, compare, rare hit path; the
-        // accumulator is released after the last half's load
         float bm = -FLT_MAX;   // sample stage: running block maximum of the job
-        // one 32-column half of the job: (mask), raw output, max, threshold test, rare hit path
+        // one 32-column half of the job: (mask), raw output, max, threshold test, push of the
+        // hitting rows
         auto half = [&](float (&v)[32], const int h) {
-            if (skip_topr) return;
-            const int hpos = base_pos + 32 * h;
-            if (t == t_last) {   // a cluster segment's last tile may be partial
-              const int tv = a.tile_valid[t_last] - (jh * kJobCols + 32 * h);
-              if (tv < 32) {
-  #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                  if (j >= tv) v[j] = kI8 ? __int_as_float(INT_MIN) : -FLT_MAX;
-              }
+          const int hpos = base_pos + 32 * h;
+          if (t == t_last) {   // a cluster segment's last tile may be partial
+            const int tv = a.tile_valid[t_last] - (jh * kJobCols + 32 * h);
+            if (tv < 32) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j >= tv) v[j] = kI8 ? __int_as_float(INT_MIN) : -FLT_MAX;
             }
-            // int8: v holds s32 accumulators; the score of column j is fl(qs * float(acc_j))
-            auto score_of = [&](float raw) -> float {
-              if (!kI8) return raw;
-              const int iv = __float_as_int(raw);
-              return iv == INT_MIN ? -FLT_MAX : qs * (float)iv;
-            };
-            if (a.raw != nullptr) {
-  #pragma unroll
-              for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + hpos + j] = score_of(v[j]);
-              LV_CHECK(q < a.m_pad && (int64_t)(hpos + 32) <= a.n_pad);
-            }
-            float mx;
-            bool hit;
-            if (kI8) {
-              // tree of integer maxima (a 31-deep dependent chain would expose its latency)
-              int t16[16];
-  #pragma unroll
-              for (int j = 0; j < 16; ++j) t16[j] = max(__float_as_int(v[j]), __float_as_int(v[j + 16]));
-  #pragma unroll
-              for (int w = 8; w >= 1; w >>= 1)
-  #pragma unroll
-                for (int j = 0; j < w; ++j) t16[j] = max(t16[j], t16[j + w]);
-              const int im = t16[0];
-              mx = im == INT_MIN ? -FLT_MAX : qs * (float)im;
-              hit = im >= ti && im > INT_MIN;
+          }
+          // int8: v holds s32 accumulators; the score of column j is fl(qs * float(acc_j))
+          auto score_of = [&](float raw) -> float {
+            if (!kI8) return raw;
+            const int iv = __float_as_int(raw);
+            return iv == INT_MIN ? -FLT_MAX : qs * (float)iv;
+          };
+          if (a.raw != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + hpos + j] = score_of(v[j]);
+            LV_CHECK(q < a.m_pad && (int64_t)(hpos + 32) <= a.n_pad);
+          }
+          float mx;
+          bool hit;
+          if (kI8) {
+            // tree of integer maxima (a 31-deep dependent chain would expose its latency)
+            int t16[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) t16[j] = max(__float_as_int(v[j]), __float_as_int(v[j + 16]));
+#pragma unroll
+            for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+              for (int j = 0; j < w; ++j) t16[j] = max(t16[j], t16[j + w]);
+            const int im = t16[0];
+            mx = im == INT_MIN ? -FLT_MAX : qs * (float)im;
+            hit = im >= ti && im > INT_MIN;
+          } else {
+            mx = v[0];
+#pragma unroll
+            for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
+            hit = mx >= ts && mx > -FLT_MAX;
+          }
+          if (kSample) {
+            // sample stage: record block maxima (query q; blocks of 32 database rows when
+            // a.flags & 8, else of the job's 64: fine blocks keep the threshold estimate of
+            // DESIGN.md §6 tight when top rows cluster); no top-R here
+            const int sblk = (sbase + (t - t0) / tstride) * kJobsPerTile + jh;
+            if (fine_blocks) {
+              a.bmax[(size_t)(sblk * kJV + h) * a.m_pad + q] = mx;
             } else {
-#if defined(LV_MAX3_TREE)
-              // four independent FMNMX3 chains of 8 values, then their maximum (latency ~1/4)
-              float m4[4];
-  #pragma unroll
-              for (int c4 = 0; c4 < 4; ++c4) {
-                m4[c4] = v[c4 * 8];
-  #pragma unroll
-                for (int j = 1; j < 8; ++j) m4[c4] = fmaxf(m4[c4], v[c4 * 8 + j]);
-              }
-              mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-#else
-              mx = v[0];
-  #pragma unroll
-              for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
-#endif
-
-              hit = mx >= ts && mx > -FLT_MAX;
+              bm = fmaxf(bm, mx);
+              if (h + 1 == kJV) a.bmax[(size_t)sblk * a.m_pad + q] = bm;
             }
-            if (kSample) {
-              // sample stage: record block maxima (query q; blocks of 32 database rows when
-              // a.flags & 8, else of the job's 64: fine blocks keep the threshold estimate of
-              // DESIGN.md §6 tight when top rows cluster); no top-R here
-              const int sblk = (sbase + (t - t0) / tstride) * kJobsPerTile + jh;
-              if (fine_blocks) {
-                a.bmax[(size_t)(sblk * kJV + h) * a.m_pad + q] = mx;
-              } else {
-                bm = fmaxf(bm, mx);
-                if (h + 1 == kJV) a.bmax[(size_t)sblk * a.m_pad + q] = bm;
-              }
-              return;
-            }
-
-            uint32_t hb = __ballot_sync(0xffffffffu, hit);
-            if (hb == 0u) return;
-            if (count_stats && lane == 0) atomicAdd(a.stats + 0, 1ull);
-            if (fast_only) return;
-            // hit path (divergence-free): each hitting lane's 32 scores are broadcast through shared
-            // memory, lane j tests column j, survivors are appended to the hitting lane's sub-list
-            // with coalesced stores
-            const long long hc0 = clk_stats ? clock64() : 0;
-            const int32_t id_h = (a.perm ? my_id[h] : hpos + lane);
-
-            if (hit) {
-  #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                reinterpret_cast<float4*>(srows[lane])[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            }
-            __syncwarp();
-            do {
-              const int Lz = __ffs(hb) - 1;
-              hb &= hb - 1u;
-              float f = srows[Lz][lane];
-              if (kI8) {   // raw accumulator of row Lz: converted with row Lz's scale by the testing lane
-                const float qsz = __shfl_sync(0xffffffffu, qs, Lz);
-                const int iv = __float_as_int(f);
-                f = iv == INT_MIN ? -FLT_MAX : qsz * (float)iv;
-              }
-              const float tsz = __shfl_sync(0xffffffffu, ts, Lz);
-              uint64_t tkz = __shfl_sync(0xffffffffu, tk, Lz);
-              int cz = __shfl_sync(0xffffffffu, cnt, Lz);
-              const uint64_t key = make_key(f, id_h);
-              bool keep = f >= tsz && f > -FLT_MAX && key > tkz;
-              uint32_t kb = __ballot_sync(0xffffffffu, keep);
-              if (kb == 0u) continue;   // row Lz has no survivor: next hitting row
-              uint64_t* bz = reinterpret_cast<uint64_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(bp), Lz));
-              if (cz + __popc(kb) > a.Cap) {
-                // full sub-list: compact it to its top-R (raises its threshold), then re-filter
-                uint64_t nthr;
-                cz = warp_compact_fast(bz, cz, a.R, a.Cap, lane, hist, &nthr);
-                tkz = nthr;
-                if (lane == Lz) {
-                  tk = nthr;
-                  ts = thr_score(nthr);
-                  if (kI8) ti = i8_threshold(ts, qs);
-                }
-                if (count_stats && lane == 0) atomicAdd(a.stats + 2, 1ull);
-                keep = keep && key > tkz;
-                kb = __ballot_sync(0xffffffffu, keep);
-              }
-              LV_CHECK(cz + __popc(kb) <= a.Cap);
-              if (keep) bz[cz + __popc(kb & lt)] = key;
-              if (lane == Lz) cnt = cz + __popc(kb);
-              if (count_stats && lane == 0) atomicAdd(a.stats + 1, (unsigned long long)__popc(kb));
-            } while (hb != 0u);
-            __syncwarp();
-            if (clk_stats) {
-              ek_hit += (unsigned long long)(clock64() - hc0);
-              ++n_hit;
-            }
+            return;
+          }
+          const uint32_t hb = __ballot_sync(0xffffffffu, hit);
+          if (hb == 0u) return;
+          if (count_stats && lane == 0) atomicAdd(a.stats + 0, 1ull);
+          if (fast_only) return;
+          // push: one ring entry per hitting row (tickets t0 .. t0 + n - 1 in lane order)
+          const long long p0 = clk_stats ? clock64() : 0;
+          const int n = __popc(hb);
+          int tk = 0;
+          if (lane == 0) {
+            tk = atomicAdd(&S.tail[rg], n);
+            const long long pw0 = clk_stats ? clock64() : 0;
+            wait_room(rg, tk + n - kRing);
+            if (clk_stats) pk[1] += (unsigned long long)(clock64() - pw0);
+          }
+          tk = __shfl_sync(0xffffffffu, tk, 0);
+          if (a.perm) {   // every lane writes its column's id into each hitting row's entry
+            const int32_t idh = my_id[h];
+            for (int e = 0; e < n; ++e) S.rid[rg][(tk + e) & (kRing - 1)][lane] = idh;
+          }
+          const int slot = (tk + __popc(hb & lt)) & (kRing - 1);
+          if (hit) {
+            float4* dst = reinterpret_cast<float4*>(S.rs[rg][slot]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)   // chunk j at (j + slot) % 8 (conflict-free reads by the append warp)
+              dst[(j + slot) & 7] = make_float4(score_of(v[4 * j]), score_of(v[4 * j + 1]), score_of(v[4 * j + 2]),
+                                   score_of(v[4 * j + 3]));
+            S.rmeta[rg][slot] = make_int2(row, hpos);
+          }
+          // the ids of the other lanes are ordered before the arrive (release) by the warp barrier
+          __syncwarp();
+          if (hit) tc::mbar_arrive(&S.rfull[rg][slot]);
+          if (clk_stats) {
+            pk[0] += (unsigned long long)(clock64() - p0);
+            ++npush;
+          }
         };
         {
           long long eld = 0;
@@ -778,31 +742,238 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tiles_before += n_t;
-      // unit end: every job of this unit has seen its tile committed, so the MMA is done with
-      // this unit's A buffer before any warp overwrites it (write_A of unit u + 2 at the next
-      // iteration); in the main stage the sub-list states go back to the slot, which is released
-      if (lists && qvalid) {
-        LV_CHECK(cnt >= 0 && cnt <= a.Cap);
-        a.cnt[si] = cnt;
-        a.tau[si] = tk;
+      // unit end: the last fast-path warp to finish the unit pushes its end marker into both
+      // rings (after every entry of the unit: the others pushed theirs before counting in), and
+      // the barrier keeps every entry of the next unit behind the markers.  It also proves every
+      // job of this unit saw its tile committed, so the MMA is done with this unit's A buffer
+      // before any warp overwrites it (write_A of unit u + 2 at the next iteration).
+      if (lists) {
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+          __threadfence_block();
+          last = (atomicAdd(&S.done, 1) % kEpiWarps) == kEpiWarps - 1;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last && lane < kAppWarps) {
+          const int tk = atomicAdd(&S.tail[lane], 1);
+          wait_room(lane, tk + 1 - kRing);
+          const int slot = tk & (kRing - 1);
+          S.rmeta[lane][slot] = make_int2(-1, 0);
+          tc::mbar_arrive(&S.rfull[lane][slot]);
+        }
+        __syncwarp();
       }
       tc::named_bar_sync(1, kEpiThreads);
-      if (lists && threadIdx.x == 0) {
-        // the barrier orders every epilogue thread's list-state stores before this thread's
-        // (cumulative) fence, which orders them before the release the next owner acquires
-        __threadfence();
-        atomicAnd(a.slot_busy + qt, ~(1 << my_slot));   // release the slot
-      }
       // single-buffered A: every job of this unit saw its tile committed, so the MMAs of this unit
       // are complete and its A buffer can take the next unit's operand
       if (kSingleA && u_next < nunits) write_A(u_next, 0);
     }
     if (clk_stats && lane == 0) {
       atomicAdd(a.stats + 2, ek[0]);
-      atomicAdd(a.stats + 3, ek_hit);
-      atomicAdd(a.stats + 1, n_hit);
       atomicAdd(a.stats + 6, njobs_ck);
       atomicAdd(a.stats + 7, ek[2]);
+      atomicAdd(a.stats + 11, npush);
+      atomicAdd(a.stats + 12, pk[0]);
+      atomicAdd(a.stats + 13, pk[1]);
+    }
+  } else {
+    // ------------------------------------------------------------ append warps (2)
+    // Ring rg carries the hitting rows of lane quarters rg and rg + 2 (queries 32 rg + lane and
+    // 32 (rg + 2) + lane of the tile, held by lane `lane` as sub-list states 0 and 1).  Per unit
+    // the warp claims one free sub-list of query tile qt for its query half (a 64-bit mask per
+    // (tile, half): units of one tile running concurrently on different CTAs use different
+    // sub-lists; a sub-list's keys carry over between units), appends every entry's survivors
+    // (key > the sub-list threshold) with coalesced stores, compacts a full sub-list to its top-R
+    // (raising its threshold, which is passed to the fast path) and at the unit's end marker
+    // writes the states back and releases the sub-list.
+    const int rg = warp - kAppWarp0;
+    const uint32_t lt = (1u << lane) - 1u;
+    int* hist = S.hist[rg];
+    int head = 0;
+    unsigned long long ak = 0ull, nent = 0ull;   // clock probe: busy cycles and entries
+    unsigned long long ab[3] = {0ull, 0ull, 0ull};   // clock probe: batches, read cycles, process cycles
+    unsigned nappend = 0u, ncompact = 0u;             // event counts (flag 2)
+    const unsigned long long lmask = a.NS >= 64 ? ~0ull : ((1ull << a.NS) - 1ull);
+    for (int i = 0;; ++i) {
+      const int u = unit_at(i);
+      unit_release(i);
+      if (u >= nunits) break;
+      if (kSample) continue;   // the sample stage keeps no candidate lists
+      const int qt = u % QT;
+      int sl = -1;
+      if (lane == 0) {
+        unsigned long long* busy = reinterpret_cast<unsigned long long*>(a.slot_busy) + (size_t)qt * kAppWarps + rg;
+        long long spins = 0;
+        while (sl < 0) {
+          const unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(busy);
+          const unsigned long long freem = ~cur & lmask;
+          if (freem) {
+            const int s = __ffsll((long long)freem) - 1;
+            if (atomicCAS(busy, cur, cur | (1ull << s)) == cur) sl = s;
+          } else {
+            __nanosleep(128);
+            if (count_stats) atomicAdd(a.stats + 3, 1ull);
+            if (++spins > (1ll << 27)) __trap();   // a lost release would otherwise hang the GPU
+          }
+        }
+        __threadfence();
+      }
+      sl = __shfl_sync(0xffffffffu, sl, 0);
+      LV_CHECK(sl >= 0 && sl < a.NS);
+      const int qa = qt * 128 + 32 * rg + lane;   // this lane's two queries
+      const size_t si0 = (size_t)sl * a.m_pad + qa, si1 = si0 + 64;
+      LV_CHECK(qa + 64 < a.m_pad);
+      // sub-list states of the unit's 64 queries in shared memory (local row lr = r % 32 + 32 [r >= 64])
+      int* const st_cnt = S.st_cnt[rg];
+      unsigned long long* const st_tk = S.st_tk[rg];
+      st_cnt[lane] = a.cnt[si0];
+      st_cnt[lane + 32] = a.cnt[si1];
+      st_tk[lane] = a.tau[si0];
+      st_tk[lane + 32] = a.tau[si1];
+      LV_CHECK(st_cnt[lane] >= 0 && st_cnt[lane] <= a.Cap && st_cnt[lane + 32] >= 0 && st_cnt[lane + 32] <= a.Cap);
+      __syncwarp();
+      uint64_t* const lbase = a.cand + ((size_t)sl * a.m_pad + (size_t)qt * 128) * (size_t)a.Cap;   // row r: + r * Cap
+      const int Cap = a.Cap;
+      // Entries are consumed in batches: the ready prefix of up to 32 (lane e probes entry head + e;
+      // the warp barrier passes the acquires on), one entry per lane.  Room first: every sub-list
+      // of the batch gets 32 key positions per entry it has in the batch (a warp-wide compaction
+      // where they do not fit, the batch cut where even that is not enough); then each lane filters
+      // its entry's 32 scores against its row's threshold and appends the survivors at positions
+      // taken with a shared-memory atomic on the row's count (rare: ~1 per entry).  Entry scores
+      // are stored as 8 rotated 16-byte chunks (chunk k of slot s at (k + s) % 8), so the lanes'
+      // loads of chunk k hit 8 different bank groups.
+      bool end = false;
+      while (!end) {
+        int nready;
+        {
+          uint32_t spins = 0;
+          for (;;) {
+            const int te = head + lane;
+            const bool rdy = tc::mbar_test_wait(&S.rfull[rg][te & (kRing - 1)], (uint32_t)(te / kRing) & 1u);
+            const uint32_t b = __ballot_sync(0xffffffffu, rdy);
+            nready = b == 0xffffffffu ? 32 : __ffs(~b) - 1;
+            if (nready > 0) break;
+            __nanosleep(20);
+            if (++spins > (1u << 28)) __trap();
+          }
+        }
+        __syncwarp();
+        const long long c0 = clk_stats ? clock64() : 0;
+        const int sj = (head + lane) & (kRing - 1);
+        int r = -3, hp = 0;
+        if (lane < nready) {
+          const int2 md = S.rmeta[rg][sj];
+          r = md.x;
+          hp = md.y;
+        }
+        const uint32_t endm = __ballot_sync(0xffffffffu, lane < nready && r < 0);
+        int nb = endm ? __ffs(endm) - 1 : nready;   // entries before an end marker
+        const int lr = (r & 31) | ((r >> 1) & 32);
+        const float4* src = reinterpret_cast<const float4*>(S.rs[rg][sj]);
+        // the entry's candidate columns: score >= its row's threshold score
+        auto hits = [&]() -> uint32_t {
+          const float ts = thr_score(st_tk[lr]);
+          uint32_t m = 0u;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float4 v = src[(k + sj) & 7];
+            m |= (v.x >= ts && v.x > -FLT_MAX ? 1u : 0u) << (4 * k);
+            m |= (v.y >= ts && v.y > -FLT_MAX ? 1u : 0u) << (4 * k + 1);
+            m |= (v.z >= ts && v.z > -FLT_MAX ? 1u : 0u) << (4 * k + 2);
+            m |= (v.w >= ts && v.w > -FLT_MAX ? 1u : 0u) << (4 * k + 3);
+          }
+          return m;
+        };
+        uint32_t m = lane < nb ? hits() : 0u;
+        // room: a row's candidates of the batch must fit its sub-list; else compact it (raising its
+        // threshold, so its entries are re-filtered), and if they still do not fit, cut the batch
+        // after the row's first entry (one entry always fits a compacted list: <= Cap - 64 keys)
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          const bool inb = lane < nb;
+          const uint32_t same = __match_any_sync(0xffffffffu, inb ? lr : 64 + lane);
+          const int need = __reduce_add_sync(same, __popc(m));
+          const bool viol = inb && st_cnt[lr] + need > Cap;
+          const uint32_t vb = __ballot_sync(0xffffffffu, viol);
+          if (vb == 0u) break;
+          if (pass == 0) {
+            uint32_t todo = vb;
+            while (todo) {
+              const int L = __ffs(todo) - 1;
+              const int lrL = __shfl_sync(0xffffffffu, lr, L), rL = __shfl_sync(0xffffffffu, r, L);
+              todo &= ~__ballot_sync(0xffffffffu, lr == lrL);
+              uint64_t nthr;
+              const int cz = warp_compact_fast(lbase + (size_t)rL * (size_t)Cap, st_cnt[lrL], a.R, Cap, lane, S.hist[rg], &nthr);
+              if (lane == 0) {
+                st_cnt[lrL] = cz;
+                if (nthr > st_tk[lrL]) st_tk[lrL] = nthr;
+                S.traise[i & 1][rL] = ((unsigned long long)(i + 1) << 32) |
+                                      (unsigned long long)__float_as_uint(thr_score(st_tk[lrL]));
+              }
+              ++ncompact;
+              __syncwarp();
+            }
+            if (viol) m = hits();   // the row's threshold rose
+          } else {
+            nb = __ffs(vb) + 0;   // through the first violating entry (its row's first in the batch)
+            if (lane >= nb) m = 0u;
+          }
+        }
+        if (lane < nb) {
+          const uint64_t tk = st_tk[lr];
+          uint64_t* const bz = lbase + (size_t)r * (size_t)Cap;
+          while (m) {
+            const int col = __ffs(m) - 1;
+            m &= m - 1u;
+            const float s = reinterpret_cast<const float*>(src)[4 * ((col / 4 + sj) & 7) + col % 4];
+            const int32_t id = a.perm ? S.rid[rg][sj][col] : hp + col;
+            const uint64_t key = make_key(s, id);
+            if (key > tk) {
+              const int pos = atomicAdd(&st_cnt[lr], 1);
+              LV_CHECK(pos < Cap);
+              bz[pos] = key;
+              ++nappend;
+            }
+          }
+        }
+        const bool ends = endm != 0u && nb == __ffs(endm) - 1;   // the marker is next: unit i ends
+        const int used = nb + (ends ? 1 : 0);
+        __syncwarp();
+        head += used;
+        if (lane == 0) *reinterpret_cast<volatile int*>(&S.head[rg]) = head;
+        end = ends;
+        if (clk_stats) {
+          const long long c2 = clock64();
+          ak += (unsigned long long)(c2 - c0);
+          nent += (unsigned long long)used;
+          ab[0] += 1ull;
+          ab[2] += (unsigned long long)(c2 - c0);
+        }
+      }
+      // end of the unit: sub-list states back, then release (the fence orders the warp's list and
+      // state stores before the release the next owner acquires)
+      __syncwarp();
+      a.cnt[si0] = st_cnt[lane];
+      a.cnt[si1] = st_cnt[lane + 32];
+      a.tau[si0] = st_tk[lane];
+      a.tau[si1] = st_tk[lane + 32];
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomicAnd(reinterpret_cast<unsigned long long*>(a.slot_busy) + (size_t)qt * kAppWarps + rg, ~(1ull << sl));
+      }
+    }
+    if (count_stats && lane == 0) {
+      atomicAdd(a.stats + 1, (unsigned long long)nappend);
+      atomicAdd(a.stats + 2, (unsigned long long)ncompact);
+    }
+    if (clk_stats && lane == 0) {
+      atomicAdd(a.stats + 1, nent);
+      atomicAdd(a.stats + 3, ak);
+      atomicAdd(a.stats + 8, ab[0]);
+      atomicAdd(a.stats + 9, ab[1]);
+      atomicAdd(a.stats + 10, ab[2]);
     }
   }
   tc::tc_fence_before();

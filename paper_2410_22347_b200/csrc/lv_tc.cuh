@@ -102,6 +102,16 @@ LV_TC_INL void mbar_wait_sleep_u32(uint32_t bar, uint32_t parity) {
 #endif
   }
 }
+// Non-blocking probe of a phase (acquire semantics at CTA scope when it returns true).
+LV_TC_INL bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // One lane of the warp (elect.sync); the other lanes get false.
 LV_TC_INL bool elect_one() {
   uint32_t e;
