@@ -860,7 +860,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
     const size_t mp = pl.m_pad;
     size_t need = (mp * Cd * 2 + 256) + ((size_t)3 * mp * ix->Kp * 2 + 256) + ((size_t)NS2 * mp * pl.Cap * 8 + 256) +
                   ((size_t)NS2 * mp * 4 + 256) +
-                  ((size_t)NS2 * mp * 8 + 256) + ((size_t)pl.QP * 16 + 256) + (16 * 4 + 256) + (kMaxScans * 4 + 256) +
+                  ((size_t)NS2 * mp * 8 + 256) + (mp * 8 + 256) + ((size_t)pl.QP * 16 + 256) + (16 * 4 + 256) + (kMaxScans * 4 + 256) +
                   (mp * (size_t)R * 4 + 256) + (mp * 4 + 256) +
                   (nchunk_ints * 4 + 256 * (pl.chunks.size() + 2));
     if (pl.sampled)
@@ -884,6 +884,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
     pc.zero_lo = p;
     pc.cnt = carve<int32_t>(p, (size_t)NS2 * mp);
     pc.tau = carve<uint64_t>(p, (size_t)NS2 * mp);
+    pc.tbest = carve<unsigned long long>(p, mp);
     pc.slot_busy = carve<int32_t>(p, (size_t)pl.QP * 4);   // [QP][2] 64-bit sub-list masks (one per query half)
     pc.sel_ids = carve<int32_t>(p, mp * (size_t)R);
     pc.sel_n = carve<int32_t>(p, mp);
@@ -978,6 +979,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
   sa.cand = pc.cand;
   sa.cnt = pc.cnt;
   sa.tau = pc.tau;
+  sa.tbest = pc.tbest;
   sa.raw = dbg ? dbg->raw_scores : nullptr;
   sa.bmax = nullptr;
   sa.m_dev = nullptr;
@@ -1109,7 +1111,7 @@ static lv_status search_batch(lv_index* ix, const float* Q, int64_t m, int32_t k
       int32_t* fcount = pc.fail + round;
       int32_t* mdev = pc.fail + 4 + round;
       LV_CUDA(lv::launch_repair_setup(Qp, Cd * ix->esz() / 2, flist, fcount, pc.Qr, round == 0 ? pc.tau2 : nullptr,
-                                      pc.tau, pc.cnt, NS2, pl.m_pad, (int)m, mdev, pc.qscale, pc.qscale_r, ix->C, s));
+                                      pc.tau, pc.tbest, pc.cnt, NS2, pl.m_pad, (int)m, mdev, pc.qscale, pc.qscale_r, ix->C, s));
       sa.Qp = pc.Qr;
       sa.qscale = pc.qscale_r;
       sa.m_dev = mdev;
@@ -1262,7 +1264,7 @@ lv_status lv_search_host(lv_index* ix, const float* Q_host, int64_t m, int32_t k
   }
   if (!ix->cs) {
     LV_CUDA(cudaStreamCreateWithFlags(&ix->cs, cudaStreamNonBlocking));
-    for (int i = 0; i < 4; ++i) LV_CUDA(cudaEventCreateWithFlags(&ix->hev[i], cudaEventDisableTiming));
+    for (int i = 0; i < kHostEv; ++i) LV_CUDA(cudaEventCreateWithFlags(&ix->hev[i], cudaEventDisableTiming));
   }
   uint8_t* p = reinterpret_cast<uint8_t*>(ix->hs);
   float* dQ = carve<float>(p, (size_t)m * ix->D);
@@ -1271,9 +1273,12 @@ lv_status lv_search_host(lv_index* ix, const float* Q_host, int64_t m, int32_t k
   // two query batches when the batch is large: batch 1's upload (copy stream) overlaps batch 0's
   // search, batch 0's download overlaps batch 1's search
   int64_t nb = 1, mb = m;
-  const bool split = env_double("LV_HOST_BATCHES", 2.0) >= 2.0;   // 1: one batch (no copy/compute overlap)
-  if (m >= 4096 && split) batch_layout(m, std::min<int64_t>(max_batch(), (m + 1) / 2 + 127), &nb, &mb);
-  if (nb > 2) batch_layout(m, max_batch(), &nb, &mb);
+  // LV_HOST_BATCHES: equal query batches (1: one batch, no copy/compute overlap), each >= 2048 queries
+  const int64_t nh = std::max<int64_t>(1, std::min<int64_t>(kHostEv - 2, (int64_t)env_double("LV_HOST_BATCHES", 2.0)));
+  const int64_t want = std::min<int64_t>(nh, std::max<int64_t>(1, m / 2048));
+  if (want >= 2) batch_layout(m, std::min<int64_t>(max_batch(), (m + want - 1) / want + 127), &nb, &mb);
+  if (nb > kHostEv - 2) batch_layout(m, max_batch(), &nb, &mb);
+  if (nb > kHostEv - 2) return fail(LV_EUNSUPPORTED, "lv_search_host: m=%lld needs more than %d batches", (long long)m, kHostEv - 2);
   const int64_t D = ix->D;
   std::vector<int64_t> lo(nb), hi(nb), off(nb);
   for (int64_t b = 0; b < nb; ++b) {
@@ -1281,19 +1286,21 @@ lv_status lv_search_host(lv_index* ix, const float* Q_host, int64_t m, int32_t k
     lo[b] = b == 0 ? 0 : hi[b - 1];   // rows first needed by batch b
     hi[b] = off[b] + mb;
   }
+  // events: [b] upload of batch b's rows done (copy stream), [kHostEv - 2] start, [kHostEv - 1]
+  // search of the current batch done
   cudaEvent_t* ev = ix->hev;
-  LV_CUDA(cudaEventRecord(ev[2], s));          // the copy stream starts after prior work on s
-  LV_CUDA(cudaStreamWaitEvent(ix->cs, ev[2], 0));
+  cudaEvent_t ev_start = ev[kHostEv - 2], ev_done = ev[kHostEv - 1];
+  LV_CUDA(cudaEventRecord(ev_start, s));          // the copy stream starts after prior work on s
+  LV_CUDA(cudaStreamWaitEvent(ix->cs, ev_start, 0));
   for (int64_t b = 0; b < nb; ++b) {
     // uploads: batch b's new rows on the copy stream
     LV_CUDA(cudaMemcpyAsync(dQ + lo[b] * D, Q_host + lo[b] * D, (size_t)(hi[b] - lo[b]) * D * 4, cudaMemcpyHostToDevice,
                             ix->cs));
-    if (b == 0) LV_CUDA(cudaEventRecord(ev[0], ix->cs));
+    LV_CUDA(cudaEventRecord(ev[b], ix->cs));
   }
-  LV_CUDA(cudaEventRecord(ev[1], ix->cs));
   int64_t done = 0;
   for (int64_t b = 0; b < nb; ++b) {
-    LV_CUDA(cudaStreamWaitEvent(s, ev[b == 0 ? 0 : 1], 0));
+    LV_CUDA(cudaStreamWaitEvent(s, ev[b], 0));
     st = search_batch(ix, dQ + off[b] * D, mb, k, R, dI + off[b] * k, dS + off[b] * k, nullptr, stream);
     if (st) {
       cudaStreamSynchronize(ix->cs);
@@ -1301,8 +1308,8 @@ lv_status lv_search_host(lv_index* ix, const float* Q_host, int64_t m, int32_t k
     }
     // downloads of the rows no later batch rewrites: [done, off[b + 1]) (the last batch: to m)
     const int64_t r1 = (b + 1 < nb) ? off[b + 1] : m;
-    LV_CUDA(cudaEventRecord(ev[3], s));
-    LV_CUDA(cudaStreamWaitEvent(ix->cs, ev[3], 0));
+    LV_CUDA(cudaEventRecord(ev_done, s));
+    LV_CUDA(cudaStreamWaitEvent(ix->cs, ev_done, 0));
     if (r1 > done) {
       LV_CUDA(cudaMemcpyAsync(ids_host + done * k, dI + done * k, (size_t)(r1 - done) * k * 4, cudaMemcpyDeviceToHost,
                               ix->cs));

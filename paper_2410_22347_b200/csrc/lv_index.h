@@ -10,6 +10,8 @@
 #include "../../include/lv.h"
 #include "lv_internal.h"
 
+constexpr int kHostEv = 16;   // lv_search_host: at most kHostEv - 2 query batches
+
 // Work decomposition of one lv_search shape (m, R) and its carve of the index workspace.
 // Chunk records are lv::kChunkInts ints: tile_begin, tile_end, cluster, tile_stride, sample_base.
 struct Plan {
@@ -32,6 +34,7 @@ struct PlanCache {
   uint64_t* cand = nullptr;
   int32_t* cnt = nullptr;
   uint64_t* tau = nullptr;
+  unsigned long long* tbest = nullptr;   // per list row: the best valid threshold key (scan compactions)
   void* Qplanes = nullptr;     // bf16 [3][m_pad][Kp]: Q split for the K1 GEMM
   CUtensorMap tmap_q;
   uint64_t* tau2 = nullptr;    // sampled: per-query repair threshold
@@ -99,7 +102,7 @@ struct lv_index {
   void* hs = nullptr;
   size_t hs_bytes = 0;
   cudaStream_t cs = nullptr;
-  cudaEvent_t hev[4] = {};
+  cudaEvent_t hev[kHostEv] = {};   // lv_search_host: per-batch upload events + start / done
 };
 
 namespace lv {

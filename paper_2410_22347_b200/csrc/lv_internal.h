@@ -34,6 +34,7 @@ struct ScoreArgs {
   uint64_t* cand;              // [NS][m_pad][Cap]
   int32_t* cnt;                // [NS][m_pad]
   uint64_t* tau;               // [NS][m_pad]
+  unsigned long long* tbest;   // [m_pad] a valid threshold key per list row, raised (atomicMax) by compactions
   int32_t* slot_busy;          // [QP][2] 64-bit masks of claimed sub-lists per query tile and half (zero between launches)
   float* raw;                  // [m_pad][n_pad] or nullptr
   float* bmax;                 // sample stage: [n_sample_tiles * blocks_per_tile][m_pad] block maxima, else nullptr
@@ -78,8 +79,8 @@ struct RerankArgs {
 cudaError_t launch_bmax_select(const float* bmax, int nblk, int m, int m_pad, int j1, int j2, uint64_t* tau,
                                int32_t* cnt, int NS, uint64_t* tau2, cudaStream_t s);
 cudaError_t launch_repair_setup(const void* Qp, int row_u16, const int32_t* fail_list, const int32_t* fail_count,
-                                void* Qr, const uint64_t* tau_src, uint64_t* tau, int32_t* cnt, int NS, int m_pad,
-                                int m_max, int32_t* m_out, const float* qs_src, float* qs_dst, int C, cudaStream_t s);
+                                void* Qr, const uint64_t* tau_src, uint64_t* tau, unsigned long long* tbest, int32_t* cnt,
+                                int NS, int m_pad, int m_max, int32_t* m_out, const float* qs_src, float* qs_dst, int C, cudaStream_t s);
 cudaError_t launch_select_topr(const RerankArgs& a, cudaStream_t s);   // K4
 cudaError_t launch_rerank_topk(const RerankArgs& a, cudaStream_t s);   // K5
 cudaError_t launch_tau_merge(uint64_t* cand, int32_t* cnt, uint64_t* tau, int NS, int m, int m_pad, int Cap, int R,

@@ -3,8 +3,9 @@
 // N_low(j) = the R largest keys (reduced score desc, original id asc) among the union of the
 // query's slot buffers (every buffer holds a superset of its slot's top-R), found
 // by an 8-bit MSB radix select in shared memory (Alg. 1 line 2's kappa = R).
-// Re-rank (Alg. 1 line 3): r_ji = <q_j, x_i> in fp32 on the full vectors; one warp per
-// candidate row, 128-bit coalesced loads, warp-shuffle reduction; top-k by (r desc, id asc).
+// Re-rank (Alg. 1 line 3): r_ji = <q_j, x_i> in fp32 on the full vectors; one CTA of four
+// warps per query (the warps split its R candidates), 128-bit coalesced loads, warp-shuffle
+// reduction; top-k by (r desc, id asc).
 #include <cfloat>
 
 #include "lv_common.cuh"
@@ -189,13 +190,20 @@ __global__ void __launch_bounds__(kSelW * 32) k_select_topr(const RerankArgs a) 
   const int R = min(a.R, total);
   const bool staged = total <= kStageKeys;
   if (staged) {
-    // lane l copies lists l and l + 32 (lists are short: ~total / NS keys; loads pipelined)
-    const uint64_t* src0 = a.cand + ((size_t)lane * a.m_pad + r) * (size_t)a.Cap;
-    const uint64_t* src1 = a.cand + ((size_t)(lane + 32) * a.m_pad + r) * (size_t)a.Cap;
-#pragma unroll 4
-    for (int i = 0; i < c0; ++i) keys[e0 + i] = src0[i];
-#pragma unroll 4
-    for (int i = 0; i < c1; ++i) keys[e1 + i] = src1[i];
+    // the warp copies the non-empty lists one after the other, 32 keys per step (a query's keys
+    // may sit in one or two lists: the scan's units claim the lowest free sub-list)
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+      uint32_t ne = __ballot_sync(0xffffffffu, (half ? c1 : c0) > 0);
+      while (ne) {
+        const int l = __ffs(ne) - 1;
+        ne &= ne - 1u;
+        const int c = __shfl_sync(0xffffffffu, half ? c1 : c0, l);
+        const int off = __shfl_sync(0xffffffffu, half ? e1 : e0, l);
+        const uint64_t* src = a.cand + ((size_t)(l + 32 * half) * a.m_pad + r) * (size_t)a.Cap;
+        for (int i = lane; i < c; i += 32) keys[off + i] = src[i];
+      }
+    }
     __syncwarp();
   }
   // key i of the concatenated lists (staged: shared memory; else: L2, list found by a per-lane
@@ -540,32 +548,34 @@ cudaError_t launch_bmax_select(const float* bmax, int nblk, int m, int m_pad, in
 // tau_src[fail_list[r]] (or 0 = none); *m_out = F.
 __global__ void k_repair_setup(const uint16_t* __restrict__ Qp, int row_u16, const int32_t* __restrict__ fail_list,
                                const int32_t* __restrict__ fail_count, uint16_t* __restrict__ Qr,
-                               const uint64_t* __restrict__ tau_src, uint64_t* tau, int32_t* cnt, int NS, int m_pad,
-                               int32_t* m_out, const float* __restrict__ qs_src, float* __restrict__ qs_dst, int C) {
+                               const uint64_t* __restrict__ tau_src, uint64_t* tau, unsigned long long* tbest,
+                               int32_t* cnt, int NS, int m_pad, int32_t* m_out, const float* __restrict__ qs_src, float* __restrict__ qs_dst, int C) {
   const int F = *fail_count;
   const int Fp = (F + 127) / 128 * 128;
-  const int r = blockIdx.x;
-  if (r >= Fp) return;
-  if (r == 0 && threadIdx.x == 0) *m_out = F;
-  const bool v = r < F;
-  const int q = v ? fail_list[r] : 0;
-  for (int e = threadIdx.x; e < row_u16; e += blockDim.x)
-    Qr[(size_t)r * row_u16 + e] = v ? Qp[(size_t)q * row_u16 + e] : (uint16_t)0;
-  if (qs_src)
-    for (int c = threadIdx.x; c < C; c += blockDim.x) qs_dst[(size_t)r * C + c] = v ? qs_src[(size_t)q * C + c] : 1.f;
-  const uint64_t t = (v && tau_src) ? tau_src[q] : 0ull;
-  for (int sl = threadIdx.x; sl < NS; sl += blockDim.x) {
-    tau[(size_t)sl * m_pad + r] = t;
-    cnt[(size_t)sl * m_pad + r] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *m_out = F;
+  for (int r = blockIdx.x; r < Fp; r += gridDim.x) {   // a small grid: most searches have F = 0
+    const bool v = r < F;
+    const int q = v ? fail_list[r] : 0;
+    for (int e = threadIdx.x; e < row_u16; e += blockDim.x)
+      Qr[(size_t)r * row_u16 + e] = v ? Qp[(size_t)q * row_u16 + e] : (uint16_t)0;
+    if (qs_src)
+      for (int c = threadIdx.x; c < C; c += blockDim.x) qs_dst[(size_t)r * C + c] = v ? qs_src[(size_t)q * C + c] : 1.f;
+    const uint64_t t = (v && tau_src) ? tau_src[q] : 0ull;
+    if (threadIdx.x == 0) tbest[r] = 0ull;
+    for (int sl = threadIdx.x; sl < NS; sl += blockDim.x) {
+      tau[(size_t)sl * m_pad + r] = t;
+      cnt[(size_t)sl * m_pad + r] = 0;
+    }
   }
 }
 
 cudaError_t launch_repair_setup(const void* Qp, int row_u16, const int32_t* fail_list, const int32_t* fail_count,
-                                void* Qr, const uint64_t* tau_src, uint64_t* tau, int32_t* cnt, int NS, int m_pad,
+                                void* Qr, const uint64_t* tau_src, uint64_t* tau, unsigned long long* tbest, int32_t* cnt,
+                                int NS, int m_pad,
                                 int m_max, int32_t* m_out, const float* qs_src, float* qs_dst, int C, cudaStream_t s) {
-  const int rows = (m_max + 127) / 128 * 128;
+  const int rows = std::min((m_max + 127) / 128 * 128, 592);
   k_repair_setup<<<rows, 128, 0, s>>>((const uint16_t*)Qp, row_u16, fail_list, fail_count, (uint16_t*)Qr, tau_src, tau,
-                                      cnt, NS, m_pad, m_out, qs_src, qs_dst, C);
+                                      tbest, cnt, NS, m_pad, m_out, qs_src, qs_dst, C);
   return cudaGetLastError();
 }
 

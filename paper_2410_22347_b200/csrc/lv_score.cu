@@ -6,16 +6,17 @@
 //     fast epilogue warps, double-buffered across units), so the MMA reads only B from smem;
 //   B operand = 128-row tiles of X_low streamed by TMA through a STAGES-deep mbarrier ring;
 //   D = fp32 accumulators in TMEM, NACC buffers of 128 columns (the 512 - d columns left by A).
-// Epilogue (16 warps, 4 per SM sub-partition): thread = (query = TMEM lane, 32-column quarter
-// of the tile); tcgen05.ld.32x32b.x32 gives 32 scores whose max is compared with the thread's
-// threshold.  A warp with hitting lanes broadcasts each hitting lane's 32 scores through a
-// 128-byte shared-memory row; lane j tests column j and the survivors are appended as 64-bit keys
-// (ordered score, ~original id) to the hitting lane's sub-list in global memory (L2) with
-// coalesced stores; a full sub-list is compacted by the warp to its top-R, raising its threshold.
+// Epilogue in two stages: 16 fast-path warps (thread = query = TMEM lane) load a
+// 64-column job with two tcgen05.ld.32x32b.x32, release the accumulator, and compare the two
+// 32-score maxima with the query's threshold; every hitting row's 32 scores go through a
+// shared-memory ring to one of two append warps, which own the candidate sub-lists of the unit's
+// queries and append the survivors as 64-bit keys (ordered score, ~original id) in global memory
+// (L2), compacting a sub-list to its top-R when it fills (raising its threshold).
 // The m x n score matrix never reaches HBM.
 //
-// Work: units (database chunk c, query tile p), chunk-major, round-robin over a persistent grid;
-// a unit claims a free candidate slot of its query tile (slot lists persist across units).
+// Work: units (database chunk c, query tile p), chunk-major, handed out dynamically over a
+// persistent grid; per unit an append warp claims a free sub-list of its query half (sub-lists
+// persist across units).
 #include <cfloat>
 
 #include "lv_common.cuh"
@@ -32,6 +33,10 @@ constexpr int kAppWarps = 2, kAppWarp0 = kEpiWarps + 2;
 constexpr int kThreads = 32 * (kEpiWarps + 2 + kAppWarps);
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kMaxKeysPerLane = 12;    // Cap <= 384
+// append warps compact a list early, at R + kEarly keys (measured: kEarly = 64 raised no fast-path
+// thresholds that mattered and cost compactions, cfg 2 / 3 main scan 2.09 / 2.29 -> 2.25 / 2.52 ms;
+// so only Cap triggers)
+constexpr int kEarly = 1 << 20;
 constexpr int kRing = 64;              // entries per append ring (power of two, >= 32 + 1)
 
 // Shared-memory epilogue state.  The fast-path warps (16) only filter: a 32 x 32 block of
@@ -264,6 +269,8 @@ __device__ __forceinline__ int warp_compact_fast(uint64_t* buf, int count, int R
 template <int kFmt, int kD, bool kSample>
 __global__ void __launch_bounds__(kThreads, 1)
     k_score_topr(const __grid_constant__ CUtensorMap tmap_xlow, const ScoreArgs a) {
+  // a repair pass with no failed queries: nothing to do (before any TMEM or barrier set-up)
+  if (a.m_dev != nullptr && *a.m_dev == 0) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base (SWIZZLE_128B atoms) as an offset into the shared array, so that every
   // access through it stays in the shared address space (LDS/STS, not generic LD/ST)
@@ -576,7 +583,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       // stored keys lie above it, or it is the start threshold that K4 verifies), so sub-list 0's;
       // the append warp raises it when a compaction of this unit's list raises that list's
       LV_CHECK(q < a.m_pad);
-      const uint64_t tk0 = (lists && qvalid) ? a.tau[q] : 0ull;
+      uint64_t tk0 = 0ull;
+      if (lists && qvalid) {
+        tk0 = a.tau[q];
+        const uint64_t tb = a.tbest[q];   // raised by other units' compactions
+        if (tb > tk0) tk0 = tb;
+      }
       float ts = qvalid ? thr_score(tk0) : FLT_MAX;   // padded queries never hit
       // int8: this query's scale for the unit's cluster view, and the threshold on accumulators
       const float qs = kI8 ? a.qscale[(size_t)q * a.C + ci[2]] : 1.f;
@@ -624,49 +636,66 @@ __global__ void __launch_bounds__(kThreads, 1)
         const long long e1 = clk_stats ? clock64() : 0;
         tc::tc_fence_after();
         float bm = -FLT_MAX;   // sample stage: running block maximum of the job
-        // one 32-column half of the job: (mask), raw output, max, threshold test, push of the
-        // hitting rows
-        auto half = [&](float (&v)[32], const int h) {
-          const int hpos = base_pos + 32 * h;
+        // int8: v holds s32 accumulators; the score of column j is fl(qs * float(acc_j))
+        auto score_of = [&](float raw) -> float {
+          if (!kI8) return raw;
+          const int iv = __float_as_int(raw);
+          return iv == INT_MIN ? -FLT_MAX : qs * (float)iv;
+        };
+        // (mask of a partial last tile) and the raw-score debug output of the job's halves
+        auto prep = [&](float (*v)[32]) {
           if (t == t_last) {   // a cluster segment's last tile may be partial
-            const int tv = a.tile_valid[t_last] - (jh * kJobCols + 32 * h);
-            if (tv < 32) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (j >= tv) v[j] = kI8 ? __int_as_float(INT_MIN) : -FLT_MAX;
+            for (int h = 0; h < kJV; ++h) {
+              const int tv = a.tile_valid[t_last] - (jh * kJobCols + 32 * h);
+              if (tv < 32) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (j >= tv) v[h][j] = kI8 ? __int_as_float(INT_MIN) : -FLT_MAX;
+              }
             }
           }
-          // int8: v holds s32 accumulators; the score of column j is fl(qs * float(acc_j))
-          auto score_of = [&](float raw) -> float {
-            if (!kI8) return raw;
-            const int iv = __float_as_int(raw);
-            return iv == INT_MIN ? -FLT_MAX : qs * (float)iv;
-          };
           if (a.raw != nullptr) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + hpos + j] = score_of(v[j]);
-            LV_CHECK(q < a.m_pad && (int64_t)(hpos + 32) <= a.n_pad);
+            for (int h = 0; h < kJV; ++h) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) a.raw[(size_t)q * a.n_pad + base_pos + 32 * h + j] = score_of(v[h][j]);
+              LV_CHECK(q < a.m_pad && (int64_t)(base_pos + 32 * h + 32) <= a.n_pad);
+            }
           }
-          float mx;
-          bool hit;
+        };
+        // maxima of the halves (independent chains, interleaved) and their threshold tests
+        auto maxes = [&](float (*v)[32], float* mx, bool* hit) {
           if (kI8) {
-            // tree of integer maxima (a 31-deep dependent chain would expose its latency)
-            int t16[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) t16[j] = max(__float_as_int(v[j]), __float_as_int(v[j + 16]));
+            for (int h = 0; h < kJV; ++h) {
+              // tree of integer maxima (a 31-deep dependent chain would expose its latency)
+              int t16[16];
 #pragma unroll
-            for (int w = 8; w >= 1; w >>= 1)
+              for (int j = 0; j < 16; ++j) t16[j] = max(__float_as_int(v[h][j]), __float_as_int(v[h][j + 16]));
 #pragma unroll
-              for (int j = 0; j < w; ++j) t16[j] = max(t16[j], t16[j + w]);
-            const int im = t16[0];
-            mx = im == INT_MIN ? -FLT_MAX : qs * (float)im;
-            hit = im >= ti && im > INT_MIN;
+              for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+                for (int j = 0; j < w; ++j) t16[j] = max(t16[j], t16[j + w]);
+              const int im = t16[0];
+              mx[h] = im == INT_MIN ? -FLT_MAX : qs * (float)im;
+              hit[h] = im >= ti && im > INT_MIN;
+            }
           } else {
-            mx = v[0];
 #pragma unroll
-            for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
-            hit = mx >= ts && mx > -FLT_MAX;
+            for (int h = 0; h < kJV; ++h) mx[h] = v[h][0];
+#pragma unroll
+            for (int j = 1; j < 32; ++j)
+#pragma unroll
+              for (int h = 0; h < kJV; ++h) mx[h] = fmaxf(mx[h], v[h][j]);
+#pragma unroll
+            for (int h = 0; h < kJV; ++h) hit[h] = mx[h] >= ts && mx[h] > -FLT_MAX;
           }
+        };
+        // one 32-column half after its maximum: block maxima (sample stage) or the push of the
+        // hitting rows
+        auto half = [&](float (&v)[32], const int h, const float mx, const bool hit) {
+          const int hpos = base_pos + 32 * h;
           if (kSample) {
             // sample stage: record block maxima (query q; blocks of 32 database rows when
             // a.flags & 8, else of the job's 64: fine blocks keep the threshold estimate of
@@ -718,20 +747,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         {
           long long eld = 0;
+          // both halves' loads, one wait, then the accumulator goes back to the MMA before any
+          // filtering (the shortest hold)
+          float v[kJV][32];
+          const long long l0 = clk_stats ? clock64() : 0;
 #pragma unroll
-          for (int h = 0; h < kJV; ++h) {
-            float v[32];
-            const long long l0 = clk_stats ? clock64() : 0;
-            tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kAccN + acol + (uint32_t)(32 * h), v);
-            tc::tmem_wait_ld();
-            if (clk_stats) eld += clock64() - l0;
-            if (h + 1 == kJV) {
-              tc::tc_fence_before();
-              __syncwarp();
-              if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
-            }
-            if (skip_topr) continue;
-            half(v, h);
+          for (int h = 0; h < kJV; ++h)
+            tc::tmem_ld_32x32b_x32(tm_lane + (uint32_t)accb * kAccN + acol + (uint32_t)(32 * h), v[h]);
+          tc::tmem_wait_ld();
+          if (clk_stats) eld += clock64() - l0;
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_u32(acc_empty_u + 8u * (uint32_t)accb);
+          if (!skip_topr) {
+            prep(v);
+            float mx[kJV];
+            bool hit[kJV];
+            maxes(v, mx, hit);
+#pragma unroll
+            for (int h = 0; h < kJV; ++h) half(v[h], h, mx[h], hit[h]);
           }
           if (clk_stats) {
             ek[0] += (unsigned long long)(e1 - e0);
@@ -835,6 +869,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       uint64_t* const lbase = a.cand + ((size_t)sl * a.m_pad + (size_t)qt * 128) * (size_t)a.Cap;   // row r: + r * Cap
       const int Cap = a.Cap;
+      const int Ctrig = min(Cap, a.R + kEarly);
       // Entries are consumed in batches: the ready prefix of up to 32 (lane e probes entry head + e;
       // the warp barrier passes the acquires on), one entry per lane.  Room first: every sub-list
       // of the batch gets 32 key positions per entry it has in the batch (a warp-wide compaction
@@ -847,16 +882,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       while (!end) {
         int nready;
         {
-          uint32_t spins = 0;
-          for (;;) {
-            const int te = head + lane;
-            const bool rdy = tc::mbar_test_wait(&S.rfull[rg][te & (kRing - 1)], (uint32_t)(te / kRing) & 1u);
-            const uint32_t b = __ballot_sync(0xffffffffu, rdy);
-            nready = b == 0xffffffffu ? 32 : __ffs(~b) - 1;
-            if (nready > 0) break;
-            __nanosleep(20);
-            if (++spins > (1u << 28)) __trap();
-          }
+          // sleep on the head entry's barrier (woken by its arrive: no polling traffic on the
+          // barrier unit the MMA pipeline shares), then probe the entries behind it
+          tc::mbar_wait_sleep(&S.rfull[rg][head & (kRing - 1)], (uint32_t)(head / kRing) & 1u);
+          const int te = head + lane;
+          const bool rdy = lane == 0 || tc::mbar_test_wait(&S.rfull[rg][te & (kRing - 1)], (uint32_t)(te / kRing) & 1u);
+          const uint32_t b = __ballot_sync(0xffffffffu, rdy);
+          nready = b == 0xffffffffu ? 32 : __ffs(~b) - 1;
         }
         __syncwarp();
         const long long c0 = clk_stats ? clock64() : 0;
@@ -888,15 +920,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t m = lane < nb ? hits() : 0u;
         // room: a row's candidates of the batch must fit its sub-list; else compact it (raising its
         // threshold, so its entries are re-filtered), and if they still do not fit, cut the batch
-        // after the row's first entry (one entry always fits a compacted list: <= Cap - 64 keys)
+        // after the row's first entry (one entry always fits a compacted list: <= Cap - 64 keys).
+        // The common case is one test: every row has room for all of the batch's candidates.
+        // A list is compacted early, once it would pass Ctrig = R + kEarly keys (its R-th key is
+        // then a tighter threshold than the sampled one, and the raise reaches the fast path
+        // through traise), and must be when it would pass Cap.
+        const int tot = __reduce_add_sync(0xffffffffu, __popc(m));
+        if (__any_sync(0xffffffffu, lane < nb && st_cnt[lr] + tot > Ctrig))
 #pragma unroll 1
         for (int pass = 0; pass < 2; ++pass) {
           const bool inb = lane < nb;
           const uint32_t same = __match_any_sync(0xffffffffu, inb ? lr : 64 + lane);
           const int need = __reduce_add_sync(same, __popc(m));
-          const bool viol = inb && st_cnt[lr] + need > Cap;
+          const int cl = inb ? st_cnt[lr] : 0;
+          // pass 0: compact the lists (holding more than R keys) that would pass Ctrig; pass 1:
+          // only Cap binds
+          const bool viol = inb && cl + need > (pass == 0 ? Ctrig : Cap) && (pass == 1 || cl > a.R);
           const uint32_t vb = __ballot_sync(0xffffffffu, viol);
-          if (vb == 0u) break;
+          if (vb == 0u) {
+            if (pass == 0) continue;
+            break;
+          }
           if (pass == 0) {
             uint32_t todo = vb;
             while (todo) {
@@ -910,6 +954,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (nthr > st_tk[lrL]) st_tk[lrL] = nthr;
                 S.traise[i & 1][rL] = ((unsigned long long)(i + 1) << 32) |
                                       (unsigned long long)__float_as_uint(thr_score(st_tk[lrL]));
+                atomicMax(a.tbest + (size_t)qt * 128 + rL, st_tk[lrL]);   // for the query's later units
               }
               ++ncompact;
               __syncwarp();
@@ -920,10 +965,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane >= nb) m = 0u;
           }
         }
-        if (lane < nb) {
+        if (lane < nb && m != 0u) {
           const uint64_t tk = st_tk[lr];
           uint64_t* const bz = lbase + (size_t)r * (size_t)Cap;
-          while (m) {
+          if ((uint32_t)tk == 0xffffffffu || tk == 0ull) {
+            // thresholds of the form (b << 32) - 1 (all the selects' and compactions' except an
+            // exact cut) or none: score >= ts  <=>  key > tk, so every candidate is a survivor and
+            // the entry takes its positions with one atomic
+            int pos = atomicAdd(&st_cnt[lr], __popc(m));
+            LV_CHECK(pos + __popc(m) <= Cap);
+            nappend += (unsigned)__popc(m);
+            while (m) {
+              const int col = __ffs(m) - 1;
+              m &= m - 1u;
+              const float s = reinterpret_cast<const float*>(src)[4 * ((col / 4 + sj) & 7) + col % 4];
+              const int32_t id = a.perm ? S.rid[rg][sj][col] : hp + col;
+              bz[pos++] = make_key(s, id);
+            }
+          }
+          while (m) {   // exact-cut threshold: the id decides ties of the threshold score
             const int col = __ffs(m) - 1;
             m &= m - 1u;
             const float s = reinterpret_cast<const float*>(src)[4 * ((col / 4 + sj) & 7) + col % 4];
@@ -964,9 +1024,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         atomicAnd(reinterpret_cast<unsigned long long*>(a.slot_busy) + (size_t)qt * kAppWarps + rg, ~(1ull << sl));
       }
     }
-    if (count_stats && lane == 0) {
-      atomicAdd(a.stats + 1, (unsigned long long)nappend);
-      atomicAdd(a.stats + 2, (unsigned long long)ncompact);
+    if (count_stats) {
+      const unsigned tot = __reduce_add_sync(0xffffffffu, nappend);   // appends are counted per lane
+      if (lane == 0) {
+        atomicAdd(a.stats + 1, (unsigned long long)tot);
+        atomicAdd(a.stats + 2, (unsigned long long)ncompact);
+      }
     }
     if (clk_stats && lane == 0) {
       atomicAdd(a.stats + 1, nent);
