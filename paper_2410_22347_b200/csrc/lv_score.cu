@@ -46,7 +46,6 @@ constexpr int kRing = 64;              // entries per append ring (power of two,
 // survivors.  So the hit path never holds a fast-path warp.
 struct EpiShared {
   float rs[kAppWarps][kRing][32];      // entry: the hitting row's 32 scores (int8: converted)
-  int32_t rid[kAppWarps][kRing][32];   // entry: the 32 columns' ids (perm != nullptr)
   uint64_t rfull[kAppWarps][kRing];    // entry ready: mbarrier (count 1), phase = ticket / kRing
   int2 rmeta[kAppWarps][kRing];        // entry: x = row (-1: end of unit), y = first column
   unsigned long long traise[2][128];   // per unit parity and row: ((unit + 1) << 32) | raised threshold score bits
@@ -601,11 +600,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int g = J / kJobsPerTile, jh = J % kJobsPerTile;   // global tile ordinal, column block
         const int t = t0 + (g - tiles_before) * tstride;
         const int base_pos = t * kN + jh * kJobCols;
-        // GleanVec: original ids of this lane's columns, loaded now so the loads overlap the
-        // accumulator wait and the max (they are only needed when a block hits)
-        int32_t my_id[kJV];
-#pragma unroll
-        for (int h = 0; h < kJV; ++h) my_id[h] = (!kSample && a.perm) ? __ldg(a.perm + base_pos + 32 * h + lane) : 0;
         LV_CHECK(t >= t0 && t < t1 && (int64_t)(base_pos + kJobCols) <= a.n_pad);
         if (lists) {   // a threshold the append warp raised for this unit's query
           const unsigned long long w = S.traise[i & 1][row];
@@ -724,10 +718,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (clk_stats) pk[1] += (unsigned long long)(clock64() - pw0);
           }
           tk = __shfl_sync(0xffffffffu, tk, 0);
-          if (a.perm) {   // every lane writes its column's id into each hitting row's entry
-            const int32_t idh = my_id[h];
-            for (int e = 0; e < n; ++e) S.rid[rg][(tk + e) & (kRing - 1)][lane] = idh;
-          }
           const int slot = (tk + __popc(hb & lt)) & (kRing - 1);
           if (hit) {
             float4* dst = reinterpret_cast<float4*>(S.rs[rg][slot]);
@@ -737,9 +727,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                    score_of(v[4 * j + 3]));
             S.rmeta[rg][slot] = make_int2(row, hpos);
           }
-          // the ids of the other lanes are ordered before the arrive (release) by the warp barrier
-          __syncwarp();
+          // the arrive (release) orders the lane's own entry writes; the append warp looks the
+          // survivors' ids up in perm itself
           if (hit) tc::mbar_arrive(&S.rfull[rg][slot]);
+          __syncwarp();
           if (clk_stats) {
             pk[0] += (unsigned long long)(clock64() - p0);
             ++npush;
@@ -979,7 +970,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int col = __ffs(m) - 1;
               m &= m - 1u;
               const float s = reinterpret_cast<const float*>(src)[4 * ((col / 4 + sj) & 7) + col % 4];
-              const int32_t id = a.perm ? S.rid[rg][sj][col] : hp + col;
+              const int32_t id = a.perm ? __ldg(a.perm + hp + col) : hp + col;
               bz[pos++] = make_key(s, id);
             }
           }
@@ -987,7 +978,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int col = __ffs(m) - 1;
             m &= m - 1u;
             const float s = reinterpret_cast<const float*>(src)[4 * ((col / 4 + sj) & 7) + col % 4];
-            const int32_t id = a.perm ? S.rid[rg][sj][col] : hp + col;
+            const int32_t id = a.perm ? __ldg(a.perm + hp + col) : hp + col;
             const uint64_t key = make_key(s, id);
             if (key > tk) {
               const int pos = atomicAdd(&st_cnt[lr], 1);
