@@ -450,6 +450,12 @@ lv_status set_operands(lv_index* ix, const float* A_src, const float* B_src, cud
   LV_CUDA(cudaMemcpyAsync(ix->B, B_src, bytes, cudaMemcpyDeviceToDevice, s));
   LV_CUDA(lv::launch_split3(ix->A, false, Nc, Nc, D, ix->Kp, ix->A_planes, s));
   LV_CUDA(lv::launch_split3(ix->B, false, Nc, Nc, D, ix->Kp, ix->B_planes, s));
+  if (ix->Bh_planes) {   // rebuilt by the next encode of fp16 rows
+    cudaFree(ix->Bh_planes);
+    cudaFree(ix->b_scale);
+    ix->Bh_planes = nullptr;
+    ix->b_scale = nullptr;
+  }
   if (ix->flex) {
     ix->hA.resize((size_t)Nc * D);
     LV_CUDA(cudaMemcpyAsync(ix->hA.data(), ix->A, bytes, cudaMemcpyDeviceToHost, s));
@@ -722,8 +728,28 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
   // cudaMalloc between two event records would count as kernel time)
   const size_t fsz = ix->full == LV_F16 ? 2 : 4;
   if (cudaMalloc(&ix->X_full, fsz * n * ix->D) != cudaSuccess) return fail(LV_ENOMEM, "X_full");
+  // fp16 rows: B as row-scaled fp16 planes (built once per operand set, outside the timed window)
+  const bool direct = x_dtype == LV_F16 && env_double("LV_K6_DIRECT", 1.0) != 0.0;
+  if (direct && !ix->Bh_planes) {
+    const int Nc = ix->C * ix->d;
+    if (cudaMalloc(&ix->Bh_planes, (size_t)3 * Nc * ix->Kp * 2) != cudaSuccess ||
+        cudaMalloc(&ix->b_scale, sizeof(float) * Nc) != cudaSuccess)
+      return fail(LV_ENOMEM, "lv_encode_database: fp16 B planes");
+    LV_CUDA(lv::launch_split_h(ix->B, Nc, ix->D, ix->Kp, ix->Bh_planes, ix->b_scale, s));
+    lv_status hs = make_tmap(&ix->tmap_bh, ix->Bh_planes, 3 * (int64_t)Nc, ix->Kp, 64, false, ix->d);
+    if (hs) return hs;
+  }
+  const double hplanes = env_double("LV_K6_HPLANES", 0.0);   // 0: two for bf16 storage, else three
   LV_CUDA(cudaEventRecord(ev[1], s));
-  if (ix->low == LV_I8) {   // (ev[0] is unused: the sort is timed by ev[4..7])
+  if (direct) {
+    const int ot = ix->low == LV_I8 ? 2 : (ix->low == LV_BF16 ? 0 : 1);
+    LV_CUDA(lv::launch_encode_h(&ix->tmap_bh, ix->b_scale, X, ix->D, ix->Kp, ix->d, ix->C * ix->d, ix->perm, dwrow, dorder,
+                                nt, ix->low == LV_I8 ? (void*)xf : ix->X_low, ot, hplanes >= 3.0, s));
+    if (ix->low == LV_I8) {
+      LV_CUDA(lv::launch_i8_db_scales(xf, nt, ix->d, dwrow, C, amax, ix->i8_delta, s));
+      LV_CUDA(lv::launch_i8_db_codes(xf, nt, ix->d, dwrow, ix->i8_delta, reinterpret_cast<int8_t*>(ix->X_low), s));
+    }
+  } else if (ix->low == LV_I8) {   // (ev[0] is unused: the sort is timed by ev[4..7])
     LV_CUDA(lv::launch_encode_tc(&ix->tmap_b, X, x_dtype == LV_F16, ix->D, ix->Kp, ix->d, ix->C * ix->d, ix->perm, dwrow,
                                  dorder, nt, xf, 2, true, s));
     LV_CUDA(lv::launch_i8_db_scales(xf, nt, ix->d, dwrow, C, amax, ix->i8_delta, s));
@@ -1434,6 +1460,8 @@ void lv_index_destroy(lv_index* ix) {
   cudaFree(ix->dbg_stats);
   cudaFree(ix->A_planes);
   cudaFree(ix->B_planes);
+  cudaFree(ix->Bh_planes);
+  cudaFree(ix->b_scale);
   for (auto& g : ix->ev_pending)
     for (auto e : g) cudaEventDestroy(e);
   for (auto e : ix->ev_pool) cudaEventDestroy(e);

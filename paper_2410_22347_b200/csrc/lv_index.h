@@ -80,6 +80,9 @@ struct lv_index {
   CUtensorMap tmap_a;          // A planes, 128-row x 64-column boxes
   void* B_planes = nullptr;    // bf16 [3][C*d][Kp]: B split, K6 operand
   CUtensorMap tmap_b;          // B planes, d-row x 64-column boxes
+  void* Bh_planes = nullptr;   // fp16 [3][C*d][Kp]: row-scaled B, bs = h + 2^-11 (m + l) (K6 for fp16 rows, R23)
+  float* b_scale = nullptr;    // [C*d] the rows' power-of-two scales 2^e_i (b = bs 2^e_i)
+  CUtensorMap tmap_bh;         // Bh planes, d-row x 64-column boxes
   float enc_ms[3] = {0, 0, 0}; // last encode: sort, K6, full copy (lv_encode_timing)
   bool enc_timed = false;
   int64_t n = 0, n_pad = 0;

@@ -96,7 +96,13 @@ cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a,
 // K6 on tensor cores: out[r, :] = RNE(B_{c(r)} X[perm[r], :]) for 128-row tiles (tile_wrow[2t] = c*d),
 // CTA i encodes tile order[i] (nullptr: tile i)
 // (three bf16 planes; two for bf16 storage when !planes3)
-size_t encode_smem(int d, int np);
+size_t encode_smem(int d, int nxp, int nbp);
+// fp16 rows (R23): the row is its own fp16 operand plane; B as row-scaled fp16 planes
+// (launch_split_h: out fp16 [3][rows][Kp], scale[rows]); two planes for bf16 storage when !planes3
+cudaError_t launch_split_h(const float* B, int rows, int D, int Kp, void* out, float* scale, cudaStream_t s);
+cudaError_t launch_encode_h(const CUtensorMap* tmap_bh, const float* b_scale, const void* X, int D, int Kp, int d, int Nc,
+                            const int32_t* perm, const int32_t* tile_wrow, const int32_t* order, int64_t ntiles,
+                            void* out, int out_type, bool planes3, cudaStream_t s);
 // out_type: 0 bf16, 1 fp16, 2 fp32 (the int8 path's unrounded x_low)
 cudaError_t launch_encode_tc(const CUtensorMap* tmap_b, const void* X, bool x_f16, int D, int Kp, int d, int Nc,
                              const int32_t* perm, const int32_t* tile_wrow, const int32_t* order, int64_t ntiles,

@@ -223,55 +223,86 @@ cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a,
 // scheduler: one warp per SMSP could not issue the split fast enough) read each row's 64-element
 // K block with coalesced 16-byte loads, split it in registers and store the planes in the
 // SWIZZLE_128B K-major layout the MMA descriptor expects (16-byte chunk c of row r at chunk
-// c ^ (r & 7)); B planes come by TMA.  The same warps then round the accumulators and store the
-// tile.  One CTA per tile.
-constexpr int kEnPW = 8;                              // producer / epilogue warps
+// c ^ (r & 7)); B planes come by TMA.  Four epilogue warps round the accumulators and store the
+// tile.  Persistent: one CTA per SM walks the tile order with stride gridDim.x; the shared-memory
+// ring and the producers' register ring run across tile boundaries, so the next tile's rows are
+// already in flight while a tile's accumulators are drained (two accumulator buffers when
+// 2 (nH + 1) d <= 512 columns, else one).
+constexpr int kEnPW = 8;                              // producer warps
+constexpr int kEnEW = 4;                              // epilogue warps (one per TMEM lane quarter)
 constexpr int kEnRows = 128 / kEnPW;                  // tile rows per producer warp
-constexpr int kEnThreads = 64 + 32 * kEnPW;
+constexpr int kEnThreads = 64 + 32 * (kEnPW + kEnEW);
 
 __host__ __device__ constexpr int enc_hh(int d) { return (512 / d - 1) < 3 ? (512 / d - 1) : 3; }
 // np planes of the X tile and of the B block per stage
-__host__ __device__ constexpr uint32_t enc_stage_bytes(int d, int np) {
-  return (uint32_t)np * (128u * 128u + (uint32_t)d * 128u);
+// nxp planes of the X tile and nbp planes of the B block per stage
+__host__ __device__ constexpr uint32_t enc_stage_bytes(int d, int nxp, int nbp) {
+  return (uint32_t)nxp * 128u * 128u + (uint32_t)nbp * (uint32_t)d * 128u;
 }
-// as many stages (<= 3) as fit the 227 KB opt-in limit
-__host__ __device__ constexpr int enc_stages(int d, int np) {
-  return 3 * enc_stage_bytes(d, np) + 1280 <= 232448 ? 3 : (2 * enc_stage_bytes(d, np) + 1280 <= 232448 ? 2 : 1);
+// as many stages (<= 4) as fit the 227 KB opt-in limit
+__host__ __device__ constexpr int enc_stages(int d, int nxp, int nbp) {
+  return 4 * enc_stage_bytes(d, nxp, nbp) + 1280 <= 232448
+             ? 4
+             : (3 * enc_stage_bytes(d, nxp, nbp) + 1280 <= 232448
+                    ? 3
+                    : (2 * enc_stage_bytes(d, nxp, nbp) + 1280 <= 232448 ? 2 : 1));
 }
-size_t encode_smem(int d, int np) { return enc_stages(d, np) * enc_stage_bytes(d, np) + 1024 + 256; }
+size_t encode_smem(int d, int nxp, int nbp) { return enc_stages(d, nxp, nbp) * enc_stage_bytes(d, nxp, nbp) + 1024 + 256; }
 
 // kNP = 3: v = h + m + l, six products (the default); kNP = 2: v = h + m (16 significant bits),
 // products hh, hm, mh, bf16 storage only, opt-in (LV_K6_PLANES=2): the dropped terms are
 // <= 2^-18 sum|b x| and flip 0.34 % of the bf16 outputs (three planes: 0.015 %; R18).
-template <bool kXF16, int kD, int kOut, int kNP>
+//
+// kDirect (fp16 rows, R23): an fp16 row is one exact fp16 operand plane, so the rows go
+// to shared memory as they are (no split) and only B is split, into kNP fp16 planes of the row-
+// scaled weights bs = b 2^-e_i (k_split_h): bs = h + 2^-11 (m + l).  Products x*h (nH accumulators)
+// and x*m, x*l (one accumulator, scaled by 2^-11 in the epilogue); the sum is multiplied by the
+// row scale 2^e_i (exact).  kNP = 2 carries 22 bits of b, kNP = 3 all 24: two or three products
+// instead of six.
+template <bool kXF16, int kD, int kOut, int kNP, bool kDirect>
 __global__ void __launch_bounds__(kEnThreads, 1)
     k_encode_tc(const __grid_constant__ CUtensorMap tmap_b, const void* __restrict__ X, int D, int Kp, int Nc, int vec,
                 const int32_t* __restrict__ perm, const int32_t* __restrict__ tile_wrow,
-                const int32_t* __restrict__ tile_order, void* __restrict__ out) {
+                const int32_t* __restrict__ tile_order, int ntiles, const float* __restrict__ b_scale,
+                void* __restrict__ out) {
+  static_assert(!kDirect || kXF16, "the direct path needs fp16 rows");
   constexpr int nH = enc_hh(kD);                    // hh accumulators (columns nH*d .. : cross terms)
+  constexpr int nAcc = nH + 1;                      // accumulators per tile
+  constexpr int kAB = 2 * nAcc * kD <= 512 ? 2 : 1; // accumulator buffers (tiles in TMEM at once)
+  constexpr int kNXP = kDirect ? 1 : kNP;           // X planes per stage
   constexpr uint32_t kXPlane = 128u * 128u;         // 128 rows x 64 bf16
   constexpr uint32_t kBPlane = (uint32_t)kD * 128u; // d rows x 64 bf16
-  constexpr uint32_t kStage = enc_stage_bytes(kD, kNP);
-  constexpr int kEnStages = enc_stages(kD, kNP);
-  constexpr int kProds = kNP == 3 ? 6 : 3;
+  constexpr uint32_t kStage = enc_stage_bytes(kD, kNXP, kNP);
+  constexpr int kEnStages = enc_stages(kD, kNXP, kNP);
+  constexpr int kProds = kDirect ? kNP : (kNP == 3 ? 6 : 3);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kEnStages * kStage);
   uint64_t* full = bars;
   uint64_t* empty = bars + kEnStages;
-  uint64_t* acc_full = bars + 2 * kEnStages;
-  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint64_t* acc_full = bars + 2 * kEnStages;        // [kAB] MMA -> epilogue
+  uint64_t* acc_empty = acc_full + 2;               // [kAB] epilogue -> MMA
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = tile_order ? tile_order[blockIdx.x] : (int)blockIdx.x;
   const int nkb = Kp / 64;
-  const int wrow = tile_wrow[2 * tile];             // c * d: first B row of the tile's cluster (per 64-row table)
+  // persistent: this CTA encodes tiles order[blockIdx.x + j * gridDim.x], j < my_tiles (grid <= ntiles);
+  // the CTAs in flight together work on one window of the order
+  const int G = (int)gridDim.x;
+  const int my_tiles = (ntiles - (int)blockIdx.x + G - 1) / G;
+  auto tile_of = [&](int j) {
+    const int ti = (int)blockIdx.x + j * G;
+    return tile_order ? tile_order[ti] : ti;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kEnStages; ++s) {
       tc::mbar_init(full + s, 1 + kEnPW);           // TMA expect_tx arrive + the producer warps
       tc::mbar_init(empty + s, 1);
     }
-    tc::mbar_init(acc_full, 1);
+    for (int b = 0; b < kAB; ++b) {
+      tc::mbar_init(acc_full + b, 1);
+      tc::mbar_init(acc_empty + b, kEnEW);
+    }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmap_b);
   }
@@ -285,51 +316,65 @@ __global__ void __launch_bounds__(kEnThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        tc::mbar_wait(empty + stage, phase ^ 1);
-        tc::mbar_arrive_expect_tx(full + stage, (uint32_t)kNP * kBPlane);
-        uint8_t* st = smem + stage * kStage + (uint32_t)kNP * kXPlane;
-        for (int p = 0; p < kNP; ++p)
-          tc::tma_load_2d(st + p * kBPlane, &tmap_b, full + stage, kb * 64, p * Nc + wrow);
-        if (++stage == kEnStages) { stage = 0; phase ^= 1; }
+      int wrow = tile_wrow[2 * tile_of(0)];         // c * d: first B row of the tile's cluster (per 64-row table)
+      for (int j = 0; j < my_tiles; ++j) {
+        const int wrow_next = j + 1 < my_tiles ? tile_wrow[2 * tile_of(j + 1)] : 0;
+        for (int kb = 0; kb < nkb; ++kb) {
+          tc::mbar_wait(empty + stage, phase ^ 1);
+          tc::mbar_arrive_expect_tx(full + stage, (uint32_t)kNP * kBPlane);
+          uint8_t* st = smem + stage * kStage + (uint32_t)kNXP * kXPlane;
+          for (int p = 0; p < kNP; ++p)
+            tc::tma_load_2d(st + p * kBPlane, &tmap_b, full + stage, kb * 64, p * Nc + wrow);
+          if (++stage == kEnStages) { stage = 0; phase ^= 1; }
+        }
+        wrow = wrow_next;
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = tc::make_idesc_f16(128, kD, true);
+    constexpr uint32_t idesc = tc::make_idesc_f16(128, kD, !kDirect);
     int stage = 0;
     uint32_t phase = 0;
     const bool issuer = tc::elect_one();
-    for (int kb = 0; kb < nkb; ++kb) {
-      tc::mbar_wait(full + stage, phase);
-      tc::tc_fence_after();
-      if (issuer) {
-        const uint32_t st = tc::smem_u32(smem + stage * kStage);
-        const uint32_t d_big = tmem + (uint32_t)(kb % nH) * (uint32_t)kD, d_small = tmem + (uint32_t)nH * (uint32_t)kD;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-#pragma unroll
-          for (int pr = 0; pr < kProds; ++pr) {
-            const uint32_t xa = st + (uint32_t)kPjProd[pr][0] * kXPlane + (uint32_t)kk * 32u;
-            const uint32_t ba = st + (uint32_t)kNP * kXPlane + (uint32_t)kPjProd[pr][1] * kBPlane + (uint32_t)kk * 32u;
-            if (pr == 0)
-              tc::mma_f16_ss(d_big, tc::make_sdesc(xa, 128), tc::make_sdesc(ba, 128), idesc, (kb >= nH || kk > 0) ? 1u : 0u);
-            else
-              tc::mma_f16_ss(d_small, tc::make_sdesc(xa, 128), tc::make_sdesc(ba, 128), idesc,
-                             (kb | kk | (pr - 1)) != 0 ? 1u : 0u);
-          }
-        }
-        tc::mma_commit(empty + stage);
-        if (kb + 1 == nkb) tc::mma_commit(acc_full);
+    for (int j = 0; j < my_tiles; ++j) {
+      const int buf = j % kAB;
+      if (j >= kAB) {                               // the epilogue has drained this buffer's previous tile
+        tc::mbar_wait(acc_empty + buf, (uint32_t)((j / kAB - 1) & 1));
+        tc::tc_fence_after();
       }
-      __syncwarp();
-      if (++stage == kEnStages) { stage = 0; phase ^= 1; }
+      const uint32_t acc = tmem + (uint32_t)(buf * nAcc * kD);
+      for (int kb = 0; kb < nkb; ++kb) {
+        tc::mbar_wait(full + stage, phase);
+        tc::tc_fence_after();
+        if (issuer) {
+          const uint32_t st = tc::smem_u32(smem + stage * kStage);
+          const uint32_t d_big = acc + (uint32_t)(kb % nH) * (uint32_t)kD, d_small = acc + (uint32_t)nH * (uint32_t)kD;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+#pragma unroll
+            for (int pr = 0; pr < kProds; ++pr) {
+              const uint32_t xa = st + (kDirect ? 0u : (uint32_t)kPjProd[pr][0]) * kXPlane + (uint32_t)kk * 32u;
+              const uint32_t ba = st + (uint32_t)kNXP * kXPlane +
+                                  (kDirect ? (uint32_t)pr : (uint32_t)kPjProd[pr][1]) * kBPlane + (uint32_t)kk * 32u;
+              if (pr == 0)
+                tc::mma_f16_ss(d_big, tc::make_sdesc(xa, 128), tc::make_sdesc(ba, 128), idesc, (kb >= nH || kk > 0) ? 1u : 0u);
+              else
+                tc::mma_f16_ss(d_small, tc::make_sdesc(xa, 128), tc::make_sdesc(ba, 128), idesc,
+                               (kb | kk | (pr - 1)) != 0 ? 1u : 0u);
+            }
+          }
+          tc::mma_commit(empty + stage);
+          if (kb + 1 == nkb) tc::mma_commit(acc_full + buf);
+        }
+        __syncwarp();
+        if (++stage == kEnStages) { stage = 0; phase ^= 1; }
+      }
     }
-  } else {
+  } else if (warp < 2 + kEnPW) {
     // producers: warp w (2..9) owns tile rows kEnRows*(w-2) ..; each lane loads 16 bytes of one
     // row per step (4 fp32 or 8 fp16 elements: 16 or 8 lanes per 64-element row, 2 or 4 rows per
-    // step).  The loads of K block kb+1 are issued before the stage wait and the plane stores of
-    // block kb (register double buffer), so two blocks of row reads are in flight per warp and
-    // they overlap the MMAs.
+    // step).  The (tile, K block) pairs of the CTA form one sequence; the loads run kRing - 1 blocks
+    // ahead of the plane stores (register ring), across tile boundaries, so row reads stay in flight
+    // while a tile's accumulators are drained.
     constexpr int kEPL = kXF16 ? 8 : 4;          // elements per lane and step
     constexpr int kLPR = 64 / kEPL;              // lanes per row
     constexpr int kRPS = 32 / kLPR;              // rows per step
@@ -337,19 +382,24 @@ __global__ void __launch_bounds__(kEnThreads, 1)
     const int pw = warp - 2;
     const int rsub = lane / kLPR, lc = lane % kLPR;
     int srcs[kIt];
-    {
-      const int my_src = perm[(size_t)tile * 128 + pw * kEnRows + (lane % kEnRows)];
+    auto perm_at = [&](int j) {
+      return j < my_tiles ? perm[(size_t)tile_of(j) * 128 + pw * kEnRows + (lane % kEnRows)] : -1;
+    };
+    auto set_srcs = [&](int my_src) {
 #pragma unroll
       for (int it = 0; it < kIt; ++it) srcs[it] = __shfl_sync(0xffffffffu, my_src, kRPS * it + rsub);
-    }
+    };
+    set_srcs(perm_at(0));
+    int pf_src = perm_at(1);                     // the next tile's rows, requested a tile ahead
+    int hj = 0, hkb = 0;                         // the load head: tile index and K block
     int stage = 0;
     uint32_t phase = 0;
     // raw 16-byte words in registers (converted at store time), so an fp16 block costs the same
     // registers as an fp32 one and kRing blocks of loads can be in flight: 2 for fp32 (128 B per
     // lane and block), 4 for fp16 (64 B per lane and block)
     constexpr int kRing = kXF16 ? 4 : 2;
-    auto load_block = [&](uint4 (&x)[kIt], int kb) {
-      const int k0 = kb * 64 + lc * kEPL;
+    auto load_next = [&](uint4 (&x)[kIt]) {
+      const int k0 = hkb * 64 + lc * kEPL;
 #pragma unroll
       for (int it = 0; it < kIt; ++it) {
         const int src = srcs[it];
@@ -367,6 +417,12 @@ __global__ void __launch_bounds__(kEnThreads, 1)
           }
         }
       }
+      if (++hkb == nkb) {
+        hkb = 0;
+        ++hj;
+        set_srcs(pf_src);
+        pf_src = perm_at(hj + 1);
+      }
     };
     auto store_block = [&](const uint4 (&x)[kIt]) {
       tc::mbar_wait(empty + stage, phase ^ 1);
@@ -374,6 +430,10 @@ __global__ void __launch_bounds__(kEnThreads, 1)
 #pragma unroll
       for (int it = 0; it < kIt; ++it) {
         const int r = pw * kEnRows + kRPS * it + rsub;   // row in the tile
+        if constexpr (kDirect) {   // the fp16 chunk as it is
+          *reinterpret_cast<uint4*>(st + (uint32_t)r * 128u + ((uint32_t)(lc ^ (r & 7)) << 4)) = x[it];
+          continue;
+        }
         float xv[kEPL];
         const uint32_t w4[4] = {x[it].x, x[it].y, x[it].z, x[it].w};
 #pragma unroll
@@ -419,64 +479,88 @@ __global__ void __launch_bounds__(kEnThreads, 1)
       if (++stage == kEnStages) { stage = 0; phase ^= 1; }
     };
     // kRing register buffers with fixed roles (the loop is unrolled by kRing, so no register
-    // copies of in-flight loads): block kb + kRing - 1 is requested before block kb is stored
+    // copies of in-flight loads): block q + kRing - 1 is requested before block q is stored
+    const int total = my_tiles * nkb;
     uint4 xr[kRing][kIt];
 #pragma unroll
     for (int r = 0; r < kRing - 1; ++r)
-      if (r < nkb) load_block(xr[r], r);
-    for (int kb0 = 0; kb0 < nkb; kb0 += kRing) {
+      if (r < total) load_next(xr[r]);
+    for (int q0 = 0; q0 < total; q0 += kRing) {
 #pragma unroll
       for (int r = 0; r < kRing; ++r) {
-        const int kb = kb0 + r;
-        if (kb >= nkb) break;
-        if (kb + kRing - 1 < nkb) load_block(xr[(r + kRing - 1) % kRing], kb + kRing - 1);
+        const int q = q0 + r;
+        if (q >= total) break;
+        if (q + kRing - 1 < total) load_next(xr[(r + kRing - 1) % kRing]);
         store_block(xr[r]);
       }
     }
-    // epilogue: rows of TMEM lane quarter (warp % 4; the hardware ties warp w to lanes
-    // 32*(w%4)..), 32-column blocks split between the two warps of a quarter
+  } else {
+    // epilogue warps: rows of TMEM lane quarter (warp % 4; the hardware ties warp w to lanes
+    // 32*(w%4)..), all column blocks of the tile; the buffer goes back to the MMA warp as soon as
+    // its last column block is in registers
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
-    constexpr int kCB = kD / 32, kCBh = (kCB + 1) / 2;
-    const int cb0 = pw < 4 ? 0 : kCBh, cb1 = pw < 4 ? kCBh : kCB;
-    tc::mbar_wait(acc_full, 0);
-    tc::tc_fence_after();
+    constexpr int kCB = kD / 32;
     const int nbig = nkb < nH ? nkb : nH;
+    for (int j = 0; j < my_tiles; ++j) {
+      const int buf = j % kAB;
+      const int tile = tile_of(j);
+      const int wrow = tile_wrow[2 * tile];
+      tc::mbar_wait(acc_full + buf, (uint32_t)((j / kAB) & 1));
+      tc::tc_fence_after();
 #pragma unroll 1
-    for (int cb = cb0; cb < cb1; ++cb) {
-      float v[32], t[32];
-      const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb * 32u;
-      tc::tmem_ld_32x32b_x32(ta, v);
-      tc::tmem_wait_ld();
-      for (int b = 1; b < nbig; ++b) {
-        tc::tmem_ld_32x32b_x32(ta + (uint32_t)b * (uint32_t)kD, t);
+      for (int cb = 0; cb < kCB; ++cb) {
+        float v[32], t[32];
+        const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * nAcc * kD) + (uint32_t)cb * 32u;
+        tc::tmem_ld_32x32b_x32(ta, v);
         tc::tmem_wait_ld();
+        for (int b = 1; b < nbig; ++b) {
+          tc::tmem_ld_32x32b_x32(ta + (uint32_t)b * (uint32_t)kD, t);
+          tc::tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] += t[j];
-      }
-      tc::tmem_ld_32x32b_x32(ta + (uint32_t)nH * (uint32_t)kD, t);
-      tc::tmem_wait_ld();
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] += t[j];
-      if constexpr (kOut == 2) {
-        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + ((size_t)tile * 128 + row) * kD + cb * 32);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-      } else {
-      uint32_t w[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (kOut == 0) {
-          const __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-          w[j] = *reinterpret_cast<const uint32_t*>(&h2);
-        } else {
-          const __half2 h2 = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
-          w[j] = *reinterpret_cast<const uint32_t*>(&h2);
+          for (int i = 0; i < 32; ++i) v[i] += t[i];
         }
-      }
-      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(out) + ((size_t)tile * 128 + row) * kD + cb * 32);
+        tc::tmem_ld_32x32b_x32(ta + (uint32_t)nH * (uint32_t)kD, t);
+        tc::tmem_wait_ld();
+        if (cb + 1 == kCB) {
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(acc_empty + buf);
+        }
+        if constexpr (kDirect) {
+          const float4* sc = reinterpret_cast<const float4*>(b_scale + wrow + cb * 32);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+          for (int i = 0; i < 8; ++i) {
+            const float4 s4 = __ldg(sc + i);
+            v[4 * i] = fmaf(t[4 * i], 0x1p-11f, v[4 * i]) * s4.x;
+            v[4 * i + 1] = fmaf(t[4 * i + 1], 0x1p-11f, v[4 * i + 1]) * s4.y;
+            v[4 * i + 2] = fmaf(t[4 * i + 2], 0x1p-11f, v[4 * i + 2]) * s4.z;
+            v[4 * i + 3] = fmaf(t[4 * i + 3], 0x1p-11f, v[4 * i + 3]) * s4.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += t[i];
+        }
+        if constexpr (kOut == 2) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + ((size_t)tile * 128 + row) * kD + cb * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        } else {
+          uint32_t w[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (kOut == 0) {
+              const __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+              w[i] = *reinterpret_cast<const uint32_t*>(&h2);
+            } else {
+              const __half2 h2 = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+              w[i] = *reinterpret_cast<const uint32_t*>(&h2);
+            }
+          }
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(out) + ((size_t)tile * 128 + row) * kD + cb * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+        }
       }
     }
   }
@@ -485,16 +569,86 @@ __global__ void __launch_bounds__(kEnThreads, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-template <bool F, int D, int O, int NP>
+template <bool F, int D, int O, int NP, bool DR = false>
 static cudaError_t launch_enc_t(const CUtensorMap* tb, const void* X, int Dx, int Kp, int Nc, const int32_t* perm,
-                                const int32_t* tile_wrow, const int32_t* order, int64_t ntiles, void* out, cudaStream_t s) {
-  auto kern = k_encode_tc<F, D, O, NP>;
-  const size_t smem = encode_smem(D, NP);
+                                const int32_t* tile_wrow, const int32_t* order, int64_t ntiles, void* out, cudaStream_t s,
+                                const float* b_scale = nullptr) {
+  auto kern = k_encode_tc<F, D, O, NP, DR>;
+  const size_t smem = encode_smem(D, DR ? 1 : NP, NP);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // 16-byte row loads need 16-byte aligned rows: D % 4 == 0 (fp32), D % 8 == 0 (fp16)
   const int vec = ((Dx & (F ? 7 : 3)) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) ? 1 : 0;
-  kern<<<(unsigned)ntiles, kEnThreads, smem, s>>>(*tb, X, Dx, Kp, Nc, vec, perm, tile_wrow, order, out);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      nsm = 148;
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, nsm);   // persistent: one CTA per SM
+  kern<<<grid, kEnThreads, smem, s>>>(*tb, X, Dx, Kp, Nc, vec, perm, tile_wrow, order, (int)ntiles, b_scale, out);
+  return cudaGetLastError();
+}
+
+template <int O, int NP>
+static cudaError_t launch_enc_h(int d, const CUtensorMap* tb, const void* X, int Dx, int Kp, int Nc, const int32_t* perm,
+                                const int32_t* tile_wrow, const int32_t* order, int64_t ntiles, void* out,
+                                const float* b_scale, cudaStream_t s) {
+  switch (d) {
+    case 32: return launch_enc_t<true, 32, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale);
+    case 64: return launch_enc_t<true, 64, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale);
+    case 96: return launch_enc_t<true, 96, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale);
+    case 128: return launch_enc_t<true, 128, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale);
+    case 160: return launch_enc_t<true, 160, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale);
+    case 192: return launch_enc_t<true, 192, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// fp16 rows against the scaled fp16 planes of B (tmap_bh over [3][Nc][Kp] fp16, b_scale[Nc]): two
+// planes for bf16 storage (22 bits of b), three (all 24) for fp16 / fp32 output
+cudaError_t launch_encode_h(const CUtensorMap* tmap_bh, const float* b_scale, const void* X, int D, int Kp, int d, int Nc,
+                            const int32_t* perm, const int32_t* tile_wrow, const int32_t* order, int64_t ntiles,
+                            void* out, int out_type, bool planes3, cudaStream_t s) {
+  if (out_type == 2) return launch_enc_h<2, 3>(d, tmap_bh, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, b_scale, s);
+  if (out_type == 1) return launch_enc_h<1, 3>(d, tmap_bh, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, b_scale, s);
+  return planes3 ? launch_enc_h<0, 3>(d, tmap_bh, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, b_scale, s)
+                 : launch_enc_h<0, 2>(d, tmap_bh, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, b_scale, s);
+}
+
+// B [rows, D] fp32 -> out fp16 [3][rows][Kp] (zero padded) and scale[rows] = 2^e_i, with e_i the
+// exponent that puts the row's largest magnitude in [0.5, 1): bs = b 2^-e_i, h = RNE_fp16(bs),
+// r1 = (bs - h) 2^11 (exact), m = RNE_fp16(r1), l = RNE_fp16(r1 - m).  One warp per row.
+__global__ void k_split_h(const float* __restrict__ B, int rows, int D, int Kp, __half* __restrict__ out,
+                          float* __restrict__ scale) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* b = B + (size_t)row * D;
+  float mx = 0.f;
+  for (int k = lane; k < D; k += 32) mx = fmaxf(mx, fabsf(b[k]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int e = 0;
+  if (mx > 0.f && mx < INFINITY) frexpf(mx, &e);
+  e = e < -100 ? -100 : (e > 100 ? 100 : e);
+  const float inv = ldexpf(1.f, -e);
+  if (lane == 0) scale[row] = ldexpf(1.f, e);
+  const size_t plane = (size_t)rows * Kp;
+  __half* o0 = out + (size_t)row * Kp;
+  for (int k = lane; k < Kp; k += 32) {
+    const float bs = k < D ? b[k] * inv : 0.f;
+    const __half h = __float2half_rn(bs);
+    const float r1 = (bs - __half2float(h)) * 2048.f;
+    const __half m = __float2half_rn(r1);
+    const __half l = __float2half_rn(r1 - __half2float(m));
+    o0[k] = h;
+    o0[plane + k] = m;
+    o0[2 * plane + k] = l;
+  }
+}
+
+cudaError_t launch_split_h(const float* B, int rows, int D, int Kp, void* out, float* scale, cudaStream_t s) {
+  k_split_h<<<(rows + 7) / 8, 256, 0, s>>>(B, rows, D, Kp, reinterpret_cast<__half*>(out), scale);
   return cudaGetLastError();
 }
 

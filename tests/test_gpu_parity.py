@@ -166,6 +166,48 @@ def test_g1_encode_shapes(lv, D, d, C, xdt, low, monkeypatch, planes="3"):
     assert np.all(got[~valid] == 0)            # padded rows of a cluster's last tile encode to 0
 
 
+@pytest.mark.parametrize("D,d,C,low,hplanes,direct", [(768, 160, 2, "bf16", "0", "1"), (200, 64, 1, "fp16", "0", "1"),
+                                                       (512, 128, 3, "bf16", "3", "1"), (72, 32, 1, "bf16", "0", "1"),
+                                                       (520, 96, 2, "fp16", "0", "1"), (768, 160, 2, "bf16", "0", "0")])
+def test_g1_encode_fp16_rows_scaled_weights(lv, D, d, C, low, hplanes, direct, monkeypatch):
+    """K6 for fp16 rows (R23): the rows are the fp16 operand as stored, B goes in as
+    row-scaled fp16 planes bs = h + 2^-11 (m + l).  Weights whose rows span 2^-12..2^12 and whose
+    entries span four decades inside a row, rows with entries over three decades (fp16 subnormals
+    included): G1 against the oracle's fp64 B_c x, two planes (bf16 storage) and three; the last
+    case runs the three-bf16-plane kernel (LV_K6_DIRECT=0) on the same inputs."""
+    monkeypatch.setenv("LV_K6_HPLANES", hplanes)
+    monkeypatch.setenv("LV_K6_DIRECT", direct)
+    rng = np.random.default_rng(D * 11 + d)
+    n = 2500
+    X = rng.standard_normal((n, D)) * 10.0 ** rng.uniform(-3, 0, (n, D))
+    X[:, ::7] *= 1e-4                                     # fp16 subnormals
+    X = X.astype(np.float16)
+    B = rng.standard_normal((C, d, D)) / np.sqrt(D) * 10.0 ** rng.uniform(-4, 0, (C, d, D))
+    B *= 2.0 ** rng.integers(-12, 13, (C, d, 1))
+    B[0, 1, :] = 0.0                                      # an all-zero weight row
+    B = B.astype(np.float32)
+    A = (rng.standard_normal((C, d, D)) / np.sqrt(D)).astype(np.float32)
+    assign = rng.integers(0, C, n).astype(np.int32)
+    ix = lv.lv_index_create(D, d, C, low, "fp16", torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    lv.lv_encode_database(ix, torch.from_numpy(X).cuda(), torch.from_numpy(assign).cuda() if C > 1 else None)
+    X_low, perm, offs = lv.lv_index_export(ix)
+    perm = perm.cpu().numpy()
+    valid = perm >= 0
+    X64 = X.astype(np.float64)
+    a = assign if C > 1 else None
+    B1 = B if C > 1 else B[0]
+    xl_ref = O.encode(X64, B1, a, store=low)[perm[valid]]
+    absdot = O.encode(np.abs(X64), np.abs(B1), a)[perm[valid]]
+    got = X_low.float().cpu().numpy().astype(np.float64)
+    assert np.isfinite(got).all()
+    # two fp16 planes carry b to 2^-22 relative: 2^-22 sum|b x| on top of _g1_ok's bound
+    extra = 1.0 if hplanes == "3" or low == "fp16" or direct == "0" else 1.0 + 4.0 / D
+    ok, flips = _g1_ok(got[valid], xl_ref, absdot * extra, low, D)
+    assert ok and flips < 5e-3, flips
+    assert np.all(got[~valid] == 0)
+    assert np.all(got[valid][assign[perm[valid]] == 0, 1] == 0)   # the zero weight row
+
+
 @pytest.mark.parametrize("D,d,C", [(768, 160, 2), (200, 64, 1), (512, 128, 1)])
 def test_g1_encode_two_planes_bf16(lv, D, d, C, monkeypatch):
     """The opt-in two-plane encode (LV_K6_PLANES=2, bf16 storage) within its own bound (R18)."""
