@@ -229,6 +229,7 @@ def roofline_encode(cfg, k6_ms, n_pad, x_bytes):
     fp16 rows go in as they are against row-scaled fp16 planes of B: 2 products (bf16 storage) or 3."""
     pk = _peaks()
     byts = cfg.n * cfg.D * x_bytes + n_pad * cfg.d * 2 + n_pad * 4
+    note = f"n D {x_bytes} + n_pad d 2 + n_pad 4"
     ach = byts / (k6_ms * 1e-3) / 1e9
     prods = 6 if x_bytes == 4 else (2 if cfg.low_dtype == "bf16" else 3)
     tf = prods * 2.0 * cfg.n * cfg.d * cfg.D / (k6_ms * 1e-3) / 1e12
@@ -236,7 +237,7 @@ def roofline_encode(cfg, k6_ms, n_pad, x_bytes):
             "tensor_tflops": round(tf, 1), "tensor_frac": round(tf / pk["bf16"], 4),
             "tensor_products": prods,
             "kernel": "k_encode_tc (K6, one persistent launch)", "launch_ms": round(k6_ms, 4),
-            "algorithmic": f"{byts:.3e} B per launch (n D {x_bytes} + n_pad d 2 + n_pad 4)"}
+            "algorithmic": f"{byts:.3e} B per launch ({note})"}
 
 
 def _tkey(cfg):

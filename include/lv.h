@@ -148,10 +148,13 @@ lv_status lv_index_create(lv_index** out, int32_t D, int32_t d, int32_t C,
  * Layout: rows are stably sorted by cluster (counting sort), each
  * cluster segment is padded to a multiple of 128 rows, so every 128-row tile of X_low
  * belongs to one cluster; perm maps sorted position -> original id (-1 = padding).
- * x_low = RNE(fp32-faithful product) to low_dtype: K6 on tcgen05, X rows and B split into three
- * bf16 planes (24 significant bits), six plane products accumulated in fp32 TMEM (DESIGN.md
- * R18; LV_K6_PLANES=2 opts into a two-plane split for bf16 storage, LV_K6=simt into an fp32
- * CUDA-core GEMM).  X is converted to full_dtype.  lv_encode_timing reports the kernel times.
+ * x_low = RNE(fp32-faithful product) to low_dtype: K6 on tcgen05 (one persistent launch).  fp32
+ * rows: X rows and B split into three bf16 planes (24 significant bits), six plane products
+ * accumulated in fp32 TMEM (R18; LV_K6_PLANES=2 opts into a two-plane split for bf16
+ * storage).  fp16 rows: the row is the fp16 operand as stored, B goes in as row-scaled fp16
+ * planes (two for bf16 storage, three otherwise; R23).  X is converted to full_dtype by
+ * a separate pass (writing X_full from K6's producers was measured slower).
+ * lv_encode_timing reports the kernel times.
  * The caller may free X after the call returns (the call synchronises `stream`).
  * Replaces any previous contents.  Errors: LV_EINVAL, LV_EDATA, LV_ENOMEM, LV_ECUDA.
  */
@@ -307,6 +310,15 @@ lv_status lv_index_info(const lv_index* index, int64_t* n, int64_t* n_pad, int32
  */
 lv_status lv_index_export(const lv_index* index, void* X_low, int32_t* perm, int64_t* offsets,
                           void* stream);
+
+/*
+ * lv_index_export_full — test/debug copy of the full-precision vectors kept for the re-rank
+ * (Alg. 1 line 3): X_full device full_dtype [n, D], original row order (row i = id i).
+ * It equals X bit for bit when the types agree, RNE(x) for fp32 -> fp16, x for fp16 -> fp32.
+ * Not for a flexible index (lv_index_export_xprime).  Synchronises `stream`.
+ * Errors: LV_EINVAL (NULL, not encoded, flexible index), LV_ECUDA.
+ */
+lv_status lv_index_export_full(const lv_index* index, void* X_full, void* stream);
 
 /* Frees every device allocation of the index.  NULL is a no-op. */
 void lv_index_destroy(lv_index* index);

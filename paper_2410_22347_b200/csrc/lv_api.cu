@@ -1448,6 +1448,17 @@ lv_status lv_index_export(const lv_index* ix, void* X_low, int32_t* perm, int64_
   return LV_OK;
 }
 
+lv_status lv_index_export_full(const lv_index* ix, void* X_full, void* stream) {
+  if (!ix || !X_full) return fail(LV_EINVAL, "lv_index_export_full: NULL argument");
+  if (ix->flex) return fail(LV_EINVAL, "lv_index_export_full: a flexible index stores x' (lv_index_export_xprime)");
+  if (ix->n <= 0 || !ix->X_full) return fail(LV_EINVAL, "lv_index_export_full: index not encoded");
+  cudaStream_t s = (cudaStream_t)stream;
+  LV_CUDA(cudaMemcpyAsync(X_full, ix->X_full, (size_t)ix->n * ix->D * (ix->full == LV_F16 ? 2 : 4),
+                          cudaMemcpyDeviceToDevice, s));
+  LV_CUDA(cudaStreamSynchronize(s));
+  return LV_OK;
+}
+
 void lv_index_destroy(lv_index* ix) {
   if (!ix) return;
   free_db(ix);

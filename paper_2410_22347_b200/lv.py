@@ -25,7 +25,7 @@ EXPORTS = ["lv_last_error", "lv_version", "lv_fit_stats", "lv_index_create", "lv
            "lv_index_get_search_dim", "lv_normalize_rows", "lv_kmeans_assign", "lv_kmeans_centre_sums",
            "lv_index_create_flex", "lv_stream_insert", "lv_stream_remove", "lv_stream_observe_queries",
            "lv_stream_stats", "lv_stream_reproject", "lv_index_export_xprime", "lv_project_queries_i8",
-           "lv_index_i8_scales"]
+           "lv_index_i8_scales", "lv_index_export_full"]
 
 
 class LVError(RuntimeError):
@@ -82,6 +82,7 @@ def lib():
             "lv_index_info": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32),
                               ctypes.POINTER(i32), ctypes.POINTER(i32)],
             "lv_index_export": [vp, vp, vp, vp, vp],
+            "lv_index_export_full": [vp, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -405,6 +406,14 @@ def lv_kmeans_centre_sums(X: torch.Tensor, assign: torch.Tensor, C: int):
                                        sums.ctypes.data_as(ctypes.c_void_p), counts.ctypes.data_as(ctypes.c_void_p),
                                        _stream()), "lv_kmeans_centre_sums")
     return sums, counts
+
+
+def lv_index_export_full(index: Index):
+    """X_full [n, D] in the index's full dtype, original row order (CUDA tensor)."""
+    n = index.info()["n"]
+    Xf = torch.empty((n, index.D), dtype=_TORCH_DT[_DT[index.full]], device="cuda")
+    _check(lib().lv_index_export_full(index.h, _ptr(Xf), _stream()), "lv_index_export_full")
+    return Xf
 
 
 def lv_index_export(index: Index):

@@ -208,6 +208,28 @@ def test_g1_encode_fp16_rows_scaled_weights(lv, D, d, C, low, hplanes, direct, m
     assert np.all(got[valid][assign[perm[valid]] == 0, 1] == 0)   # the zero weight row
 
 
+@pytest.mark.parametrize("D,d,C,xdt,full", [(512, 128, 1, "f32", "fp32"), (768, 160, 3, "f16", "fp16"),
+                                             (200, 64, 2, "f32", "fp16"), (328, 96, 2, "f16", "fp32"),
+                                             (204, 32, 1, "f32", "fp32"), (64, 32, 1, "f32", "fp32")])
+def test_encode_full_copy_is_exact(lv, D, d, C, xdt, full):
+    """X_full (the re-rank's full-precision rows, Alg. 1 l.3 P:92-95): bit-identical to X when the
+    types agree, RNE(x) for fp32 -> fp16, x for fp16 -> fp32; original row order whatever the
+    cluster sort does; n not a multiple of 128 and more tiles than one round of the persistent K6."""
+    rng = np.random.default_rng(D + d)
+    n = 128 * 150 + 77
+    X = (rng.standard_normal((n, D)) * 10.0 ** rng.uniform(-3, 1, (n, 1))).astype(np.float32)
+    if xdt == "f16":
+        X = X.astype(np.float16)
+    B = (rng.standard_normal((C, d, D)) / np.sqrt(D)).astype(np.float32)
+    assign = rng.integers(0, C, n).astype(np.int32)
+    ix = lv.lv_index_create(D, d, C, "bf16", full, torch.from_numpy(B).cuda(), torch.from_numpy(B).cuda())
+    lv.lv_encode_database(ix, torch.from_numpy(X).cuda(), torch.from_numpy(assign).cuda() if C > 1 else None)
+    Xf = lv.lv_index_export_full(ix).cpu().numpy()
+    want = X.astype(np.float16 if full == "fp16" else np.float32)
+    bits = np.uint16 if full == "fp16" else np.uint32
+    assert Xf.dtype == want.dtype and np.array_equal(Xf.view(bits), want.view(bits))
+
+
 @pytest.mark.parametrize("D,d,C", [(768, 160, 2), (200, 64, 1), (512, 128, 1)])
 def test_g1_encode_two_planes_bf16(lv, D, d, C, monkeypatch):
     """The opt-in two-plane encode (LV_K6_PLANES=2, bf16 storage) within its own bound (R18)."""

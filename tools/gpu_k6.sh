@@ -1,11 +1,13 @@
-# K6 encode: G1 parity of every encode shape, then timing at the cfg 2 / 3 / 5 shapes
-# (persistent kernel; fp16 rows: direct fp16 operand against scaled fp16 B planes, A/B LV_K6_DIRECT=0)
+# K6 encode: G1 parity of every encode shape + the X_full copy, then timing at the cfg 2 / 3 / 4 / 5
+# shapes; fp16 rows: direct with 2 / 3 planes (LV_K6_HPLANES) or as three bf16 planes (LV_K6_DIRECT=0)
 OUT=gpurun_out/${OUTDIR:-k6}
 mkdir -p $OUT
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "g1_encode or mma_exact" > $OUT/pytest_g1.txt 2>&1; echo "pytest rc=$?"; tail -3 $OUT/pytest_g1.txt
-timeout 300 python tools/prof_encode.py --n 1000000 --D 512 --d 128 --C 1 > $OUT/enc_cfg2.log 2>&1; tail -1 $OUT/enc_cfg2.log
-timeout 300 python tools/prof_encode.py --n 1000000 --D 512 --d 96 --C 16 > $OUT/enc_cfg3.log 2>&1; tail -1 $OUT/enc_cfg3.log
-timeout 300 python tools/prof_encode.py --n 4000000 --D 768 --d 160 --C 32 --xf16 > $OUT/enc_cfg5.log 2>&1; tail -1 $OUT/enc_cfg5.log
-LV_K6_HPLANES=3 timeout 300 python tools/prof_encode.py --n 4000000 --D 768 --d 160 --C 32 --xf16 > $OUT/enc_cfg5_h3.log 2>&1; tail -1 $OUT/enc_cfg5_h3.log
-LV_K6_DIRECT=0 timeout 300 python tools/prof_encode.py --n 4000000 --D 768 --d 160 --C 32 --xf16 > $OUT/enc_cfg5_bf16planes.log 2>&1; tail -1 $OUT/enc_cfg5_bf16planes.log
-timeout 300 python tools/prof_encode.py --n 4000000 --D 200 --d 64 --C 1 --low fp16 > $OUT/enc_cfg4.log 2>&1; tail -1 $OUT/enc_cfg4.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "g1_encode or mma_exact or full_copy" > $OUT/pytest_g1.txt 2>&1; echo "pytest rc=$?"; tail -3 $OUT/pytest_g1.txt
+run() { name=$1; shift; timeout 300 python tools/prof_encode.py "$@" > $OUT/enc_$name.log 2>&1; echo "$name: $(tail -1 $OUT/enc_$name.log)"; }
+C5="--n 4000000 --D 768 --d 160 --C 32 --xf16"
+run cfg2 --n 1000000 --D 512 --d 128 --C 1
+run cfg3 --n 1000000 --D 512 --d 96 --C 16
+run cfg4 --n 4000000 --D 200 --d 64 --C 1 --low fp16
+run cfg5 $C5
+LV_K6_HPLANES=3 run cfg5_h3 $C5
+LV_K6_DIRECT=0 run cfg5_bf16planes $C5

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--low", default="bf16")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--xf16", action="store_true", help="fp16 database rows (cfg 5's canonical type)")
+    ap.add_argument("--full", default=None, help="full dtype kept for the re-rank (default: the rows' type)")
     a = ap.parse_args()
     g = torch.Generator(device="cuda").manual_seed(0)
     X = torch.randn(a.n, a.D, device="cuda", generator=g)
@@ -29,13 +30,15 @@ def main():
     A = torch.randn(a.C, a.d, a.D, device="cuda", generator=g) / a.D ** 0.5
     B = torch.randn(a.C, a.d, a.D, device="cuda", generator=g) / a.D ** 0.5
     assign = torch.randint(0, a.C, (a.n,), device="cuda", dtype=torch.int32, generator=g) if a.C > 1 else None
-    ix = lv.lv_index_create(a.D, a.d, a.C, a.low, "fp32", A, B)
+    a.full = a.full or ("fp16" if a.xf16 else "fp32")
+    ix = lv.lv_index_create(a.D, a.d, a.C, a.low, a.full, A, B)
     for r in range(a.reps):
         lv.lv_encode_database(ix, X, assign)
         t = lv.lv_encode_timing(ix)
         n_pad = ix.info()["n_pad"]
-        gbs = (a.n * a.D * X.element_size() + n_pad * a.d * 2 + n_pad * 4) / (t["encode_K6"] * 1e-3) / 1e9
-        print(f"rep {r}: {t}  K6 {gbs:.0f} GB/s algorithmic", flush=True)
+        byts = a.n * a.D * X.element_size() + n_pad * a.d * 2 + n_pad * 4
+        gbs = byts / (t["encode_K6"] * 1e-3) / 1e9
+        print(f"rep {r}: {t}  K6 {gbs:.0f} GB/s algorithmic ({byts / 1e9:.2f} GB)", flush=True)
 
 
 if __name__ == "__main__":
