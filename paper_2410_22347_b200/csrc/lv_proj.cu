@@ -233,7 +233,10 @@ constexpr int kEnEW = 4;                              // epilogue warps (one per
 constexpr int kEnRows = 128 / kEnPW;                  // tile rows per producer warp
 constexpr int kEnThreads = 64 + 32 * (kEnPW + kEnEW);
 
-__host__ __device__ constexpr int enc_hh(int d) { return (512 / d - 1) < 3 ? (512 / d - 1) : 3; }
+#ifndef LV_K6_NH
+#define LV_K6_NH 3   // hh accumulators per tile, at most (experiment builds: 1 or 2 leave room for a second buffer)
+#endif
+__host__ __device__ constexpr int enc_hh(int d) { return (512 / d - 1) < LV_K6_NH ? (512 / d - 1) : LV_K6_NH; }
 // np planes of the X tile and of the B block per stage
 // nxp planes of the X tile and nbp planes of the B block per stage
 __host__ __device__ constexpr uint32_t enc_stage_bytes(int d, int nxp, int nbp) {

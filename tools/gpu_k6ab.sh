@@ -1,3 +1,4 @@
+# (record of a round-2 experiment: the LV_K6_NOFULL / LV_K6_NOPF code paths it selected were removed after the measurement)
 # K6 A/B on one box: default build with the fused copy / L2 prefetch toggled by environment, and the
 # variant builds k6base (neither compiled in) and k6ring3 (fp32 register ring of 3 blocks, no fused copy)
 OUT=gpurun_out/${OUTDIR:-k6ab}
