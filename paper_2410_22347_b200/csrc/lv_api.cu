@@ -216,7 +216,9 @@ lv_status plan_search(const lv_index* ix, int64_t m, int R, int nsm, Plan* pl) {
   // sampled-threshold path: a sample stage over every stride-th tile records
   // block maxima, a per-query threshold with >= j1 rows above it is selected, one main stage
   // scans everything with it; queries left with < R candidates are repaired exactly.
-  const int stride = (int)env_double("LV_SAMPLE_STRIDE", 16.0);
+  // stride 16; 32 from 32768 tiles (4M rows) on, where the sample stage costs more than the ~35 %
+  // more candidates a half-size sample lets through (cfg 5: 28.3 -> 27.7 ms per search, no repairs)
+  const int stride = (int)env_double("LV_SAMPLE_STRIDE", ntot >= 32768 ? 32.0 : 16.0);
   int nsamp = 0;
   for (auto& sg : seg) nsamp += (sg.second - sg.first + stride - 1) / stride;
   // j1: about j1 * stride database rows score above the j1-th largest sampled block maximum, with a
@@ -744,20 +746,20 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
   if (direct) {
     const int ot = ix->low == LV_I8 ? 2 : (ix->low == LV_BF16 ? 0 : 1);
     LV_CUDA(lv::launch_encode_h(&ix->tmap_bh, ix->b_scale, X, ix->D, ix->Kp, ix->d, ix->C * ix->d, ix->perm, dwrow, dorder,
-                                nt, ix->low == LV_I8 ? (void*)xf : ix->X_low, ot, hplanes >= 3.0, s));
+                                nt, ix->low == LV_I8 ? (void*)xf : ix->X_low, ot, hplanes >= 3.0, s, n));
     if (ix->low == LV_I8) {
       LV_CUDA(lv::launch_i8_db_scales(xf, nt, ix->d, dwrow, C, amax, ix->i8_delta, s));
       LV_CUDA(lv::launch_i8_db_codes(xf, nt, ix->d, dwrow, ix->i8_delta, reinterpret_cast<int8_t*>(ix->X_low), s));
     }
   } else if (ix->low == LV_I8) {   // (ev[0] is unused: the sort is timed by ev[4..7])
     LV_CUDA(lv::launch_encode_tc(&ix->tmap_b, X, x_dtype == LV_F16, ix->D, ix->Kp, ix->d, ix->C * ix->d, ix->perm, dwrow,
-                                 dorder, nt, xf, 2, true, s));
+                                 dorder, nt, xf, 2, true, s, n));
     LV_CUDA(lv::launch_i8_db_scales(xf, nt, ix->d, dwrow, C, amax, ix->i8_delta, s));
     LV_CUDA(lv::launch_i8_db_codes(xf, nt, ix->d, dwrow, ix->i8_delta, reinterpret_cast<int8_t*>(ix->X_low), s));
   } else {
     LV_CUDA(lv::launch_encode_tc(&ix->tmap_b, X, x_dtype == LV_F16, ix->D, ix->Kp, ix->d, ix->C * ix->d, ix->perm, dwrow,
                                  dorder, nt, ix->X_low, ix->low == LV_BF16 ? 0 : 1,
-                                 env_double("LV_K6_PLANES", 3.0) >= 3.0, s));
+                                 env_double("LV_K6_PLANES", 3.0) >= 3.0, s, n));
   }
   LV_CUDA(cudaEventRecord(ev[2], s));
   LV_CUDA(lv::launch_convert(X, x_dtype == LV_F16, ix->X_full, ix->full == LV_F16, n * ix->D, s));

@@ -102,11 +102,11 @@ size_t encode_smem(int d, int nxp, int nbp);
 cudaError_t launch_split_h(const float* B, int rows, int D, int Kp, void* out, float* scale, cudaStream_t s);
 cudaError_t launch_encode_h(const CUtensorMap* tmap_bh, const float* b_scale, const void* X, int D, int Kp, int d, int Nc,
                             const int32_t* perm, const int32_t* tile_wrow, const int32_t* order, int64_t ntiles,
-                            void* out, int out_type, bool planes3, cudaStream_t s);
-// out_type: 0 bf16, 1 fp16, 2 fp32 (the int8 path's unrounded x_low)
+                            void* out, int out_type, bool planes3, cudaStream_t s, int64_t n_rows);
+// out_type: 0 bf16, 1 fp16, 2 fp32 (the int8 path's unrounded x_low); n_rows = rows of X (LV_CHECKS bound)
 cudaError_t launch_encode_tc(const CUtensorMap* tmap_b, const void* X, bool x_f16, int D, int Kp, int d, int Nc,
                              const int32_t* perm, const int32_t* tile_wrow, const int32_t* order, int64_t ntiles,
-                             void* out, int out_type, bool planes3, cudaStream_t s);
+                             void* out, int out_type, bool planes3, cudaStream_t s, int64_t n_rows);
 // int8 reduced vectors (NEXT-4): per (cluster, coordinate) scale delta = max |x| / 127 over the
 // cluster's rows, codes = RNE(x / delta) in [-127, 127]; queries per (query, view): q~ = q' * delta,
 // s = max |q~| / 127, codes = RNE(q~ / s)

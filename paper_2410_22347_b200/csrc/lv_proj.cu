@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kEnThreads, 1)
     k_encode_tc(const __grid_constant__ CUtensorMap tmap_b, const void* __restrict__ X, int D, int Kp, int Nc, int vec,
                 const int32_t* __restrict__ perm, const int32_t* __restrict__ tile_wrow,
                 const int32_t* __restrict__ tile_order, int ntiles, const float* __restrict__ b_scale,
-                void* __restrict__ out) {
+                void* __restrict__ out, int64_t n_rows) {
   static_assert(!kDirect || kXF16, "the direct path needs fp16 rows");
   constexpr int nH = enc_hh(kD);                    // hh accumulators (columns nH*d .. : cross terms)
   constexpr int nAcc = nH + 1;                      // accumulators per tile
@@ -294,7 +294,10 @@ __global__ void __launch_bounds__(kEnThreads, 1)
   const int my_tiles = (ntiles - (int)blockIdx.x + G - 1) / G;
   auto tile_of = [&](int j) {
     const int ti = (int)blockIdx.x + j * G;
-    return tile_order ? tile_order[ti] : ti;
+    LV_CHECK(ti >= 0 && ti < ntiles);
+    const int t = tile_order ? tile_order[ti] : ti;
+    LV_CHECK(t >= 0 && t < ntiles);
+    return t;
   };
 
   if (threadIdx.x == 0) {
@@ -408,6 +411,7 @@ __global__ void __launch_bounds__(kEnThreads, 1)
         const int src = srcs[it];
         x[it] = make_uint4(0u, 0u, 0u, 0u);
         if (src >= 0) {
+          LV_CHECK((int64_t)src < n_rows && k0 >= 0 && k0 < Kp);
           using T = typename std::conditional<kXF16, __half, float>::type;
           const T* row = reinterpret_cast<const T*>(X) + (size_t)src * D;
           if (vec && k0 + kEPL - 1 < D) {
@@ -509,6 +513,7 @@ __global__ void __launch_bounds__(kEnThreads, 1)
       const int buf = j % kAB;
       const int tile = tile_of(j);
       const int wrow = tile_wrow[2 * tile];
+      LV_CHECK(wrow >= 0 && wrow + kD <= Nc);
       tc::mbar_wait(acc_full + buf, (uint32_t)((j / kAB) & 1));
       tc::tc_fence_after();
 #pragma unroll 1
@@ -575,7 +580,7 @@ __global__ void __launch_bounds__(kEnThreads, 1)
 template <bool F, int D, int O, int NP, bool DR = false>
 static cudaError_t launch_enc_t(const CUtensorMap* tb, const void* X, int Dx, int Kp, int Nc, const int32_t* perm,
                                 const int32_t* tile_wrow, const int32_t* order, int64_t ntiles, void* out, cudaStream_t s,
-                                const float* b_scale = nullptr) {
+                                const float* b_scale, int64_t n_rows) {
   auto kern = k_encode_tc<F, D, O, NP, DR>;
   const size_t smem = encode_smem(D, DR ? 1 : NP, NP);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -589,21 +594,21 @@ static cudaError_t launch_enc_t(const CUtensorMap* tb, const void* X, int Dx, in
       nsm = 148;
   }
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, nsm);   // persistent: one CTA per SM
-  kern<<<grid, kEnThreads, smem, s>>>(*tb, X, Dx, Kp, Nc, vec, perm, tile_wrow, order, (int)ntiles, b_scale, out);
+  kern<<<grid, kEnThreads, smem, s>>>(*tb, X, Dx, Kp, Nc, vec, perm, tile_wrow, order, (int)ntiles, b_scale, out, n_rows);
   return cudaGetLastError();
 }
 
 template <int O, int NP>
 static cudaError_t launch_enc_h(int d, const CUtensorMap* tb, const void* X, int Dx, int Kp, int Nc, const int32_t* perm,
                                 const int32_t* tile_wrow, const int32_t* order, int64_t ntiles, void* out,
-                                const float* b_scale, cudaStream_t s) {
+                                const float* b_scale, cudaStream_t s, int64_t n_rows) {
   switch (d) {
-    case 32: return launch_enc_t<true, 32, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale);
-    case 64: return launch_enc_t<true, 64, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale);
-    case 96: return launch_enc_t<true, 96, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale);
-    case 128: return launch_enc_t<true, 128, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale);
-    case 160: return launch_enc_t<true, 160, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale);
-    case 192: return launch_enc_t<true, 192, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale);
+    case 32: return launch_enc_t<true, 32, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale, n_rows);
+    case 64: return launch_enc_t<true, 64, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale, n_rows);
+    case 96: return launch_enc_t<true, 96, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale, n_rows);
+    case 128: return launch_enc_t<true, 128, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale, n_rows);
+    case 160: return launch_enc_t<true, 160, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale, n_rows);
+    case 192: return launch_enc_t<true, 192, O, NP, true>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, b_scale, n_rows);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -612,11 +617,11 @@ static cudaError_t launch_enc_h(int d, const CUtensorMap* tb, const void* X, int
 // planes for bf16 storage (22 bits of b), three (all 24) for fp16 / fp32 output
 cudaError_t launch_encode_h(const CUtensorMap* tmap_bh, const float* b_scale, const void* X, int D, int Kp, int d, int Nc,
                             const int32_t* perm, const int32_t* tile_wrow, const int32_t* order, int64_t ntiles,
-                            void* out, int out_type, bool planes3, cudaStream_t s) {
-  if (out_type == 2) return launch_enc_h<2, 3>(d, tmap_bh, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, b_scale, s);
-  if (out_type == 1) return launch_enc_h<1, 3>(d, tmap_bh, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, b_scale, s);
-  return planes3 ? launch_enc_h<0, 3>(d, tmap_bh, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, b_scale, s)
-                 : launch_enc_h<0, 2>(d, tmap_bh, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, b_scale, s);
+                            void* out, int out_type, bool planes3, cudaStream_t s, int64_t n_rows) {
+  if (out_type == 2) return launch_enc_h<2, 3>(d, tmap_bh, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, b_scale, s, n_rows);
+  if (out_type == 1) return launch_enc_h<1, 3>(d, tmap_bh, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, b_scale, s, n_rows);
+  return planes3 ? launch_enc_h<0, 3>(d, tmap_bh, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, b_scale, s, n_rows)
+                 : launch_enc_h<0, 2>(d, tmap_bh, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, b_scale, s, n_rows);
 }
 
 // B [rows, D] fp32 -> out fp16 [3][rows][Kp] (zero padded) and scale[rows] = 2^e_i, with e_i the
@@ -657,14 +662,15 @@ cudaError_t launch_split_h(const float* B, int rows, int D, int Kp, void* out, f
 
 template <bool F, int O, int NP>
 static cudaError_t launch_enc_d(int d, const CUtensorMap* tb, const void* X, int Dx, int Kp, int Nc, const int32_t* perm,
-                                const int32_t* tile_wrow, const int32_t* order, int64_t ntiles, void* out, cudaStream_t s) {
+                                const int32_t* tile_wrow, const int32_t* order, int64_t ntiles, void* out, cudaStream_t s,
+                                int64_t n_rows) {
   switch (d) {
-    case 32: return launch_enc_t<F, 32, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
-    case 64: return launch_enc_t<F, 64, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
-    case 96: return launch_enc_t<F, 96, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
-    case 128: return launch_enc_t<F, 128, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
-    case 160: return launch_enc_t<F, 160, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
-    case 192: return launch_enc_t<F, 192, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    case 32: return launch_enc_t<F, 32, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, nullptr, n_rows);
+    case 64: return launch_enc_t<F, 64, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, nullptr, n_rows);
+    case 96: return launch_enc_t<F, 96, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, nullptr, n_rows);
+    case 128: return launch_enc_t<F, 128, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, nullptr, n_rows);
+    case 160: return launch_enc_t<F, 160, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, nullptr, n_rows);
+    case 192: return launch_enc_t<F, 192, O, NP>(tb, X, Dx, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, nullptr, n_rows);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -672,18 +678,18 @@ static cudaError_t launch_enc_d(int d, const CUtensorMap* tb, const void* X, int
 // three planes (six products); two planes (three products) for bf16 storage when !planes3
 cudaError_t launch_encode_tc(const CUtensorMap* tmap_b, const void* X, bool x_f16, int D, int Kp, int d, int Nc,
                              const int32_t* perm, const int32_t* tile_wrow, const int32_t* order, int64_t ntiles,
-                             void* out, int out_type, bool planes3, cudaStream_t s) {
+                             void* out, int out_type, bool planes3, cudaStream_t s, int64_t n_rows) {
   if (out_type == 2)
-    return x_f16 ? launch_enc_d<true, 2, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
-                 : launch_enc_d<false, 2, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    return x_f16 ? launch_enc_d<true, 2, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, n_rows)
+                 : launch_enc_d<false, 2, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, n_rows);
   if (out_type == 1)
-    return x_f16 ? launch_enc_d<true, 1, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
-                 : launch_enc_d<false, 1, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    return x_f16 ? launch_enc_d<true, 1, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, n_rows)
+                 : launch_enc_d<false, 1, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, n_rows);
   if (planes3)
-    return x_f16 ? launch_enc_d<true, 0, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
-                 : launch_enc_d<false, 0, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
-  return x_f16 ? launch_enc_d<true, 0, 2>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s)
-               : launch_enc_d<false, 0, 2>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s);
+    return x_f16 ? launch_enc_d<true, 0, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, n_rows)
+                 : launch_enc_d<false, 0, 3>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, n_rows);
+  return x_f16 ? launch_enc_d<true, 0, 2>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, n_rows)
+               : launch_enc_d<false, 0, 2>(d, tmap_b, X, D, Kp, Nc, perm, tile_wrow, order, ntiles, out, s, n_rows);
 }
 
 }  // namespace lv
