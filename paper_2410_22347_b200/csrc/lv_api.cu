@@ -464,7 +464,7 @@ lv_status set_operands(lv_index* ix, const float* A_src, const float* B_src, cud
   }
   LV_CUDA(cudaStreamSynchronize(s));
   lv_status st = make_tmap(&ix->tmap_a, ix->A_planes, 3 * Nc, ix->Kp, 64, true, 128);
-  if (!st && !ix->flex) st = make_tmap(&ix->tmap_b, ix->B_planes, 3 * Nc, ix->Kp, 64, true, ix->d);
+  if (!st && !ix->flex) st = make_tmap(&ix->tmap_b, ix->B_planes, 3 * Nc, ix->Kp, lv::encode_kblock(), true, ix->d);
   if (!st && ix->flex) st = make_tmap(&ix->tmap_b128, ix->B_planes, 3 * Nc, ix->Kp, 64, true, 128);
   return st;
 }
@@ -738,7 +738,7 @@ lv_status lv_encode_database(lv_index* ix, const void* X, lv_dtype x_dtype, int6
         cudaMalloc(&ix->b_scale, sizeof(float) * Nc) != cudaSuccess)
       return fail(LV_ENOMEM, "lv_encode_database: fp16 B planes");
     LV_CUDA(lv::launch_split_h(ix->B, Nc, ix->D, ix->Kp, ix->Bh_planes, ix->b_scale, s));
-    lv_status hs = make_tmap(&ix->tmap_bh, ix->Bh_planes, 3 * (int64_t)Nc, ix->Kp, 64, false, ix->d);
+    lv_status hs = make_tmap(&ix->tmap_bh, ix->Bh_planes, 3 * (int64_t)Nc, ix->Kp, lv::encode_kblock(), false, ix->d);
     if (hs) return hs;
   }
   const double hplanes = env_double("LV_K6_HPLANES", 0.0);   // 0: two for bf16 storage, else three

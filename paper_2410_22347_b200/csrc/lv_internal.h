@@ -97,6 +97,7 @@ cudaError_t launch_proj_tc(const CUtensorMap* tmap_q, const CUtensorMap* tmap_a,
 // CTA i encodes tile order[i] (nullptr: tile i)
 // (three bf16 planes; two for bf16 storage when !planes3)
 size_t encode_smem(int d, int nxp, int nbp);
+int encode_kblock();   // K elements per K6 pipeline stage (32 or 64): the column box of its B-plane tensor maps
 // fp16 rows (R23): the row is its own fp16 operand plane; B as row-scaled fp16 planes
 // (launch_split_h: out fp16 [3][rows][Kp], scale[rows]); two planes for bf16 storage when !planes3
 cudaError_t launch_split_h(const float* B, int rows, int D, int Kp, void* out, float* scale, cudaStream_t s);

@@ -238,17 +238,25 @@ constexpr int kEnThreads = 64 + 32 * (kEnPW + kEnEW);
 #endif
 __host__ __device__ constexpr int enc_hh(int d) { return (512 / d - 1) < LV_K6_NH ? (512 / d - 1) : LV_K6_NH; }
 // np planes of the X tile and of the B block per stage
+// K block of one pipeline stage: 64 elements (128-byte shared-memory rows, SWIZZLE_128B).
+// -DLV_K6_KB=32 (64-byte rows, SWIZZLE_64B; twice the stages: four instead of two for the six-plane
+// d = 128 stages) measured 4-14 % slower, so the pipeline depth is not the bound.
+#ifndef LV_K6_KB
+#define LV_K6_KB 64
+#endif
+constexpr int kEnKB = LV_K6_KB;
+constexpr uint32_t kEnRowB = (uint32_t)kEnKB * 2u;      // bytes per operand row and K block
+static_assert(kEnKB == 32 || kEnKB == 64, "K block of 32 or 64 elements");
+int encode_kblock() { return kEnKB; }
 // nxp planes of the X tile and nbp planes of the B block per stage
 __host__ __device__ constexpr uint32_t enc_stage_bytes(int d, int nxp, int nbp) {
-  return (uint32_t)nxp * 128u * 128u + (uint32_t)nbp * (uint32_t)d * 128u;
+  return (uint32_t)nxp * 128u * kEnRowB + (uint32_t)nbp * (uint32_t)d * kEnRowB;
 }
-// as many stages (<= 4) as fit the 227 KB opt-in limit
+// as many stages (<= 8) as fit the 227 KB opt-in limit
 __host__ __device__ constexpr int enc_stages(int d, int nxp, int nbp) {
-  return 4 * enc_stage_bytes(d, nxp, nbp) + 1280 <= 232448
-             ? 4
-             : (3 * enc_stage_bytes(d, nxp, nbp) + 1280 <= 232448
-                    ? 3
-                    : (2 * enc_stage_bytes(d, nxp, nbp) + 1280 <= 232448 ? 2 : 1));
+  int s = 8;
+  while (s > 1 && (uint32_t)s * enc_stage_bytes(d, nxp, nbp) + 1280u > 232448u) --s;
+  return s;
 }
 size_t encode_smem(int d, int nxp, int nbp) { return enc_stages(d, nxp, nbp) * enc_stage_bytes(d, nxp, nbp) + 1024 + 256; }
 
@@ -273,8 +281,8 @@ __global__ void __launch_bounds__(kEnThreads, 1)
   constexpr int nAcc = nH + 1;                      // accumulators per tile
   constexpr int kAB = 2 * nAcc * kD <= 512 ? 2 : 1; // accumulator buffers (tiles in TMEM at once)
   constexpr int kNXP = kDirect ? 1 : kNP;           // X planes per stage
-  constexpr uint32_t kXPlane = 128u * 128u;         // 128 rows x 64 bf16
-  constexpr uint32_t kBPlane = (uint32_t)kD * 128u; // d rows x 64 bf16
+  constexpr uint32_t kXPlane = 128u * kEnRowB;         // 128 rows x one K block
+  constexpr uint32_t kBPlane = (uint32_t)kD * kEnRowB; // d rows x one K block
   constexpr uint32_t kStage = enc_stage_bytes(kD, kNXP, kNP);
   constexpr int kEnStages = enc_stages(kD, kNXP, kNP);
   constexpr int kProds = kDirect ? kNP : (kNP == 3 ? 6 : 3);
@@ -287,7 +295,7 @@ __global__ void __launch_bounds__(kEnThreads, 1)
   uint64_t* acc_empty = acc_full + 2;               // [kAB] epilogue -> MMA
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkb = Kp / 64;
+  const int nkb = Kp / kEnKB;
   // persistent: this CTA encodes tiles order[blockIdx.x + j * gridDim.x], j < my_tiles (grid <= ntiles);
   // the CTAs in flight together work on one window of the order
   const int G = (int)gridDim.x;
@@ -330,7 +338,7 @@ __global__ void __launch_bounds__(kEnThreads, 1)
           tc::mbar_arrive_expect_tx(full + stage, (uint32_t)kNP * kBPlane);
           uint8_t* st = smem + stage * kStage + (uint32_t)kNXP * kXPlane;
           for (int p = 0; p < kNP; ++p)
-            tc::tma_load_2d(st + p * kBPlane, &tmap_b, full + stage, kb * 64, p * Nc + wrow);
+            tc::tma_load_2d(st + p * kBPlane, &tmap_b, full + stage, kb * kEnKB, p * Nc + wrow);
           if (++stage == kEnStages) { stage = 0; phase ^= 1; }
         }
         wrow = wrow_next;
@@ -355,16 +363,17 @@ __global__ void __launch_bounds__(kEnThreads, 1)
           const uint32_t st = tc::smem_u32(smem + stage * kStage);
           const uint32_t d_big = acc + (uint32_t)(kb % nH) * (uint32_t)kD, d_small = acc + (uint32_t)nH * (uint32_t)kD;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
+          for (int kk = 0; kk < kEnKB / 16; ++kk) {
 #pragma unroll
             for (int pr = 0; pr < kProds; ++pr) {
               const uint32_t xa = st + (kDirect ? 0u : (uint32_t)kPjProd[pr][0]) * kXPlane + (uint32_t)kk * 32u;
               const uint32_t ba = st + (uint32_t)kNXP * kXPlane +
                                   (kDirect ? (uint32_t)pr : (uint32_t)kPjProd[pr][1]) * kBPlane + (uint32_t)kk * 32u;
               if (pr == 0)
-                tc::mma_f16_ss(d_big, tc::make_sdesc(xa, 128), tc::make_sdesc(ba, 128), idesc, (kb >= nH || kk > 0) ? 1u : 0u);
+                tc::mma_f16_ss(d_big, tc::make_sdesc(xa, kEnRowB), tc::make_sdesc(ba, kEnRowB), idesc,
+                               (kb >= nH || kk > 0) ? 1u : 0u);
               else
-                tc::mma_f16_ss(d_small, tc::make_sdesc(xa, 128), tc::make_sdesc(ba, 128), idesc,
+                tc::mma_f16_ss(d_small, tc::make_sdesc(xa, kEnRowB), tc::make_sdesc(ba, kEnRowB), idesc,
                                (kb | kk | (pr - 1)) != 0 ? 1u : 0u);
             }
           }
@@ -382,7 +391,7 @@ __global__ void __launch_bounds__(kEnThreads, 1)
     // ahead of the plane stores (register ring), across tile boundaries, so row reads stay in flight
     // while a tile's accumulators are drained.
     constexpr int kEPL = kXF16 ? 8 : 4;          // elements per lane and step
-    constexpr int kLPR = 64 / kEPL;              // lanes per row
+    constexpr int kLPR = kEnKB / kEPL;           // lanes per row
     constexpr int kRPS = 32 / kLPR;              // rows per step
     constexpr int kIt = kEnRows / kRPS;          // steps per K block
     const int pw = warp - 2;
@@ -403,9 +412,9 @@ __global__ void __launch_bounds__(kEnThreads, 1)
     // raw 16-byte words in registers (converted at store time), so an fp16 block costs the same
     // registers as an fp32 one and kRing blocks of loads can be in flight: 2 for fp32 (128 B per
     // lane and block), 4 for fp16 (64 B per lane and block)
-    constexpr int kRing = kXF16 ? 4 : 2;
+    constexpr int kRing = (kXF16 ? 4 : 2) * (64 / kEnKB);
     auto load_next = [&](uint4 (&x)[kIt]) {
-      const int k0 = hkb * 64 + lc * kEPL;
+      const int k0 = hkb * kEnKB + lc * kEPL;
 #pragma unroll
       for (int it = 0; it < kIt; ++it) {
         const int src = srcs[it];
@@ -431,6 +440,9 @@ __global__ void __launch_bounds__(kEnThreads, 1)
         pf_src = perm_at(hj + 1);
       }
     };
+    // 16-byte chunk c of row r lands at chunk c ^ swz(r): SWIZZLE_128B (address bits 4-6 ^= bits 7-9)
+    // for 128-byte rows, SWIZZLE_64B (bits 4-5 ^= bits 7-8) for 64-byte rows
+    auto swz = [](int r) { return kEnKB == 64 ? (r & 7) : ((r >> 1) & 3); };
     auto store_block = [&](const uint4 (&x)[kIt]) {
       tc::mbar_wait(empty + stage, phase ^ 1);
       uint8_t* st = smem + stage * kStage;
@@ -438,7 +450,7 @@ __global__ void __launch_bounds__(kEnThreads, 1)
       for (int it = 0; it < kIt; ++it) {
         const int r = pw * kEnRows + kRPS * it + rsub;   // row in the tile
         if constexpr (kDirect) {   // the fp16 chunk as it is
-          *reinterpret_cast<uint4*>(st + (uint32_t)r * 128u + ((uint32_t)(lc ^ (r & 7)) << 4)) = x[it];
+          *reinterpret_cast<uint4*>(st + (uint32_t)r * kEnRowB + ((uint32_t)(lc ^ swz(r)) << 4)) = x[it];
           continue;
         }
         float xv[kEPL];
@@ -467,14 +479,13 @@ __global__ void __launch_bounds__(kEnThreads, 1)
           mp[e] = *reinterpret_cast<const uint32_t*>(&m2);
           lp[e] = *reinterpret_cast<const uint32_t*>(&l2);
         }
-        // SWIZZLE_128B: the 16-byte chunk c of row r lands at chunk c ^ (r & 7)
         if constexpr (kEPL == 8) {   // one whole chunk per lane
-          const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(lc ^ (r & 7)) << 4);
+          const uint32_t off = (uint32_t)r * kEnRowB + ((uint32_t)(lc ^ swz(r)) << 4);
           *reinterpret_cast<uint4*>(st + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
           *reinterpret_cast<uint4*>(st + kXPlane + off) = make_uint4(mp[0], mp[1], mp[2], mp[3]);
           if (kNP == 3) *reinterpret_cast<uint4*>(st + 2u * kXPlane + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
         } else {                     // half a chunk per lane
-          const uint32_t off = (uint32_t)r * 128u + ((uint32_t)((lc >> 1) ^ (r & 7)) << 4) + (uint32_t)(lc & 1) * 8u;
+          const uint32_t off = (uint32_t)r * kEnRowB + ((uint32_t)((lc >> 1) ^ swz(r)) << 4) + (uint32_t)(lc & 1) * 8u;
           *reinterpret_cast<uint2*>(st + off) = make_uint2(hp[0], hp[1]);
           *reinterpret_cast<uint2*>(st + kXPlane + off) = make_uint2(mp[0], mp[1]);
           if (kNP == 3) *reinterpret_cast<uint2*>(st + 2u * kXPlane + off) = make_uint2(lp[0], lp[1]);
