@@ -490,6 +490,16 @@ def test_sampled_path_parity(lv):
     assert dbg["path"] == 1
 
 
+def test_sampled_path_stride32(lv, monkeypatch):
+    """The sampled path with every 32nd tile sampled (the default from 32 768 tiles on: the 10M-row
+    configurations), forced here on a database small enough for the whole oracle comparison: j1
+    follows the stride, results stay the exact top-R / top-k."""
+    monkeypatch.setenv("LV_SAMPLE_STRIDE", "32")
+    c, X, Q, A32, B32, assign, R, k = _case(1, n=300_000, m=300, d=64)
+    dbg = _check_search(lv, c, X, Q, A32, B32, assign, R, k, 1, timing=True)
+    assert dbg["path"] == 1
+
+
 def test_sampled_path_repairs(lv, monkeypatch):
     """A deliberately far too high sampled threshold (gamma 0.05: ~64 survivors for R = 256) makes
     every query fail the exactness check; round 1 repairs with the looser bound (about half fail
